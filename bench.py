@@ -1,0 +1,388 @@
+#!/usr/bin/env python3
+"""bench.py — ADP emulated DGEMM on B200 (effective FP64 TFLOP/s, 2mnk/t).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1)
+
+Workload (BASELINE.json configs[1], the headline metric): ADP DGEMM
+8192^3 per GPU, synthetic U(1,2) operands (seeded), column-major NN through
+the C-ABI drop-in adpb200_dgemm with the ADP guardrails live (scan, ESC,
+decision on device): ESC picks s = 7 slices = the 55-bit window, and the
+slice pairs below the target precision are skipped (d_a + d_b <= s). For
+N > 1 the rows of A/C are partitioned (weak scaling: 8192 rows per GPU,
+B replicated) and the ADP decision inputs are max-allreduced over NCCL.
+
+The JSON line also reports native FP64 (cuBLAS via torch.matmul) on the same
+GPU, the ADP overhead against fixed-slice emulation, the U[-1,1] (s = 8) and
+bitwise-reference (all s^2 pairs) variants, the per-stage times, the roofline
+of the dominant kernel and the reference CPU implementation timed on this
+host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+NOMINAL = 8192
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--n", type=int, default=NOMINAL, help="m_per_gpu = n = k")
+    p.add_argument("--quick", action="store_true", help="skip the side measurements")
+    p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu=timestamp,{self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def stop(self, t0, t1):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = [s for (t, s) in self.samples if t0 - 0.2 <= t <= t1 + 0.2] or [s for _, s in self.samples[-5:]]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [x.strip() for x in r.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+def reference_arm(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref,
+    built from /root/reference sources) of adp_gemm, on a bounded sample of the
+    same workload per step, all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from oracle.oracle import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    cores = os.cpu_count() or 1
+    rs, cs, k = 256, 2048, args.n  # a 256 x 2048 block of C, full k: same decision path (min dim 256)
+    rng = np.random.default_rng(1)
+    a = rng.uniform(1.0, 2.0, (rs, k))
+    b = rng.uniform(1.0, 2.0, (k, cs))
+    times = []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            orc.time_call(1, a, b)
+        else:
+            orc.adp_gemm(a, b)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = 2.0 * rs * cs * k / t / 1e12
+    line = {
+        "impl": "reference", "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, 8192^3",
+        "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic U(1,2)",
+        "config": {"workload": f"reference adp_gemm (CPU, OpenMP) on a {rs}x{cs}x{k} block of the "
+                               f"{args.n}^3 ADP DGEMM", "sample_m": rs, "sample_n": cs, "k": k},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                         "sample": f"{rs}x{cs}x{k} block of C per step"},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(A_host_rows, B_host, k):
+    """The reference CPU path on a bounded sample (rank 0, N=1 only)."""
+    from oracle.oracle import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    orc = Oracle(kind)
+    cores = os.cpu_count() or 1
+    a, b = A_host_rows, B_host
+    t0 = time.perf_counter()
+    if kind == "reference":
+        dt = orc.time_call(1, a, b)
+    else:
+        orc.adp_gemm(a, b)
+        dt = time.perf_counter() - t0
+    m, n = a.shape[0], b.shape[1]
+    return {"value": 2.0 * m * n * k / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+            "sample": f"reference adp_gemm on a {m}x{n}x{k} block of the same operands ({dt:.1f} s)"}
+
+
+# ---------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_13778_b200 as adp
+    from paper_2511_13778_b200 import _lib
+    from paper_2511_13778_b200.dist import dgemm_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = k = args.n
+    m = args.n                      # rows per GPU (weak scaling)
+    m_global = m * world
+    handle = adp.Handle.default(dev.index)
+
+    # synthetic operands, column-major storage (torch row-major of the transpose)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    At = torch.rand((k, m), generator=g, device=dev, dtype=torch.float64).add_(1.0)   # A: m x k col-major
+    g.manual_seed(2)
+    Bt = torch.rand((n, k), generator=g, device=dev, dtype=torch.float64).add_(1.0)   # B: k x n col-major
+    Ct = torch.zeros((n, m), device=dev, dtype=torch.float64)                          # C: m x n col-major
+    cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET)
+    trace_buf = torch.zeros(_lib.TRACE_BYTES, dtype=torch.uint8, device=dev)
+
+    def step(config=cfg, A=At, B=Bt, Cm=Ct, trace=None):
+        if world > 1:
+            dgemm_rows("N", "N", m_global, m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
+        else:
+            adp.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def timed(fn, steps, warmup):
+        for _ in range(warmup):
+            fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---- headline: device-resident ADP DGEMM -----------------------------------------
+    step(trace=trace_buf)
+    torch.cuda.synchronize()
+    trace = adp.AdpTrace.from_c(_lib.Trace.from_buffer_copy(trace_buf.cpu().numpy().tobytes()))
+    for _ in range(args.warmup):
+        step()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    time.sleep(1.0)
+    barrier()
+    launches0 = handle.launches()
+    handle.profile_enable(args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    barrier()
+    wall1 = time.time()
+    launches = handle.launches() - launches0
+    clocks = sampler.stop(wall0, wall1)
+    stage = handle.profile_read()
+    handle.profile_enable(0)
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops_global = 2.0 * m_global * n * k
+    value = flops_global / (ms * 1e-3) / 1e12
+
+    # per-stage averages (this rank); for N > 1 each call is two pipeline calls
+    stage_ms = {}
+    if stage:
+        for key in _lib.PROFILE_STAGES:
+            stage_ms[key] = sum(c[key] for c in stage) / args.steps
+    gemm_ms = stage_ms.get("gemm", 0.0)
+
+    pk, pk_kind = peaks()
+    int8_peak = 2.0 * pk["bf16_tflops"]  # dense INT8 = 2x dense BF16 on Blackwell; BF16 is measured
+    pairs = trace.pairs or 0
+    achieved = 2.0 * m * n * k * pairs / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            traffic = json.load(f).get("igemm_dram_bytes_per_launch")
+    except OSError:
+        pass
+    roofline = {"bound": "tensor", "kernel": "igemm_kernel (tcgen05 kind::i8 + fused exact epilogue)",
+                "achieved": achieved, "peak": int8_peak, "unit": "TFLOP/s",
+                "frac": (achieved / int8_peak) if achieved else None, "traffic": traffic,
+                "peak_source": f"2 x bf16_tflops of MEASURED_PEAKS.json ({pk_kind}); int8 ops = 2mnk x pairs",
+                "pairs": pairs}
+
+    extra = {}
+    if not args.quick:
+        # ---- e2e through the C-ABI with host buffers (H2D + dgemm + D2H per step) --------
+        A_h = At.cpu().pin_memory()
+        B_h = Bt.cpu().pin_memory()
+        C_h = torch.empty_like(Ct, device="cpu").pin_memory()
+
+        def e2e_step():
+            At.copy_(A_h, non_blocking=True)
+            Bt.copy_(B_h, non_blocking=True)
+            step()
+            C_h.copy_(Ct, non_blocking=True)
+
+        e2e_ms = timed(e2e_step, max(3, args.steps // 2), 2)
+        extra["e2e"] = {"value": flops_global / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                        "h2d_bytes_per_step": int(At.numel() * 8 + Bt.numel() * 8),
+                        "d2h_bytes_per_step": int(Ct.numel() * 8), "ms_per_step": e2e_ms}
+        # ---- native FP64 (cuBLAS DGEMM through torch) on the same shapes -------------
+        X = At.t()
+        Y = Bt.t()
+        nat_ms = timed(lambda: torch.mm(X, Y), max(3, args.steps // 2), 2)
+        extra["native_fp64"] = {"value": 2.0 * m * n * k / (nat_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                "impl": "cublasDgemm via torch.mm", "ms_per_step": nat_ms}
+        # ---- ADP overhead: guardrails + pinned s=7 vs plain fixed 7-slice emulation ------
+        fixed = adp.AdpConfig(mode=adp.AdpMode.ForceEmulate, forced_slices=7, pair_limit=adp.PAIRS_TARGET)
+        guarded = adp.AdpConfig(mode=adp.AdpMode.ForceEmulate, forced_slices=7, pair_limit=adp.PAIRS_TARGET,
+                                guardrails_forced=True)
+        f_ms = timed(lambda: step(fixed), max(3, args.steps // 2), 2)
+        g_ms = timed(lambda: step(guarded), max(3, args.steps // 2), 2)
+        extra["adp_overhead"] = {"fixed7_ms": f_ms, "guardrails_pinned7_ms": g_ms, "auto_ms": ms,
+                                 "overhead_frac": (g_ms - f_ms) / f_ms}
+        # ---- U[-1,1] operands: coarsened ESC picks s = 8 --------------------------------
+        Au = torch.rand((k, m), generator=g.manual_seed(3 + rank), device=dev, dtype=torch.float64).mul_(2).sub_(1)
+        Bu = torch.rand((n, k), generator=g.manual_seed(4), device=dev, dtype=torch.float64).mul_(2).sub_(1)
+        tr2 = torch.zeros_like(trace_buf)
+        step(cfg, Au, Bu, Ct, tr2)
+        torch.cuda.synchronize()
+        t2 = adp.AdpTrace.from_c(_lib.Trace.from_buffer_copy(tr2.cpu().numpy().tobytes()))
+        u_ms = timed(lambda: step(cfg, Au, Bu, Ct), max(3, args.steps // 2), 2)
+        extra["uniform_pm1"] = {"value": flops_global / (u_ms * 1e-3) / 1e12, "slices": t2.slices,
+                                "esc_bits": t2.esc_bits, "pairs": t2.pairs}
+        # ---- bitwise-reference policy: all s^2 pairs -------------------------------------
+        full_ms = timed(lambda: step(adp.AdpConfig()), max(3, args.steps // 2), 2)
+        extra["full_pairs"] = {"value": flops_global / (full_ms * 1e-3) / 1e12,
+                               "note": "all s^2 slice pairs: output bitwise equal to the reference adp_gemm"}
+        del Au, Bu
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rows = At[:, :256].t().contiguous().cpu().numpy()        # 256 x k block of A (row-major)
+            cols = Bt[:1024, :].t().contiguous().cpu().numpy()       # k x 1024 block of B (row-major)
+            cpu = cpu_baseline(rows, cols, k)
+        except Exception as e:  # noqa: BLE001 — a missing CPU baseline must not sink the GPU number
+            cpu = {"value": None, "error": str(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, 8192^3",
+            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic U(1,2), seeded (torch.Generator)",
+            "config": {"workload": f"ADP DGEMM {m_global}x{n}x{k} column-major NN (8192 rows per GPU), "
+                                   "guardrails live, ESC-chosen s, pairs d_a+d_b<=s",
+                       "m": m_global, "n": n, "k": k, "slices": trace.slices, "esc_bits": trace.esc_bits,
+                       "path": trace.path, "pairs": pairs, "gemm_variant": trace.gemm_variant,
+                       "parallelism": f"row-block x{world}, B replicated, ADP decision max-allreduced (NCCL)",
+                       "l2": "inputs larger than L2 (512 MiB per operand)"},
+            "gpu_launches": launches,
+            "stage_ms": stage_ms,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        line.update(extra)
+        if "native_fp64" in extra:
+            line["speedup_vs_native_fp64"] = value / world / extra["native_fp64"]["value"]
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,196 @@
+/* adpb200 — B200-native (sm_100a) Automatic Dynamic Precision emulated DGEMM.
+ *
+ * C ABI of the drop-in for the reference's ADP GEMM path
+ * (ozadp::adp_gemm, /root/reference/proj/include/ozadp/adp.hpp:84-87,
+ *  impl proj/src/adp.cpp:139-178). Plain pointers and sizes only; every
+ * matrix pointer is a DEVICE pointer; every call is stream-ordered and never
+ * synchronises the host (the ADP decision lives in device memory).
+ *
+ * Return codes mirror the reference CLI's exit codes
+ * (proj/tools/ozadp_main.cpp:235-244): 0 ok, 2 runtime/usage error
+ * (CUDA failure, bad handle), 3 contract violation (the cases where the
+ * reference throws std::invalid_argument: bad config, shape mismatch,
+ * beta != 0 without C). No C++ exception crosses this boundary.
+ */
+#ifndef ADPB200_H
+#define ADPB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADPB200_OK 0
+#define ADPB200_ERR_RUNTIME 2
+#define ADPB200_ERR_CONTRACT 3
+
+/* AdpMode (adp.hpp:16) */
+#define ADPB200_MODE_AUTO 0
+#define ADPB200_MODE_EMULATE 1 /* ForceEmulate: forced_slices */
+#define ADPB200_MODE_NATIVE 2  /* ForceNative */
+
+/* AdpPath / AdpReason (adp.hpp:35-45), same numbering */
+#define ADPB200_PATH_EMULATED 0
+#define ADPB200_PATH_NATIVE 1
+#define ADPB200_REASON_OK 0
+#define ADPB200_REASON_FORCED 1
+#define ADPB200_REASON_EXCEPTIONAL 2
+#define ADPB200_REASON_ESC_TOO_LARGE 3
+#define ADPB200_REASON_TOO_SMALL 4
+#define ADPB200_REASON_COST_MODEL 5
+
+/* Slice-pair policy (igemm.hpp:11-18).
+ *   ADPB200_PAIRS_FULL   : all s^2 pairs — what adp_gemm uses (adp.cpp:172);
+ *                          output bitwise equal to the reference.
+ *   ADPB200_PAIRS_TARGET : pairs with d_a + d_b <= s only, i.e. the pairs
+ *                          below the target precision are skipped (the north
+ *                          star's fast path); = DiagonalTruncated(limit = s).
+ *   >= 0                 : DiagonalTruncated(limit) exactly. */
+#define ADPB200_PAIRS_FULL (-1)
+#define ADPB200_PAIRS_TARGET (-2)
+
+/* Native-fallback flavour. */
+#define ADPB200_FALLBACK_REFERENCE 0 /* ascending-k, separate mul/add: bitwise native_gemm */
+
+typedef struct adpb200_options {
+    /* ozadp::AdpConfig (adp.hpp:18-33), same meaning and defaults */
+    int32_t target_bits;   /* 53 */
+    int32_t max_slices;    /* 18, valid [7, 32] */
+    int64_t esc_block_len; /* 256 */
+    int64_t min_dim;       /* 256 */
+    int32_t mode;          /* ADPB200_MODE_* */
+    int32_t forced_slices; /* 7 */
+    double cost_ratio;     /* 512 */
+    int64_t chunk_len;     /* 65536; validated like GemmParams (igemm.cpp:10-16) */
+    /* extensions */
+    int32_t pair_limit;        /* ADPB200_PAIRS_FULL (default) / _TARGET / >= 0 */
+    int32_t guardrails_forced; /* 1: MODE_EMULATE still runs the scan+ESC+decide
+                                  guardrails (the paper's "ADP forced to 55 bits",
+                                  PAPER.md:734-757); the slice count stays pinned to
+                                  forced_slices, exceptional inputs still fall back */
+    int32_t fallback;          /* ADPB200_FALLBACK_* */
+    int32_t reserved[5];
+} adpb200_options;
+
+/* AdpTrace (adp.hpp:57-67) + decision details; written to DEVICE memory by
+ * the pipeline (stream-ordered). -1 encodes JSON null. */
+typedef struct adpb200_trace {
+    int32_t path;       /* ADPB200_PATH_* */
+    int32_t reason;     /* ADPB200_REASON_* */
+    int32_t esc_bits;   /* -1 when ESC never ran */
+    int32_t slices;     /* -1 unless emulated */
+    int32_t pair_limit; /* largest admitted d_a+d_b actually computed (-1 if native) */
+    int32_t pairs;      /* slice pairs computed per output element */
+    double modeled_cost_ratio;
+    uint64_t nan_a, inf_a, negzero_a; /* ScanReport (fpbits.hpp:78-83) */
+    uint64_t nan_b, inf_b, negzero_b;
+    int64_t m, n, k;
+    int32_t gemm_variant; /* columns per diagonal accumulator of the tcgen05 kernel */
+    int32_t k_chunks;     /* int32 TMEM accumulation chunks along k */
+} adpb200_trace;
+
+typedef struct adpb200_context* adpb200_handle;
+
+void adpb200_default_options(adpb200_options* opt);
+/* AdpConfig::validate (adp.cpp:15-28): 0 or ADPB200_ERR_CONTRACT */
+int adpb200_validate_options(const adpb200_options* opt);
+const char* adpb200_status_string(int status);
+/* last error message of the calling thread (empty when none) */
+const char* adpb200_last_error(void);
+/* library version string; also proves the .so loads without a GPU */
+const char* adpb200_version(void);
+
+int adpb200_create(adpb200_handle* handle, int device);
+int adpb200_destroy(adpb200_handle handle);
+
+/* ---- the drop-in entry points ------------------------------------------------ */
+
+/* BLAS DGEMM: C = alpha*op(A)*op(B) + beta*C, column-major, trans in
+ * {'N','n','T','t','C','c'}. beta == 0 never reads C (BLAS / reference
+ * convention, oracle.cpp:23). trace may be NULL. */
+int adpb200_dgemm(adpb200_handle handle, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                  double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                  double beta, double* C, int64_t ldc, const adpb200_options* opt,
+                  adpb200_trace* trace, void* stream);
+
+/* ozadp::adp_gemm semantics on row-major device buffers (MatrixF64 layout):
+ * out = alpha*A*B + beta*c_in, A m x k, B k x n. c_in may be NULL iff beta == 0
+ * and may alias out. Bitwise equal to the reference for the same options. */
+int adpb200_adp_gemm(adpb200_handle handle, int64_t m, int64_t n, int64_t k, double alpha,
+                     const double* A, const double* B, double beta, const double* c_in,
+                     double* out, const adpb200_options* opt, adpb200_trace* trace,
+                     void* stream);
+
+/* Row-block partition across ranks (one process per GPU): this rank owns rows
+ * [r0, r0+m) of C / op(A) of a global m_global x n x k product and all of
+ * op(B). phase 1 runs the guardrails (scan, exponent stats, ESC) on the local
+ * rows and writes {exceptional, esc_bits} to xchg (device int32[2]); the caller
+ * max-allreduces xchg over the ranks (e.g. ncclAllReduce(ncclMax, ncclInt32)
+ * on the same stream); phase 2 consumes the reduced xchg, decides with the
+ * global dimensions and computes the local rows. Same s and decision on every
+ * rank, so C is bit-identical to the single-GPU result. */
+int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char transa, char transb,
+                       int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                       const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                       const adpb200_options* opt, adpb200_trace* trace, int32_t* xchg, void* stream);
+
+/* ---- stage exports (parity surface; row-major device buffers) --------------- */
+
+/* decide() (adp.cpp:46-96) evaluated on the HOST by the same code the
+ * device decision kernel runs. esc_bits = what the ESC provider returns.
+ * out[0..4] = path, reason, slices, provider_called, esc_bits(-1 if not). */
+int adpb200_decide_host(int exc_a, int exc_b, int64_t m, int64_t n, int64_t k, int esc_bits,
+                        const adpb200_options* opt, int32_t out[5], double* cost_ratio);
+
+/* scan_matrix (fpbits.cpp:5-24): counts[0..2] nan/inf/-0 (device uint64) */
+int adpb200_scan(adpb200_handle handle, const double* A, int64_t count, uint64_t* counts,
+                 void* stream);
+/* block_exponent_stats (fpbits.cpp:26-73); orient 0 ByRow, 1 ByCol.
+ * max_exp/min_exp: lines x blocks int32, line_max: lines int32 (device).
+ * exceptional (device int32, may be NULL) is set to 1 on Inf/NaN. */
+int adpb200_block_stats(adpb200_handle handle, const double* A, int64_t rows, int64_t cols,
+                        int orient, int64_t block_len, int32_t* max_exp, int32_t* min_exp,
+                        int32_t* line_max, int32_t* exceptional, void* stream);
+/* esc_coarsened (esc.cpp:89-117) on device stats; out[0..2] = esc_bits,
+ * window_bits, slices_required (device int32). */
+int adpb200_esc_coarsened(adpb200_handle handle, const int32_t* a_max, const int32_t* a_min,
+                          const int32_t* a_line, const int32_t* b_max, const int32_t* b_min,
+                          const int32_t* b_line, int64_t m, int64_t n, int64_t blocks,
+                          int target_bits, int32_t* out, void* stream);
+/* decompose (slicing.cpp:90-136): digits = slices planes of lines x len int8
+ * (plane-major, each plane line-major = K-major), scale_exp: lines int32. */
+int adpb200_decompose(adpb200_handle handle, const double* A, int64_t rows, int64_t cols,
+                      int orient, int slices, int8_t* digits, int32_t* scale_exp, void* stream);
+/* slice_pair_mm (igemm.cpp:38-97) computed on the tcgen05 INT8 tensor cores:
+ * acc = m x n x (2s-1) int64 element-major (DiagonalAccumulators layout,
+ * igemm.hpp:34-47). pair_limit: ADPB200_PAIRS_FULL or >= 0. */
+int adpb200_slice_pair_mm(adpb200_handle handle, const double* A, const double* B, int64_t m,
+                          int64_t n, int64_t k, int slices, int pair_limit, int64_t* acc,
+                          void* stream);
+/* emulated_gemm (igemm.cpp:129-137): fixed slices, no guardrails. */
+int adpb200_emulated_gemm(adpb200_handle handle, const double* A, const double* B, int64_t m,
+                          int64_t n, int64_t k, double alpha, double beta, const double* c_in,
+                          double* out, int slices, int pair_limit, void* stream);
+/* native_gemm (oracle.cpp:7-28): ascending-k, separate multiply/add. */
+int adpb200_native_gemm(adpb200_handle handle, const double* A, const double* B, int64_t m,
+                        int64_t n, int64_t k, double alpha, double beta, const double* c_in,
+                        double* out, void* stream);
+
+/* Kernel launches issued by this handle since creation (all kernels are ours). */
+uint64_t adpb200_launch_count(adpb200_handle handle);
+
+/* Stage timing with CUDA events on the caller's stream (no effect on results).
+ * Stages: 0 scan+stats (K1), 1 ESC (K2), 2 decide, 3 slicing (K3),
+ * 4 tcgen05 GEMM + epilogue (K4/K5), 5 native fallback (K6).
+ * enable(max_calls) records the next max_calls pipeline calls (0 disables);
+ * read() waits for them and returns ms[call*6 + stage], then resets. */
+#define ADPB200_PROFILE_STAGES 6
+int adpb200_profile_enable(adpb200_handle handle, int max_calls);
+int adpb200_profile_read(adpb200_handle handle, float* ms, int* ncalls);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADPB200_H */

@@ -1,0 +1,300 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" wrappers over the UNMODIFIED reference library (ozadp, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/). These
+// let the Python tests and the C restatement (oracle/adp_oracle.c) be pinned
+// against the reference's own code on the same inputs. Only tests/, smoke()
+// and bench.py's cpu_baseline / --impl reference leg may load the result.
+//
+// Every wrapper takes plain pointers + sizes, row-major like ozadp::MatrixF64
+// (proj/include/ozadp/matrix.hpp:12-43), and returns 0 on success, 3 for
+// std::invalid_argument / std::domain_error (the CLI's contract exit code,
+// proj/tools/ozadp_main.cpp:235-244) and 2 for anything else.
+#include <chrono>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+
+#include "ozadp/adp.hpp"
+#include "ozadp/esc.hpp"
+#include "ozadp/fpbits.hpp"
+#include "ozadp/grading.hpp"
+#include "ozadp/igemm.hpp"
+#include "ozadp/oracle.hpp"
+#include "ozadp/slicing.hpp"
+#include "ozadp/threads.hpp"
+
+using namespace ozadp;
+
+namespace {
+
+MatrixF64 wrap(const double* p, std::size_t r, std::size_t c) {
+    MatrixF64 m(r, c);
+    if (r * c) std::memcpy(m.data(), p, r * c * sizeof(double));
+    return m;
+}
+
+void unwrap(const MatrixF64& m, double* out) {
+    if (m.size()) std::memcpy(out, m.data(), m.size() * sizeof(double));
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return 3;
+    } catch (const std::domain_error&) {
+        return 3;
+    } catch (...) {
+        return 2;
+    }
+}
+
+GemmParams params(double alpha, double beta, int slices, long long chunk, int limit) {
+    GemmParams p;
+    p.alpha = alpha;
+    p.beta = beta;
+    p.slices = slices;
+    p.chunk_len = std::size_t(chunk);
+    if (limit >= 0) {
+        p.policy.kind = PairPolicy::Kind::DiagonalTruncated;
+        p.policy.limit = limit;
+    }
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ozref_set_threads(int n) {
+    set_thread_cap(n);
+    return 0;
+}
+
+int ozref_gen_uniform_rect(long long rows, long long cols, unsigned long long seed, double lo,
+                           double hi, double* out) {
+    return guarded([&] { unwrap(gen_uniform_rect(rows, cols, seed, lo, hi), out); });
+}
+
+int ozref_gen_test2(long long n, int b, unsigned long long seed, double* lhs, double* rhs) {
+    return guarded([&] {
+        Test2Instance t = gen_test2(std::size_t(n), b, seed);
+        unwrap(t.lhs, lhs);
+        unwrap(t.rhs, rhs);
+    });
+}
+
+// counts[0..2] = nan, inf, -0; returns has_exceptional in *exc.
+int ozref_scan(const double* a, long long rows, long long cols, unsigned long long* counts,
+               int* exc) {
+    return guarded([&] {
+        ScanReport r = scan_matrix(wrap(a, rows, cols));
+        counts[0] = r.nan_count;
+        counts[1] = r.inf_count;
+        counts[2] = r.negzero_count;
+        *exc = r.has_exceptional ? 1 : 0;
+    });
+}
+
+// orient 0 = ByRow, 1 = ByCol. Outputs sized lines*blocks, lines*blocks, lines.
+int ozref_block_stats(const double* a, long long rows, long long cols, int orient,
+                      long long block_len, int* max_exp, int* min_exp, int* line_max) {
+    return guarded([&] {
+        BlockStats s = block_exponent_stats(wrap(a, rows, cols),
+                                            orient ? Orientation::ByCol : Orientation::ByRow,
+                                            std::size_t(block_len));
+        if (!s.max_exp.empty()) std::memcpy(max_exp, s.max_exp.data(), s.max_exp.size() * 4);
+        if (!s.min_exp.empty()) std::memcpy(min_exp, s.min_exp.data(), s.min_exp.size() * 4);
+        if (!s.line_max.empty()) std::memcpy(line_max, s.line_max.data(), s.line_max.size() * 4);
+    });
+}
+
+// out[0..2] = esc_bits, window_bits, slices_required.
+int ozref_esc_coarsened(const double* a, const double* b, long long m, long long n, long long k,
+                        long long block_len, int target_bits, int* out) {
+    return guarded([&] {
+        BlockStats sa = block_exponent_stats(wrap(a, m, k), Orientation::ByRow, block_len);
+        BlockStats sb = block_exponent_stats(wrap(b, k, n), Orientation::ByCol, block_len);
+        EscReport r = esc_coarsened(sa, sb, target_bits);
+        out[0] = r.esc_bits;
+        out[1] = r.window_bits;
+        out[2] = r.slices_required;
+    });
+}
+
+int ozref_esc_exact(const double* a, const double* b, long long m, long long n, long long k,
+                    int target_bits, int* out) {
+    return guarded([&] {
+        EscReport r = esc_exact(wrap(a, m, k), wrap(b, k, n), target_bits);
+        out[0] = r.esc_bits;
+        out[1] = r.window_bits;
+        out[2] = r.slices_required;
+    });
+}
+
+int ozref_required_slices(int target_bits, int esc_bits, int* out) {
+    return guarded([&] { *out = required_slices(target_bits, esc_bits); });
+}
+
+// digits: slices planes of lines*len int8; scale: lines int32.
+int ozref_decompose(const double* a, long long rows, long long cols, int orient, int slices,
+                    signed char* digits, int* scale) {
+    return guarded([&] {
+        SlicedMatrix s = decompose(wrap(a, rows, cols),
+                                   orient ? Orientation::ByCol : Orientation::ByRow, slices);
+        if (!s.digits.empty()) std::memcpy(digits, s.digits.data(), s.digits.size());
+        if (!s.scale_exp.empty()) std::memcpy(scale, s.scale_exp.data(), s.scale_exp.size() * 4);
+    });
+}
+
+// acc: m*n*(2s-1) int64, element-major (igemm.hpp:34-47). limit < 0 = Full.
+int ozref_slice_pair_mm(const double* a, const double* b, long long m, long long n, long long k,
+                        int slices, long long chunk, int limit, long long* acc) {
+    return guarded([&] {
+        GemmParams p = params(1.0, 0.0, slices, chunk, limit);
+        SlicedMatrix sa = decompose(wrap(a, m, k), Orientation::ByRow, slices);
+        SlicedMatrix sb = decompose(wrap(b, k, n), Orientation::ByCol, slices);
+        DiagonalAccumulators d = slice_pair_mm(sa, sb, p);
+        if (!d.acc.empty()) std::memcpy(acc, d.acc.data(), d.acc.size() * 8);
+    });
+}
+
+int ozref_emulated_gemm(const double* a, const double* b, long long m, long long n, long long k,
+                        double alpha, double beta, const double* c, int slices, long long chunk,
+                        int limit, double* out) {
+    return guarded([&] {
+        GemmParams p = params(alpha, beta, slices, chunk, limit);
+        MatrixF64 cm;
+        if (c) cm = wrap(c, m, n);
+        unwrap(emulated_gemm(wrap(a, m, k), wrap(b, k, n), p, c ? &cm : nullptr), out);
+    });
+}
+
+int ozref_native_gemm(const double* a, const double* b, long long m, long long n, long long k,
+                      double alpha, double beta, const double* c, double* out) {
+    return guarded([&] {
+        MatrixF64 cm;
+        if (c) cm = wrap(c, m, n);
+        unwrap(native_gemm(wrap(a, m, k), wrap(b, k, n), alpha, beta, c ? &cm : nullptr), out);
+    });
+}
+
+int ozref_exact_gemm(const double* a, const double* b, long long m, long long n, long long k,
+                     double* out) {
+    return guarded([&] { unwrap(exact_gemm(wrap(a, m, k), wrap(b, k, n)), out); });
+}
+
+// cfg_i: target_bits, esc_block_len, max_slices, min_dim, mode(0 auto,1 emulate,2 native),
+//        forced_slices, chunk_len;  cfg_d: cost_ratio.
+// trace_i: path(0 emulated,1 native), reason(0..5 as AdpReason), esc_bits(-1 null),
+//          slices(-1 null), m, n, k, scan counts a[3], b[3].
+// trace_d: modeled_cost_ratio.  json: optional buffer for AdpTrace::to_json.
+int ozref_adp_gemm(const double* a, const double* b, long long m, long long n, long long k,
+                   double alpha, double beta, const double* c, const long long* cfg_i,
+                   const double* cfg_d, double* out, long long* trace_i, double* trace_d,
+                   char* json, int json_cap) {
+    return guarded([&] {
+        AdpConfig cfg;
+        cfg.target_bits = int(cfg_i[0]);
+        cfg.esc_block_len = std::size_t(cfg_i[1]);
+        cfg.max_slices = int(cfg_i[2]);
+        cfg.min_dim = std::size_t(cfg_i[3]);
+        cfg.mode = cfg_i[4] == 1 ? AdpMode::ForceEmulate
+                                 : (cfg_i[4] == 2 ? AdpMode::ForceNative : AdpMode::Auto);
+        cfg.forced_slices = int(cfg_i[5]);
+        cfg.chunk_len = std::size_t(cfg_i[6]);
+        cfg.cost_ratio = cfg_d[0];
+        MatrixF64 cm;
+        if (c) cm = wrap(c, m, n);
+        auto [res, tr] = adp_gemm(wrap(a, m, k), wrap(b, k, n), alpha, beta, c ? &cm : nullptr, cfg);
+        unwrap(res, out);
+        trace_i[0] = tr.decision.path == AdpPath::Emulated ? 0 : 1;
+        trace_i[1] = int(tr.decision.reason);
+        trace_i[2] = tr.decision.esc ? tr.decision.esc->esc_bits : -1;
+        trace_i[3] = tr.decision.path == AdpPath::Emulated ? tr.decision.slices : -1;
+        trace_i[4] = (long long)tr.m;
+        trace_i[5] = (long long)tr.n;
+        trace_i[6] = (long long)tr.k;
+        trace_i[7] = (long long)tr.scan_a.nan_count;
+        trace_i[8] = (long long)tr.scan_a.inf_count;
+        trace_i[9] = (long long)tr.scan_a.negzero_count;
+        trace_i[10] = (long long)tr.scan_b.nan_count;
+        trace_i[11] = (long long)tr.scan_b.inf_count;
+        trace_i[12] = (long long)tr.scan_b.negzero_count;
+        trace_d[0] = tr.decision.modeled_cost_ratio;
+        if (json && json_cap > 0) {
+            std::string js = tr.to_json();
+            std::strncpy(json, js.c_str(), std::size_t(json_cap) - 1);
+            json[json_cap - 1] = 0;
+        }
+    });
+}
+
+// decide() with a fake ESC provider (the reference's own test seam,
+// proj/tests/test_adp.cpp:38-54). scan flags: exc_a, exc_b. esc_in = esc_bits
+// the fake reports (slices_required = required_slices(target, esc_in)).
+// out_i: path, reason, slices, provider_calls, esc_bits(-1 none); out_d: cost ratio.
+int ozref_decide(int exc_a, int exc_b, long long m, long long n, long long k, int esc_in,
+                 const long long* cfg_i, const double* cfg_d, int* out_i, double* out_d) {
+    return guarded([&] {
+        AdpConfig cfg;
+        cfg.target_bits = int(cfg_i[0]);
+        cfg.esc_block_len = std::size_t(cfg_i[1]);
+        cfg.max_slices = int(cfg_i[2]);
+        cfg.min_dim = std::size_t(cfg_i[3]);
+        cfg.mode = cfg_i[4] == 1 ? AdpMode::ForceEmulate
+                                 : (cfg_i[4] == 2 ? AdpMode::ForceNative : AdpMode::Auto);
+        cfg.forced_slices = int(cfg_i[5]);
+        cfg.chunk_len = std::size_t(cfg_i[6]);
+        cfg.cost_ratio = cfg_d[0];
+        ScanReport sa, sb;
+        sa.has_exceptional = exc_a != 0;
+        sb.has_exceptional = exc_b != 0;
+        int calls = 0;
+        auto provider = [&]() {
+            ++calls;
+            EscReport r;
+            r.esc_bits = esc_in;
+            r.window_bits = cfg.target_bits + esc_in;
+            r.slices_required = required_slices(cfg.target_bits, esc_in);
+            r.method = EscMethod::Coarsened;
+            return r;
+        };
+        AdpDecision d = decide(sa, sb, m, n, k, provider, cfg);
+        out_i[0] = d.path == AdpPath::Emulated ? 0 : 1;
+        out_i[1] = int(d.reason);
+        out_i[2] = d.slices;
+        out_i[3] = calls;
+        out_i[4] = d.esc ? d.esc->esc_bits : -1;
+        out_d[0] = d.modeled_cost_ratio;
+    });
+}
+
+// Wall-clock seconds of one emulated_gemm / adp_gemm / native_gemm call on
+// row-major host buffers (bench.py's reference arm). which: 0 emulated(slices,
+// Full), 1 adp auto (default AdpConfig), 2 native.
+double ozref_time_call(int which, const double* a, const double* b, long long m, long long n,
+                       long long k, int slices, double* out) {
+    MatrixF64 am = wrap(a, m, k), bm = wrap(b, k, n);
+    auto t0 = std::chrono::steady_clock::now();
+    MatrixF64 r;
+    try {
+        if (which == 0)
+            r = emulated_gemm(am, bm, params(1.0, 0.0, slices, 65536, -1));
+        else if (which == 1)
+            r = adp_gemm(am, bm).first;
+        else
+            r = native_gemm(am, bm);
+    } catch (...) {
+        return -1.0;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    if (out) unwrap(r, out);
+    return std::chrono::duration<double>(t1 - t0).count();
+}
+
+}  // extern "C"

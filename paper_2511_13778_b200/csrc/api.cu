@@ -1,0 +1,647 @@
+// C ABI of adpb200 (include/adpb200.h): handle + workspace management and the
+// stream-ordered orchestration of the ADP pipeline
+//
+//   K1 stats(A), K1 stats(B) -> K2 ESC -> decide -> K3 slice(A), K3 slice(B)
+//   -> K4/K5 tcgen05 GEMM variants (predicated on the device plan)
+//   -> K6 native fallback (predicated on the device plan)
+//
+// mirroring ozadp::adp_gemm (proj/src/adp.cpp:139-178). Nothing here reads
+// device memory back: the decision is made and consumed on the GPU.
+#include <cuda.h>
+#include <stddef.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+
+#include "adpb200.h"
+#include "igemm.cuh"
+
+using namespace adpb200;
+
+// Stage timing (adpb200_profile_*): CUDA events recorded on the caller's
+// stream around each pipeline stage, read back on request.
+constexpr int kStages = ADPB200_PROFILE_STAGES;
+
+struct adpb200_context {
+    int device = 0;
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
+    uint64_t launches = 0;
+    int prof_cap = 0, prof_calls = 0;
+    cudaEvent_t* prof_ev = nullptr;  // [cap][kStages][2]
+    bool prof_used[kStages] = {};
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct StageTimer {
+    adpb200_context* h;
+    cudaStream_t st;
+    int call;
+    StageTimer(adpb200_context* h_, cudaStream_t s) : h(h_), st(s), call(-1) {
+        if (h->prof_ev && h->prof_calls < h->prof_cap) call = h->prof_calls++;
+    }
+    void begin(int stage) {
+        if (call >= 0) cudaEventRecord(h->prof_ev[(call * kStages + stage) * 2 + 0], st);
+    }
+    void end(int stage) {
+        if (call >= 0) {
+            cudaEventRecord(h->prof_ev[(call * kStages + stage) * 2 + 1], st);
+            h->prof_used[stage] = true;
+        }
+    }
+};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return ADPB200_OK;
+    return fail(ADPB200_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Carve-up of the workspace for one call.
+struct Layout {
+    size_t plan, stats_a_max, stats_a_min, line_a, stats_b_max, stats_b_min, line_b, scale_a, scale_b, planes_a,
+        planes_b, partial, scratch, total;
+    int64_t blocks, pitch;
+    int cap;
+};
+
+Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) {
+    Layout L{};
+    L.blocks = K == 0 ? 0 : (K + block_len - 1) / block_len;
+    L.pitch = (int64_t)align_up((size_t)std::max<int64_t>(K, 1), 16);
+    L.cap = cap;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + std::max<size_t>(bytes, 1), 1024);
+        return o;
+    };
+    L.plan = take(sizeof(Plan));
+    L.stats_a_max = take(size_t(M) * L.blocks * 4);
+    L.stats_a_min = take(size_t(M) * L.blocks * 4);
+    L.line_a = take(size_t(M) * 4);
+    L.stats_b_max = take(size_t(N) * L.blocks * 4);
+    L.stats_b_min = take(size_t(N) * L.blocks * 4);
+    L.line_b = take(size_t(N) * 4);
+    L.scale_a = take(size_t(M) * 4);
+    L.scale_b = take(size_t(N) * 4);
+    L.planes_a = take(cap ? size_t(cap) * M * L.pitch : 0);
+    L.planes_b = take(cap ? size_t(cap) * N * L.pitch : 0);
+    L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
+    L.scratch = take(4096);
+    L.total = off;
+    return L;
+}
+
+int ensure_ws(adpb200_context* h, size_t bytes, cudaStream_t st) {
+    if (h->ws_bytes >= bytes) return ADPB200_OK;
+    if (h->ws) {
+        int rc = cuda_check(cudaFreeAsync(h->ws, st), "cudaFreeAsync(workspace)");
+        if (rc) return rc;
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+    }
+    size_t want = align_up(bytes, size_t(1) << 21);
+    int rc = cuda_check(cudaMallocAsync(&h->ws, want, st), "cudaMallocAsync(workspace)");
+    if (rc) return rc;
+    h->ws_bytes = want;
+    return ADPB200_OK;
+}
+
+template <class T>
+T* at(adpb200_context* h, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(h->ws) + off);
+}
+
+bool trans_ok(char t) { return t == 'N' || t == 'n' || t == 'T' || t == 't' || t == 'C' || t == 'c'; }
+bool is_n(char t) { return t == 'N' || t == 'n'; }
+
+// Everything the pipeline needs about one call, in the internal orientation.
+struct Problem {
+    int64_t M, N, K;       // internal: C(i,j) = sum_l A(i,l) B(l,j)
+    LineView a, b;         // A-lines (M x K), B-lines (N x K)
+    double alpha, beta;
+    const double* c_in;
+    int64_t ldc_in;
+    double* c_out;
+    int64_t ldc;
+    int64_t tm, tn, tk;    // dimensions reported in the trace / seen by decide()
+    int swap_ab;           // internal A-lines are the user's B (row-major facade)
+};
+
+// Largest number of slice planes that can take part for these options.
+int plane_cap(const adpb200_options& o, int fixed_slices, int fixed_limit) {
+    int s_max;
+    int limit;
+    if (fixed_slices > 0) {
+        s_max = fixed_slices;
+        limit = fixed_limit;
+    } else {
+        if (o.mode == ADPB200_MODE_NATIVE) return 0;
+        s_max = o.mode == ADPB200_MODE_EMULATE ? o.forced_slices : o.max_slices;
+        limit = o.pair_limit;
+    }
+    int cap = s_max;
+    if (limit >= 0) cap = std::min(cap, limit + 1);
+    return cap;
+}
+
+// phase 0: the whole pipeline. Multi-GPU row partition: phase 1 runs the
+// guardrails (K1, K2) on this rank's rows and exports {exc, esc_raw} to xchg
+// (device int32[2]) for a max-allreduce across ranks; phase 2 imports the
+// reduced values and runs decide + slicing + GEMM/fallback, so every rank
+// takes the same decision with the same s (C bit-identical for any rank count).
+int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace,
+                 cudaStream_t st, int fixed_slices, int fixed_limit, int64_t* dump, int ndump, int phase = 0,
+                 int32_t* xchg = nullptr) {
+    const int cap = plane_cap(o, fixed_slices, fixed_limit);
+    const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
+    int rc = ensure_ws(h, Lw.total, st);
+    if (rc) return rc;
+    uint64_t* nl = &h->launches;
+    StageTimer tm(h, st);
+    Plan* plan = at<Plan>(h, Lw.plan);
+    if (phase != 2) {
+        rc = cuda_check(cudaMemsetAsync(plan, 0, sizeof(Plan), st), "cudaMemsetAsync(plan)");
+        if (rc) return rc;
+    }
+    int32_t* amax = at<int32_t>(h, Lw.stats_a_max);
+    int32_t* amin = at<int32_t>(h, Lw.stats_a_min);
+    int32_t* aline = at<int32_t>(h, Lw.line_a);
+    int32_t* bmax = at<int32_t>(h, Lw.stats_b_max);
+    int32_t* bmin = at<int32_t>(h, Lw.stats_b_min);
+    int32_t* bline = at<int32_t>(h, Lw.line_b);
+    const bool native_only = fixed_slices <= 0 && o.mode == ADPB200_MODE_NATIVE;
+
+    // K1: scans + exponent statistics + line maxima (skipped by ForceNative,
+    // which never inspects the data: adp.cpp:150-155)
+    tm.begin(0);
+    if (!native_only && phase != 2) {
+        if (P.M > 0)
+            launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, st, nl);
+        if (P.N > 0)
+            launch_stats(P.b, o.esc_block_len, bmax, bmin, bline, plan->counts + 3, &plan->exc, 2, st, nl);
+    }
+    tm.end(0);
+    // K2: ESC, only where decide() can reach it (mode auto, or the forced
+    // guardrail extension) and past the size gate; the kernel itself exits on
+    // exceptional inputs.
+    const int64_t mn = std::min(std::min(P.tm, P.tn), P.tk);
+    const bool esc_expected =
+        fixed_slices <= 0 &&
+        (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
+        mn >= o.min_dim && P.M > 0 && P.N > 0 && P.K > 0;
+    tm.begin(1);
+    if (esc_expected && phase != 2)
+        launch_esc(amax, amin, aline, bmax, bmin, bline, P.M, P.N, Lw.blocks, plan, &plan->esc_raw, &plan->esc_ran,
+                   st, nl);
+    tm.end(1);
+    static_assert(offsetof(Plan, esc_raw) == offsetof(Plan, exc) + 4, "xchg layout");
+    if (phase == 1) {
+        rc = cuda_check(cudaMemcpyAsync(xchg, &plan->exc, 8, cudaMemcpyDeviceToDevice, st), "export xchg");
+        return rc ? rc : cuda_check(cudaGetLastError(), "launch");
+    }
+    if (phase == 2) {
+        rc = cuda_check(cudaMemcpyAsync(&plan->exc, xchg, 8, cudaMemcpyDeviceToDevice, st), "import xchg");
+        if (rc) return rc;
+    }
+    // decision
+    tm.begin(2);
+    if (fixed_slices > 0) launch_set_plan(plan, fixed_slices, fixed_limit, P.K, st, nl);
+    else launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, P.swap_ab, trace, st, nl);
+    tm.end(2);
+
+    if (P.M == 0 || P.N == 0) return cuda_check(cudaGetLastError(), "launch");
+
+    if (P.K > 0 && cap > 0) {
+        // K3: slicing (predicated on the plan)
+        int8_t* pa = at<int8_t>(h, Lw.planes_a);
+        int8_t* pb = at<int8_t>(h, Lw.planes_b);
+        int32_t* sa = at<int32_t>(h, Lw.scale_a);
+        int32_t* sb = at<int32_t>(h, Lw.scale_b);
+        tm.begin(3);
+        launch_slice(P.a, aline, pa, Lw.pitch, Lw.pitch * P.M, sa, plan, fixed_slices, cap, st, nl);
+        launch_slice(P.b, bline, pb, Lw.pitch, Lw.pitch * P.N, sb, plan, fixed_slices, cap, st, nl);
+        tm.end(3);
+        // K4/K5: one launch per GEMM variant; exactly one does work
+        CUtensorMap ta;
+        if (!make_plane_map(&ta, pa, P.M, P.K, Lw.pitch, cap, 128))
+            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for A planes");
+        GemmArgs g{};
+        g.plan = plan;
+        g.M = P.M;
+        g.N = P.N;
+        g.K = P.K;
+        g.scale_a = sa;
+        g.scale_b = sb;
+        g.alpha = P.alpha;
+        g.beta = P.beta;
+        g.c_out = P.c_out;
+        g.ldc = P.ldc;
+        g.c_in = P.c_in;
+        g.ldc_in = P.ldc_in;
+        g.partial = at<uint64_t>(h, Lw.partial);
+        g.dump = dump;
+        g.ndump = ndump;
+        int variants[3] = {64, 32, 16};
+        tm.begin(4);
+        for (int nb : variants) {
+            if (fixed_slices > 0) {  // the host knows the variant
+                Plan hp{};
+                fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
+                if (hp.variant != nb) continue;
+            }
+            CUtensorMap tb;
+            if (!make_plane_map(&tb, pb, P.N, P.K, Lw.pitch, cap, nb))
+                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for B planes");
+            if (launch_igemm(nb, ta, tb, g, st, nl)) return fail(ADPB200_ERR_RUNTIME, "bad GEMM variant");
+        }
+        tm.end(4);
+    }
+    // K6: native fallback (predicated); with k == 0 both paths reduce to
+    // alpha*(+0.0) (+ beta*C), so it runs unconditionally.
+    if (!dump && (fixed_slices <= 0 || P.K == 0)) {
+        const Plan* pred = P.K == 0 ? nullptr : plan;
+        tm.begin(5);
+        launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, pred, st, nl);
+        tm.end(5);
+    }
+    return cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// Row-major product out = alpha*A*B + beta*c_in (MatrixF64 layout) expressed
+// in the internal orientation by the exact operand swap C^T = B^T A^T:
+// internal A-lines = columns of B, B-lines = rows of A, out(i,j) = C[j][i].
+Problem rowmajor_problem(int64_t m, int64_t n, int64_t k, double alpha, const double* A, const double* B,
+                         double beta, const double* c_in, double* out) {
+    Problem P{};
+    P.M = n;
+    P.N = m;
+    P.K = k;
+    P.a = LineView{B, n, k, 1, n};   // column j of B: B[l*n + j]
+    P.b = LineView{A, m, k, k, 1};   // row i of A: A[i*k + l]
+    P.alpha = alpha;
+    P.beta = beta;
+    P.c_in = c_in;
+    P.ldc_in = n;
+    P.c_out = out;
+    P.ldc = n;
+    P.tm = m;
+    P.tn = n;
+    P.tk = k;
+    P.swap_ab = 1;
+    return P;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* adpb200_version(void) { return "adpb200 0.1 (sm_100a, tcgen05 kind::i8)"; }
+
+const char* adpb200_last_error(void) { return g_last_error.c_str(); }
+
+const char* adpb200_status_string(int status) {
+    switch (status) {
+        case ADPB200_OK: return "ok";
+        case ADPB200_ERR_RUNTIME: return "runtime error";
+        case ADPB200_ERR_CONTRACT: return "contract violation";
+    }
+    return "unknown";
+}
+
+void adpb200_default_options(adpb200_options* o) {
+    memset(o, 0, sizeof(*o));
+    o->target_bits = 53;
+    o->max_slices = 18;
+    o->esc_block_len = 256;
+    o->min_dim = 256;
+    o->mode = ADPB200_MODE_AUTO;
+    o->forced_slices = 7;
+    o->cost_ratio = 512.0;
+    o->chunk_len = 65536;
+    o->pair_limit = ADPB200_PAIRS_FULL;
+    o->guardrails_forced = 0;
+    o->fallback = ADPB200_FALLBACK_REFERENCE;
+}
+
+int adpb200_validate_options(const adpb200_options* o) {
+    if (!o) return fail(ADPB200_ERR_CONTRACT, "options: null");
+    // AdpConfig::validate (adp.cpp:15-28)
+    if (!(o->target_bits >= 1 && o->target_bits <= 1024)) return fail(3, "AdpConfig: target_bits out of range");
+    if (!(o->esc_block_len >= 1)) return fail(3, "AdpConfig: esc_block_len must be positive");
+    if (!(o->max_slices >= 7 && o->max_slices <= kMaxSlices)) return fail(3, "AdpConfig: max_slices must be in [7, 32]");
+    if (!(o->min_dim >= 1)) return fail(3, "AdpConfig: min_dim must be positive");
+    if (!(o->cost_ratio > 0.0)) return fail(3, "AdpConfig: cost_ratio must be positive");
+    if (o->mode < 0 || o->mode > 2) return fail(3, "AdpConfig: bad mode");
+    if (o->mode == ADPB200_MODE_EMULATE && !(o->forced_slices >= 1 && o->forced_slices <= kMaxSlices))
+        return fail(3, "AdpConfig: forced_slices out of range");
+    // GemmParams::validate (igemm.cpp:10-16)
+    if (!(o->chunk_len >= 1 && o->chunk_len * 16384 < (int64_t(1) << 31)))
+        return fail(3, "GemmParams: chunk_len * 16384 must stay below 2^31");
+    if (o->pair_limit < ADPB200_PAIRS_TARGET) return fail(3, "options: bad pair_limit");
+    if (o->fallback != ADPB200_FALLBACK_REFERENCE) return fail(3, "options: bad fallback");
+    return ADPB200_OK;
+}
+
+int adpb200_create(adpb200_handle* handle, int device) {
+    if (!handle) return fail(ADPB200_ERR_CONTRACT, "create: null handle pointer");
+    int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (rc) return rc;
+    auto* h = new adpb200_context();
+    h->device = device;
+    *handle = h;
+    return ADPB200_OK;
+}
+
+int adpb200_destroy(adpb200_handle h) {
+    if (!h) return ADPB200_OK;
+    adpb200_profile_enable(h, 0);
+    if (h->ws) {
+        cudaDeviceSynchronize();
+        cudaFree(h->ws);
+    }
+    delete h;
+    return ADPB200_OK;
+}
+
+uint64_t adpb200_launch_count(adpb200_handle h) { return h ? h->launches : 0; }
+
+int adpb200_profile_enable(adpb200_handle h, int max_calls) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "profile: null handle");
+    if (h->prof_ev) {
+        for (int i = 0; i < h->prof_cap * kStages * 2; ++i) cudaEventDestroy(h->prof_ev[i]);
+        delete[] h->prof_ev;
+        h->prof_ev = nullptr;
+    }
+    h->prof_cap = max_calls > 0 ? max_calls : 0;
+    h->prof_calls = 0;
+    for (int s = 0; s < kStages; ++s) h->prof_used[s] = false;
+    if (!h->prof_cap) return ADPB200_OK;
+    h->prof_ev = new cudaEvent_t[size_t(h->prof_cap) * kStages * 2];
+    for (int i = 0; i < h->prof_cap * kStages * 2; ++i) {
+        int rc = cuda_check(cudaEventCreate(&h->prof_ev[i]), "cudaEventCreate");
+        if (rc) return rc;
+    }
+    return ADPB200_OK;
+}
+
+int adpb200_profile_read(adpb200_handle h, float* ms, int* ncalls) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "profile: null handle");
+    *ncalls = h->prof_calls;
+    for (int c = 0; c < h->prof_calls; ++c)
+        for (int s = 0; s < kStages; ++s) {
+            float v = 0.f;
+            if (h->prof_used[s]) {
+                cudaEvent_t e1 = h->prof_ev[(c * kStages + s) * 2 + 1];
+                if (cudaEventSynchronize(e1) != cudaSuccess ||
+                    cudaEventElapsedTime(&v, h->prof_ev[(c * kStages + s) * 2 + 0], e1) != cudaSuccess)
+                    v = 0.f;
+            }
+            ms[c * kStages + s] = v;
+        }
+    cudaGetLastError();  // stages that were not recorded in a call leave benign errors
+    h->prof_calls = 0;
+    return ADPB200_OK;
+}
+
+int adpb200_decide_host(int exc_a, int exc_b, int64_t m, int64_t n, int64_t k, int esc_bits,
+                        const adpb200_options* opt, int32_t out[5], double* cost_ratio) {
+    int rc = adpb200_validate_options(opt);
+    if (rc) return rc;
+    DecideInput in{exc_a, exc_b, m, n, k, esc_bits};
+    DecideOutput d = decide(in, *opt);
+    out[0] = d.path;
+    out[1] = d.reason;
+    out[2] = d.slices;
+    out[3] = d.provider_called;
+    out[4] = d.esc_bits;
+    if (cost_ratio) *cost_ratio = d.cost;
+    return ADPB200_OK;
+}
+
+int adpb200_dgemm(adpb200_handle h, char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                  const adpb200_options* opt, adpb200_trace* trace, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm: null handle");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (!trans_ok(transa) || !trans_ok(transb)) return fail(3, "dgemm: bad trans flag");
+    if (m < 0 || n < 0 || k < 0) return fail(3, "dgemm: negative dimension");
+    const int64_t arows = is_n(transa) ? m : k, brows = is_n(transb) ? k : n;
+    if (lda < std::max<int64_t>(1, arows)) return fail(3, "dgemm: lda too small");
+    if (ldb < std::max<int64_t>(1, brows)) return fail(3, "dgemm: ldb too small");
+    if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
+    if (m > 0 && n > 0 && !C) return fail(3, "dgemm: C is null");
+    if (m > 0 && k > 0 && !A) return fail(3, "dgemm: A is null");
+    if (n > 0 && k > 0 && !B) return fail(3, "dgemm: B is null");
+    Problem P{};
+    P.M = m;
+    P.N = n;
+    P.K = k;
+    // A-lines = rows of op(A); B-lines = columns of op(B) (column-major storage)
+    P.a = is_n(transa) ? LineView{A, m, k, 1, lda} : LineView{A, m, k, lda, 1};
+    P.b = is_n(transb) ? LineView{B, n, k, ldb, 1} : LineView{B, n, k, 1, ldb};
+    P.alpha = alpha;
+    P.beta = beta;
+    P.c_in = C;
+    P.ldc_in = ldc;
+    P.c_out = C;
+    P.ldc = ldc;
+    P.tm = m;
+    P.tn = n;
+    P.tk = k;
+    cudaSetDevice(h->device);
+    return run_pipeline(h, P, o, trace, static_cast<cudaStream_t>(stream), 0, 0, nullptr, 0);
+}
+
+int adpb200_dgemm_rows(adpb200_handle h, int phase, int64_t m_global, char transa, char transb, int64_t m,
+                       int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double beta, double* C, int64_t ldc, const adpb200_options* opt, adpb200_trace* trace,
+                       int32_t* xchg, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_rows: null handle");
+    if (phase != 1 && phase != 2) return fail(3, "dgemm_rows: phase must be 1 or 2");
+    if (!xchg) return fail(3, "dgemm_rows: xchg is null");
+    if (m_global < m) return fail(3, "dgemm_rows: m_global < m");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (!trans_ok(transa) || !trans_ok(transb)) return fail(3, "dgemm: bad trans flag");
+    if (m < 0 || n < 0 || k < 0) return fail(3, "dgemm: negative dimension");
+    const int64_t arows = is_n(transa) ? m : k, brows = is_n(transb) ? k : n;
+    if (lda < std::max<int64_t>(1, arows)) return fail(3, "dgemm: lda too small");
+    if (ldb < std::max<int64_t>(1, brows)) return fail(3, "dgemm: ldb too small");
+    if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
+    Problem P{};
+    P.M = m;
+    P.N = n;
+    P.K = k;
+    P.a = is_n(transa) ? LineView{A, m, k, 1, lda} : LineView{A, m, k, lda, 1};
+    P.b = is_n(transb) ? LineView{B, n, k, ldb, 1} : LineView{B, n, k, 1, ldb};
+    P.alpha = alpha;
+    P.beta = beta;
+    P.c_in = C;
+    P.ldc_in = ldc;
+    P.c_out = C;
+    P.ldc = ldc;
+    P.tm = m_global;
+    P.tn = n;
+    P.tk = k;
+    cudaSetDevice(h->device);
+    return run_pipeline(h, P, o, trace, static_cast<cudaStream_t>(stream), 0, 0, nullptr, 0, phase, xchg);
+}
+
+int adpb200_adp_gemm(adpb200_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                     const double* B, double beta, const double* c_in, double* out, const adpb200_options* opt,
+                     adpb200_trace* trace, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "adp_gemm: null handle");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (m < 0 || n < 0 || k < 0) return fail(3, "adp_gemm: negative dimension");
+    if (beta != 0.0 && !c_in) return fail(3, "adp_gemm: beta != 0 requires C");  // adp.cpp:143
+    if (m > 0 && n > 0 && !out) return fail(3, "adp_gemm: out is null");
+    Problem P = rowmajor_problem(m, n, k, alpha, A, B, beta, c_in, out);
+    cudaSetDevice(h->device);
+    return run_pipeline(h, P, o, trace, static_cast<cudaStream_t>(stream), 0, 0, nullptr, 0);
+}
+
+int adpb200_emulated_gemm(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,
+                          double alpha, double beta, const double* c_in, double* out, int slices, int pair_limit,
+                          void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "emulated_gemm: null handle");
+    if (slices < 1 || slices > kMaxSlices) return fail(3, "GemmParams: slices must be in [1, 32]");
+    if (pair_limit < ADPB200_PAIRS_TARGET) return fail(3, "emulated_gemm: bad pair_limit");
+    if (beta != 0.0 && !c_in) return fail(3, "recompose: beta != 0 needs C");
+    adpb200_options o;
+    adpb200_default_options(&o);
+    Problem P = rowmajor_problem(m, n, k, alpha, A, B, beta, c_in, out);
+    cudaSetDevice(h->device);
+    return run_pipeline(h, P, o, nullptr, static_cast<cudaStream_t>(stream), slices, pair_limit, nullptr, 0);
+}
+
+int adpb200_slice_pair_mm(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,
+                          int slices, int pair_limit, int64_t* acc, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "slice_pair_mm: null handle");
+    if (slices < 1 || slices > kMaxSlices) return fail(3, "GemmParams: slices must be in [1, 32]");
+    if (pair_limit < ADPB200_PAIRS_FULL) return fail(3, "slice_pair_mm: pair_limit must be FULL or >= 0");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int ndump = 2 * slices - 1;
+    if (m > 0 && n > 0) {
+        int rc = cuda_check(cudaMemsetAsync(acc, 0, size_t(m) * n * ndump * 8, st), "cudaMemsetAsync(acc)");
+        if (rc) return rc;
+    }
+    adpb200_options o;
+    adpb200_default_options(&o);
+    // internal orientation = reference orientation: A-lines rows of A, B-lines columns of B
+    Problem P{};
+    P.M = m;
+    P.N = n;
+    P.K = k;
+    P.a = LineView{A, m, k, k, 1};
+    P.b = LineView{B, n, k, 1, n};
+    P.tm = m;
+    P.tn = n;
+    P.tk = k;
+    cudaSetDevice(h->device);
+    return run_pipeline(h, P, o, nullptr, st, slices, pair_limit, acc, ndump);
+}
+
+int adpb200_native_gemm(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,
+                        double alpha, double beta, const double* c_in, double* out, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "native_gemm: null handle");
+    if (beta != 0.0 && !c_in) return fail(3, "native_gemm: beta != 0 needs C");
+    Problem P = rowmajor_problem(m, n, k, alpha, A, B, beta, c_in, out);
+    cudaSetDevice(h->device);
+    launch_native(P.a, P.b, alpha, beta, c_in, P.ldc_in, out, P.ldc, nullptr, static_cast<cudaStream_t>(stream),
+                  &h->launches);
+    return cuda_check(cudaGetLastError(), "native_gemm launch");
+}
+
+int adpb200_scan(adpb200_handle h, const double* A, int64_t count, uint64_t* counts, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "scan: null handle");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = cuda_check(cudaMemsetAsync(counts, 0, 3 * sizeof(uint64_t), st), "cudaMemsetAsync(counts)");
+    if (rc) return rc;
+    launch_scan(A, count, reinterpret_cast<unsigned long long*>(counts), nullptr, st, &h->launches);
+    return cuda_check(cudaGetLastError(), "scan launch");
+}
+
+int adpb200_block_stats(adpb200_handle h, const double* A, int64_t rows, int64_t cols, int orient,
+                        int64_t block_len, int32_t* max_exp, int32_t* min_exp, int32_t* line_max,
+                        int32_t* exceptional, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "block_stats: null handle");
+    if (block_len < 1) return fail(3, "block_exponent_stats: block_len must be >= 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = ensure_ws(h, 4096, st);
+    if (rc) return rc;
+    unsigned long long* counts = at<unsigned long long>(h, 0);
+    rc = cuda_check(cudaMemsetAsync(counts, 0, 64, st), "cudaMemsetAsync");
+    if (rc) return rc;
+    if (exceptional) {
+        rc = cuda_check(cudaMemsetAsync(exceptional, 0, 4, st), "cudaMemsetAsync");
+        if (rc) return rc;
+    }
+    LineView v = orient ? LineView{A, cols, rows, 1, cols} : LineView{A, rows, cols, cols, 1};
+    if (v.lines > 0) launch_stats(v, block_len, max_exp, min_exp, line_max, counts, exceptional, 1, st, &h->launches);
+    return cuda_check(cudaGetLastError(), "block_stats launch");
+}
+
+int adpb200_esc_coarsened(adpb200_handle h, const int32_t* a_max, const int32_t* a_min, const int32_t* a_line,
+                          const int32_t* b_max, const int32_t* b_min, const int32_t* b_line, int64_t m, int64_t n,
+                          int64_t blocks, int target_bits, int32_t* out, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "esc: null handle");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int rc = cuda_check(cudaMemsetAsync(out, 0, 3 * sizeof(int32_t), st), "cudaMemsetAsync(out)");
+    if (rc) return rc;
+    launch_esc(a_max, a_min, a_line, b_max, b_min, b_line, m, n, blocks, nullptr, out, nullptr, st, &h->launches);
+    launch_esc_finish(out, target_bits, st, &h->launches);
+    return cuda_check(cudaGetLastError(), "esc launch");
+}
+
+int adpb200_decompose(adpb200_handle h, const double* A, int64_t rows, int64_t cols, int orient, int slices,
+                      int8_t* digits, int32_t* scale_exp, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "decompose: null handle");
+    if (slices < 1 || slices > kMaxSlices) return fail(3, "decompose: slices must be in [1, 32]");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    LineView v = orient ? LineView{A, cols, rows, 1, cols} : LineView{A, rows, cols, cols, 1};
+    if (v.lines == 0) return ADPB200_OK;
+    const int64_t blocks = v.len == 0 ? 0 : (v.len + 255) / 256;
+    size_t need = 1024 + align_up(size_t(v.lines) * blocks * 4 + 64, 1024) * 2 + align_up(size_t(v.lines) * 4, 1024);
+    int rc = ensure_ws(h, need, st);
+    if (rc) return rc;
+    unsigned long long* counts = at<unsigned long long>(h, 0);
+    int32_t* bmax = at<int32_t>(h, 1024);
+    int32_t* bmin = at<int32_t>(h, 1024 + align_up(size_t(v.lines) * blocks * 4 + 64, 1024));
+    int32_t* lmax = at<int32_t>(h, 1024 + 2 * align_up(size_t(v.lines) * blocks * 4 + 64, 1024));
+    rc = cuda_check(cudaMemsetAsync(counts, 0, 64, st), "cudaMemsetAsync");
+    if (rc) return rc;
+    launch_stats(v, 256, bmax, bmin, lmax, counts, nullptr, 1, st, &h->launches);
+    if (v.len > 0) {
+        launch_slice(v, lmax, digits, v.len, v.len * v.lines, scale_exp, nullptr, slices, slices, st, &h->launches);
+    } else {
+        rc = cuda_check(cudaMemsetAsync(scale_exp, 0, size_t(v.lines) * 4, st), "cudaMemsetAsync(scale)");
+        if (rc) return rc;
+    }
+    return cuda_check(cudaGetLastError(), "decompose launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,34 @@
+#pragma once
+#include "common.cuh"
+
+namespace adpb200 {
+
+int num_sms();
+
+// K1: fused Inf/NaN/-0 counts + per-(line, block) exponent max/min + line max.
+void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
+                  unsigned long long* counts, int32_t* exc_flag, int exc_bit, cudaStream_t st,
+                  uint64_t* nlaunch);
+void launch_scan(const double* a, int64_t count, unsigned long long* counts, int32_t* exc, cudaStream_t st,
+                 uint64_t* nlaunch);
+// K2: coarsened ESC (atomicMax into esc_out, which must start at 0).
+void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
+                const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
+                int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch);
+void launch_esc_finish(int32_t* out, int target_bits, cudaStream_t st, uint64_t* nlaunch);
+// swap_ab: the internal operands are the user's B (A-lines) and A (B-lines).
+void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
+                   int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch);
+
+// Stage exports: a fixed emulation plan (slices s, pair policy) without guardrails.
+void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t st, uint64_t* nlaunch);
+
+// K3: slicing into K-major int8 planes [slice][line][pitch] + per-line scale E.
+// slices_fixed > 0 overrides the plan (stage exports); otherwise the kernel
+// reads s / nsl from the plan and does nothing unless the path is emulated.
+// plane_cap bounds nsl (sizes the transpose tile of the strided variant).
+void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
+                  int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
+                  uint64_t* nlaunch);
+
+}  // namespace adpb200

@@ -1,0 +1,451 @@
+// K4 + K5: the slice-pair products on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, int32 accumulators in TMEM, TMA-fed 32-byte-swizzled
+// shared-memory stages) fused with the exact FP64 reconstruction epilogue.
+//
+//   slice_pair_mm   proj/src/igemm.cpp:38-97   (per-diagonal integer sums)
+//   recompose       proj/src/igemm.cpp:99-127  (exact combine, one RNE, alpha/beta)
+//   WideInt / round_mag_to_double   proj/include/ozadp/exactsum.hpp:50-158
+//
+// Structure (one persistent CTA per SM, 8 warps):
+//   warp 0      TMA producer: per 32-byte k-block, nsl A slice tiles
+//               (128 rows) + nsl B slice tiles (NB rows) into one stage.
+//   warp 1      MMA issuer (one thread). TMEM holds one int32 accumulator of
+//               128 x NB per diagonal D = d_a + d_b (D <= L, (L+1)*NB <= 512
+//               columns). B slices are stacked along N inside a stage, so the
+//               products of A slice d_a with B slices d_b..d_b+c-1 are ONE
+//               instruction of N = c*NB whose output columns land exactly on
+//               diagonals d_a+d_b..d_a+d_b+c-1.
+//   warp 2      TMEM allocator.
+//   warps 4-7   epilogue: tcgen05.ld the L+1 diagonals of a column batch,
+//               fold them exactly (Horner in NL 64-bit limbs), round once to
+//               FP64 (RNE, gradual underflow, overflow -> Inf), apply the
+//               row/column scales 2^(E_a+E_b-14-8L) and alpha/beta, store C.
+// k longer than the int32-safe chunk (see int32_kchunk) is split into chunks;
+// each chunk's exact partial sum is kept in a limb workspace in HBM.
+#include <cuda.h>
+
+#include "igemm.cuh"
+#include "tc.cuh"
+
+namespace adpb200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBM = 128;      // rows of a tile (UMMA M)
+constexpr int kKB = 32;       // bytes of k per stage (one UMMA K step for int8)
+constexpr int kMaxStages = 8;
+constexpr int kGroupM = 16;   // raster: 16 m-tiles per group
+
+template <int NB>
+struct Cfg {
+    static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
+    static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : 5);  // exact fold limbs
+    static constexpr int kCW = 64 / kNDMax >= 2 ? 64 / kNDMax : 2;  // columns per TMEM load batch
+    static constexpr int kMaxGroup = 256 / NB;                 // B slices per MMA (N <= 256)
+};
+
+struct alignas(8) SmemHeader {
+    uint64_t full[kMaxStages];
+    uint64_t empty[kMaxStages];
+    uint64_t tmem_full;
+    uint64_t tmem_empty;
+    uint32_t tmem_slot;
+};
+
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t tiles_m, int64_t tiles_n, int64_t& mt,
+                                            int64_t& nt) {
+    const int64_t group = kGroupM * tiles_n;
+    const int64_t g = tile / group;
+    const int64_t first_m = g * kGroupM;
+    const int64_t gm = tiles_m - first_m < kGroupM ? tiles_m - first_m : kGroupM;
+    const int64_t local = tile - g * group;
+    mt = first_m + local % gm;
+    nt = local / gm;
+}
+
+// ---- exact fold + single rounding --------------------------------------------------
+template <int NL>
+__device__ __forceinline__ void limbs_shl8_add(uint64_t (&S)[NL], int64_t x) {
+#pragma unroll
+    for (int i = NL - 1; i >= 1; --i) S[i] = (S[i] << 8) | (S[i - 1] >> 56);
+    S[0] <<= 8;
+    uint64_t ext = x < 0 ? ~0ull : 0ull;
+    uint64_t prev = S[0];
+    S[0] += uint64_t(x);
+    uint64_t carry = S[0] < prev ? 1ull : 0ull;
+#pragma unroll
+    for (int i = 1; i < NL; ++i) {
+        uint64_t t = S[i] + ext;
+        uint64_t c1 = t < S[i] ? 1ull : 0ull;
+        S[i] = t + carry;
+        uint64_t c2 = S[i] < t ? 1ull : 0ull;
+        carry = c1 | c2;
+    }
+}
+template <int NL>
+__device__ __forceinline__ void limbs_add(uint64_t (&S)[NL], const uint64_t (&P)[NL]) {
+    uint64_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        uint64_t t = S[i] + P[i];
+        uint64_t c1 = t < S[i] ? 1ull : 0ull;
+        S[i] = t + carry;
+        uint64_t c2 = S[i] < t ? 1ull : 0ull;
+        carry = c1 | c2;
+    }
+}
+// bits [lo, lo+64) of a magnitude held in NL limbs (zero outside); lo may be negative
+template <int NL>
+__device__ __forceinline__ uint64_t limbs_get64(const uint64_t (&S)[NL], int lo) {
+    uint64_t r = 0;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        int off = i * 64 - lo;  // position of limb i's bit 0 within the window
+        if (off >= 64 || off <= -64) continue;
+        r |= off >= 0 ? (S[i] << off) : (S[i] >> (-off));
+    }
+    return r;
+}
+
+// Round value * 2^exp2 to FP64 (RNE) where value is the two's complement
+// integer in S. Same contract as WideInt::to_double_scaled
+// (exactsum.hpp:143-157) + round_mag_to_double (exactsum.hpp:50-74): exact
+// zero -> +0.0, gradual underflow, overflow -> +/-Inf.
+template <int NL>
+__device__ __forceinline__ double round_limbs(uint64_t (&S)[NL], int exp2) {
+    const bool neg = (S[NL - 1] >> 63) != 0;
+    if (neg) {
+        uint64_t carry = 1;
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            uint64_t t = ~S[i] + carry;
+            carry = (carry && t == 0) ? 1ull : 0ull;
+            S[i] = t;
+        }
+    }
+    int top = -1;
+#pragma unroll
+    for (int i = 0; i < NL; ++i)
+        if (S[i]) top = i * 64 + 63 - __clzll((long long)S[i]);
+    if (top < 0) return 0.0;
+    // 128-bit window with the top bit at position 127, plus sticky below it
+    const int lo = top - 127;
+    typedef unsigned __int128 u128;
+    u128 W = (u128(limbs_get64<NL>(S, lo + 64)) << 64) | u128(limbs_get64<NL>(S, lo));
+    bool sticky_low = false;
+    if (lo > 0) {
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            int b0 = i * 64;
+            if (b0 >= lo) continue;
+            uint64_t mask = (lo - b0 >= 64) ? ~0ull : ((1ull << (lo - b0)) - 1);
+            if (S[i] & mask) sticky_low = true;
+        }
+    }
+    const int e = top + exp2;
+    int p = e >= -1022 ? top - 52 : -1074 - exp2;
+    const int nb = top - p + 1;  // mantissa bits kept (<= 53)
+    uint64_t m;
+    bool rnd, sticky;
+    if (nb < 0) {
+        m = 0;
+        rnd = false;
+        sticky = true;
+    } else if (nb == 0) {
+        m = 0;
+        rnd = true;  // the top bit itself
+        sticky = ((W << 1) != 0) || sticky_low;
+    } else {
+        m = uint64_t(W >> (128 - nb));
+        rnd = ((W >> (127 - nb)) & 1) != 0;
+        u128 below = nb >= 127 ? u128(0) : (W & ((u128(1) << (127 - nb)) - 1));
+        sticky = below != 0 || sticky_low;
+    }
+    if (rnd && (sticky || (m & 1))) {
+        ++m;
+        if (m == (1ull << 53)) {
+            m >>= 1;
+            ++p;
+        }
+    }
+    uint64_t bits;
+    if (m == 0) {
+        bits = 0;
+    } else if (m >= (1ull << 52)) {
+        int biased = p + exp2 + 52 + 1023;
+        bits = biased >= 2047 ? (0x7ffull << 52) : ((uint64_t(biased) << 52) | (m & 0xFFFFFFFFFFFFFull));
+    } else {
+        bits = m;  // subnormal: m * 2^-1074
+    }
+    if (neg) bits |= 1ull << 63;
+    return __longlong_as_double((long long)bits);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(kThreads, 1)
+    igemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs g) {
+    using C = Cfg<NB>;
+    const Plan* plan = g.plan;
+    if (plan->path != ADPB200_PATH_EMULATED || plan->variant != NB) return;
+    const int s = plan->slices, L = plan->L, nsl = plan->nsl;
+    const int ndiag = L + 1;
+    const int64_t kchunk = plan->kchunk;
+    const int64_t nkb = (g.K + kKB - 1) / kKB;
+    const int64_t kb_per_chunk = kchunk / kKB;
+    const int nchunks = (int)((nkb + kb_per_chunk - 1) / kb_per_chunk);
+    const int64_t tiles_m = (g.M + kBM - 1) / kBM, tiles_n = (g.N + NB - 1) / NB;
+    const int64_t ntiles = tiles_m * tiles_n;
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    SmemHeader* hdr = reinterpret_cast<SmemHeader*>(smem);
+    uint8_t* stages = smem + 1024;
+    const uint32_t a_bytes = uint32_t(nsl) * kBM * kKB;
+    const uint32_t stage_bytes = uint32_t(nsl) * (kBM + NB) * kKB;
+    const uint32_t avail = uint32_t(g.smem_bytes) - 2048;
+    int nstages = int(avail / stage_bytes);
+    if (nstages > kMaxStages) nstages = kMaxStages;
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nstages; ++i) {
+            tc::mbar_init(&hdr->full[i], 1);
+            tc::mbar_init(&hdr->empty[i], 1);
+        }
+        tc::mbar_init(&hdr->tmem_full, 1);
+        tc::mbar_init(&hdr->tmem_empty, 128);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        tc::tma_prefetch(&tmap_a);
+        tc::tma_prefetch(&tmap_b);
+    }
+    if (warp == 2) tc::tmem_alloc(&hdr->tmem_slot, 512);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem_base = hdr->tmem_slot;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                int64_t mt, nt;
+                tile_coords(tile, tiles_m, tiles_n, mt, nt);
+                for (int64_t kb = 0; kb < nkb; ++kb) {
+                    tc::mbar_wait(&hdr->empty[stage], phase ^ 1);
+                    uint8_t* sa = stages + size_t(stage) * stage_bytes;
+                    uint8_t* sb = sa + a_bytes;
+                    tc::mbar_expect_tx(&hdr->full[stage], stage_bytes);
+                    for (int d = 0; d < nsl; ++d) {
+                        tc::tma_load_3d(sa + d * (kBM * kKB), &tmap_a, &hdr->full[stage], int(kb * kKB),
+                                        int(mt * kBM), d);
+                        tc::tma_load_3d(sb + d * (NB * kKB), &tmap_b, &hdr->full[stage], int(kb * kKB),
+                                        int(nt * NB), d);
+                    }
+                    if (++stage == nstages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            const int da_max = s - 1 < L ? s - 1 : L;
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int c = 0; c < nchunks; ++c) {
+                    tc::mbar_wait(&hdr->tmem_empty, acc_phase ^ 1);
+                    tc::fence_after();
+                    const int64_t kb0 = int64_t(c) * kb_per_chunk;
+                    const int64_t kb1 = kb0 + kb_per_chunk < nkb ? kb0 + kb_per_chunk : nkb;
+                    for (int64_t kb = kb0; kb < kb1; ++kb) {
+                        tc::mbar_wait(&hdr->full[stage], phase);
+                        tc::fence_after();
+                        const uint32_t sa = tc::smem_u32(stages + size_t(stage) * stage_bytes);
+                        const uint32_t sb = sa + a_bytes;
+                        const bool first = kb == kb0;
+                        for (int da = 0; da <= da_max; ++da) {
+                            const int nb = (s - 1 < L - da ? s - 1 : L - da) + 1;
+                            const uint64_t adesc = tc::smem_desc_sw32(sa + da * (kBM * kKB));
+                            // in the first k-block, d_a >= 1 may open one new diagonal (d_b = s-1)
+                            const bool opens = first && da >= 1 && da + s - 1 <= L;
+                            const int nb_main = opens ? nb - 1 : nb;
+                            const uint32_t acc_main = (first && da == 0) ? 0u : 1u;
+                            for (int db = 0; db < nb_main; db += C::kMaxGroup) {
+                                const int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
+                                tc::mma_i8(tmem_base + uint32_t((da + db) * NB), adesc,
+                                           tc::smem_desc_sw32(sb + db * (NB * kKB)), tc::idesc_i8(kBM, cnt * NB),
+                                           acc_main);
+                            }
+                            if (opens)
+                                tc::mma_i8(tmem_base + uint32_t((da + nb - 1) * NB), adesc,
+                                           tc::smem_desc_sw32(sb + (nb - 1) * (NB * kKB)), tc::idesc_i8(kBM, NB),
+                                           0u);
+                        }
+                        tc::mma_commit(&hdr->empty[stage]);
+                        if (++stage == nstages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                    tc::mma_commit(&hdr->tmem_full);
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue =====
+        const int q = warp & 3;  // TMEM lane quadrant
+        uint32_t acc_phase = 0;
+        const int exp_base = -14 - 8 * L;
+        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            int64_t mt, nt;
+            tile_coords(tile, tiles_m, tiles_n, mt, nt);
+            const int64_t row = mt * kBM + q * 32 + lane;
+            const bool row_ok = row < g.M;
+            const int ea = row_ok ? g.scale_a[row] : 0;
+            for (int c = 0; c < nchunks; ++c) {
+                tc::mbar_wait(&hdr->tmem_full, acc_phase);
+                tc::fence_after();
+                const bool last = c == nchunks - 1;
+                const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
+                for (int j0 = 0; j0 < NB; j0 += C::kCW) {
+                    uint32_t v[C::kNDMax][C::kCW];
+#pragma unroll
+                    for (int D = 0; D < C::kNDMax; ++D)
+                        if (D < ndiag) tc::tmem_ld<C::kCW>(trow + uint32_t(D * NB + j0), v[D]);
+                    tc::tmem_wait_ld();
+#pragma unroll
+                    for (int cc = 0; cc < C::kCW; ++cc) {
+                        const int64_t col = nt * NB + j0 + cc;
+                        if (!row_ok || col >= g.N) continue;
+                        if (g.dump) {
+                            int64_t* dst = g.dump + (row * g.N + col) * g.ndump;
+#pragma unroll
+                            for (int D = 0; D < C::kNDMax; ++D)
+                                if (D < ndiag) dst[D] += int64_t(int32_t(v[D][cc]));
+                            continue;
+                        }
+                        uint64_t S[C::kNL];
+                        {
+                            int64_t x0 = int32_t(v[0][cc]);
+#pragma unroll
+                            for (int i = 0; i < C::kNL; ++i) S[i] = i == 0 ? uint64_t(x0) : (x0 < 0 ? ~0ull : 0ull);
+                        }
+#pragma unroll
+                        for (int D = 1; D < C::kNDMax; ++D)
+                            if (D < ndiag) limbs_shl8_add<C::kNL>(S, int64_t(int32_t(v[D][cc])));
+                        if (nchunks > 1) {
+                            // per-CTA scratch: this CTA runs all chunks of the tile back to back
+                            uint64_t* P = g.partial + size_t(blockIdx.x) * (C::kNL * NB * kBM) +
+                                          size_t(j0 + cc) * kBM + (q * 32 + lane);
+                            const int64_t lstride = int64_t(NB) * kBM;
+                            if (c > 0) {
+                                uint64_t prev[C::kNL];
+#pragma unroll
+                                for (int i = 0; i < C::kNL; ++i) prev[i] = P[i * lstride];
+                                limbs_add<C::kNL>(S, prev);
+                            }
+                            if (!last) {
+#pragma unroll
+                                for (int i = 0; i < C::kNL; ++i) P[i * lstride] = S[i];
+                                continue;
+                            }
+                        }
+                        const double vv = round_limbs<C::kNL>(S, ea + g.scale_b[col] + exp_base);
+                        double r = __dmul_rn(g.alpha, vv);
+                        if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
+                        g.c_out[row + col * g.ldc] = r;
+                    }
+                }
+                tc::fence_before();
+                tc::mbar_arrive(&hdr->tmem_empty);
+                acc_phase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc::fence_after();
+        tc::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ---- host side -----------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+template <int NB>
+void set_attr_once() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(igemm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+        done = true;
+    }
+}
+
+}  // namespace
+
+// Planes: [cap][lines][pitch] int8; box = 32 B of k x rows lines x 1 slice.
+bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t k, int64_t pitch, int cap,
+                    int box_rows) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {cuuint64_t(k), cuuint64_t(lines), cuuint64_t(cap)};
+    cuuint64_t strides[2] = {cuuint64_t(pitch), cuuint64_t(pitch * lines)};
+    cuuint32_t box[3] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st,
+                 uint64_t* nlaunch) {
+    const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + nb - 1) / nb);
+    int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    if (grid < 1) return 0;
+    GemmArgs a = g;
+    a.smem_bytes = kGemmSmemBytes;
+    switch (nb) {
+        case 64:
+            set_attr_once<64>();
+            igemm_kernel<64><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            break;
+        case 32:
+            set_attr_once<32>();
+            igemm_kernel<32><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            break;
+        case 16:
+            set_attr_once<16>();
+            igemm_kernel<16><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            break;
+        default:
+            return -1;
+    }
+    ++*nlaunch;
+    return 0;
+}
+
+}  // namespace adpb200

@@ -1,0 +1,43 @@
+#pragma once
+#include <cuda.h>
+
+#include "guard.cuh"
+
+namespace adpb200 {
+
+constexpr int kGemmSmemBytes = 227 * 1024;
+// Exact partial sums of one tile between k-chunks: NL limbs x NB x 128 rows
+// (max over the variants: 2 x 64 x 128 x 8 B).
+constexpr size_t kPartialBytesPerCta = 131072;
+
+// Internal problem: C(i, j) = sum_l A(i, l) B(l, j), i < M (A-lines), j < N
+// (B-lines), both operands sliced K-major into planes [slice][line][pitch].
+struct GemmArgs {
+    const Plan* plan;
+    int64_t M, N, K;
+    const int32_t* scale_a;  // E per A-line
+    const int32_t* scale_b;  // E per B-line
+    double alpha, beta;
+    double* c_out;           // C(i, j) at c_out[i + j*ldc]
+    int64_t ldc;
+    const double* c_in;      // read iff beta != 0 (may alias c_out)
+    int64_t ldc_in;
+    uint64_t* partial;       // multi-chunk exact partial sums, kPartialBytesPerCta per CTA
+    int64_t* dump;           // stage export: acc[(i*N + j)*ndump + D] += diagonal D
+    int ndump;
+    int smem_bytes;
+};
+
+bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t k, int64_t pitch, int cap,
+                    int box_rows);
+// nb in {64, 32, 16}; the kernel returns immediately unless plan->variant == nb.
+int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st,
+                 uint64_t* nlaunch);
+
+// K6: native FP64 fallback in the reference's summation order (ascending k,
+// separate multiply and add: oracle.cpp:7-28). Runs iff the plan says
+// native (or always when plan == nullptr).
+void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
+                   int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch);
+
+}  // namespace adpb200

@@ -1,0 +1,289 @@
+// K3: unsigned-integer slicing of FP64 lines into signed int8 digit planes
+// (decompose / element_digits / extract_digits / remap_digits,
+//  proj/src/slicing.cpp:20-136).
+//
+// Each line is scaled by E = line_max + 2 (0 for all-zero lines); element v
+// becomes the floor fixed-point integer U = floor(v * 2^(7 + 8(s-1) - E)),
+// whose base-256 digits (lead signed, the rest unsigned) are exactly the
+// reference's extract_digits chain. The reference's least-significant-first
+// remap (c > 127 -> c - 256, carry 1) equals adding 0x80 to every sub-leading
+// byte and reading each back as (byte ^ 0x80): X = U + 0x8080...80,
+// digit_d = byte(X) ^ 0x80, lead = X >> 8(s-1). For s <= 16, U fits in a
+// signed 128-bit integer and the whole chain is ~20 integer instructions
+// per element; s in [17, 32] takes the per-digit restatement.
+//
+// HBM-bound: 8 B read + nsl B written per element (+4 B per line).
+#include "guard.cuh"
+
+namespace adpb200 {
+
+namespace {
+
+typedef unsigned __int128 u128;
+typedef __int128 i128;
+
+// Fast path (s <= 16): returns X; digit d>=1 = byte(s-1-d) ^ 0x80, lead = X >> 8(s-1).
+__device__ __forceinline__ u128 slice_word(uint64_t bits, int E, int s) {
+    if ((bits << 1) == 0) {
+        // zero: U = 0 -> X = C
+        u128 C = 0;
+        for (int j = 0; j < s - 1; ++j) C |= u128(0x80) << (8 * j);
+        return C;
+    }
+    const bool neg = (bits >> 63) != 0;
+    const uint64_t M = norm_mant(bits);
+    const int e = eff_exp(bits);
+    const int sh = 45 + E - e;             // >= 47 (E >= e + 2)
+    const int st = sh - 8 * (s - 1);      // net right shift of the mantissa
+    i128 U;
+    if (st >= 0) {
+        uint64_t q = st >= 64 ? 0ull : ((neg ? M - 1 : M) >> st);
+        U = neg ? ~i128(q) : i128(q);      // floor(-x) = ~((M-1) >> st)
+    } else {
+        u128 w = u128(M) << (-st);         // exact, <= 126 bits
+        U = neg ? -i128(w) : i128(w);
+    }
+    u128 C = 0;
+    for (int j = 0; j < s - 1; ++j) C |= u128(0x80) << (8 * j);
+    return u128(U) + C;
+}
+
+// Reference-form restatement for any s <= 32 (slicing.cpp:11-66).
+__device__ __forceinline__ uint32_t byte_window(uint64_t x, int a) {
+    if (a >= 64 || a <= -8) return 0;
+    if (a >= 0) return uint32_t(x >> a) & 0xffu;
+    return uint32_t(x << -a) & 0xffu;
+}
+__device__ void slice_digits_slow(uint64_t bits, int E, int s, int8_t* out) {
+    if ((bits << 1) == 0) {
+        for (int d = 0; d < s; ++d) out[d] = 0;
+        return;
+    }
+    const bool neg = (bits >> 63) != 0;
+    const uint64_t M = norm_mant(bits);
+    const int e = eff_exp(bits);
+    const int sh = 45 + E - e;
+    int32_t lead;
+    uint8_t sub[kMaxSlices];
+    if (!neg) {
+        lead = sh < 64 ? int32_t(M >> sh) : 0;
+        for (int d = 1; d < s; ++d) sub[d - 1] = uint8_t(byte_window(M, sh - 8 * d));
+    } else {
+        const uint64_t Mm1 = M - 1;
+        lead = sh < 64 ? -int32_t(Mm1 >> sh) - 1 : -1;
+        for (int d = 1; d < s; ++d) {
+            int a = sh - 8 * d;
+            uint32_t mask = a >= 0 ? 0xffu : (a <= -8 ? 0u : (0xffu << -a) & 0xffu);
+            sub[d - 1] = uint8_t(~byte_window(Mm1, a) & mask);
+        }
+    }
+    int carry = 0;
+    for (int d = s - 1; d >= 1; --d) {
+        int c = sub[d - 1] + carry;
+        if (c <= 127) {
+            out[d] = int8_t(c);
+            carry = 0;
+        } else {
+            out[d] = int8_t(c - 256);
+            carry = 1;
+        }
+    }
+    out[0] = int8_t(lead + carry);
+}
+
+__device__ __forceinline__ int8_t digit_of(u128 X, int s, int d) {
+    if (d == 0) return int8_t(int(i128(X) >> (8 * (s - 1))));
+    return int8_t(uint8_t(X >> (8 * (s - 1 - d))) ^ 0x80u);
+}
+
+struct SliceArgs {
+    LineView v;
+    const int32_t* line_max;
+    int8_t* planes;
+    int64_t pitch;         // bytes between lines inside a plane
+    int64_t plane_stride;  // bytes between planes
+    int32_t* scale;
+    const Plan* plan;
+    int slices_fixed;
+};
+
+__device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
+    if (a.slices_fixed > 0) {
+        s = a.slices_fixed;
+        nsl = s;
+        return true;
+    }
+    if (a.plan->path != ADPB200_PATH_EMULATED) return false;
+    s = a.plan->slices;
+    nsl = a.plan->nsl;
+    return true;
+}
+
+// Lines contiguous (ps == 1): a thread slices 8 consecutive positions and
+// writes one 8-byte word per plane; a warp covers 256 positions of a line.
+template <bool kVec>
+__global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
+    int s, nsl;
+    if (!resolve(a, s, nsl)) return;
+    const int64_t groups = (a.v.len + 7) / 8;
+    const int64_t tasks = a.v.lines * groups;
+    for (int64_t task = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; task < tasks;
+         task += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t line = task / groups, g = task - line * groups;
+        const int lm = a.line_max[line];
+        const int E = lm == kNegSentinel ? 0 : lm + 2;
+        if (g == 0 && a.scale) a.scale[line] = E;
+        const int64_t p0 = g * 8;
+        const double* lp = a.v.ptr + line * a.v.ls;
+        uint64_t bits[8];
+        if (kVec && p0 + 8 <= a.v.len) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double2 d2 = __ldg(reinterpret_cast<const double2*>(lp + p0) + q);
+                bits[2 * q] = __double_as_longlong(d2.x);
+                bits[2 * q + 1] = __double_as_longlong(d2.y);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                bits[q] = p0 + q < a.v.len ? __double_as_longlong(__ldg(lp + p0 + q)) : 0ull;
+        }
+        int8_t* out = a.planes + line * a.pitch + p0;
+        const int nvalid = a.v.len - p0 < 8 ? int(a.v.len - p0) : 8;
+        if (s <= 16) {
+            u128 X[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) X[q] = slice_word(bits[q], E, s);
+            for (int d = 0; d < nsl; ++d) {
+                uint64_t w = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) w |= uint64_t(uint8_t(digit_of(X[q], s, d))) << (8 * q);
+                if (kVec && nvalid == 8) {
+                    *reinterpret_cast<uint64_t*>(out + d * a.plane_stride) = w;
+                } else {
+                    for (int q = 0; q < nvalid; ++q) out[d * a.plane_stride + q] = int8_t(w >> (8 * q));
+                }
+            }
+        } else {
+            int8_t dig[kMaxSlices];
+            for (int q = 0; q < nvalid; ++q) {
+                slice_digits_slow(bits[q], E, s, dig);
+                for (int d = 0; d < nsl; ++d) out[d * a.plane_stride + q] = dig[d];
+            }
+        }
+    }
+}
+
+// Lines adjacent (ls == 1), positions strided: 64 lines x 64 positions per
+// CTA. Loads are coalesced across lines; digits are transposed through
+// shared memory (row stride 68 B: conflict-free 32-bit writes) so every plane
+// is written K-major with 16-byte line segments.
+constexpr int kTL = 64, kTP = 64, kTStride = 68;
+
+__global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
+    int s, nsl;
+    if (!resolve(a, s, nsl)) return;
+    extern __shared__ __align__(16) uint8_t tile[];  // nsl * kTL * kTStride
+    const int64_t line0 = int64_t(blockIdx.x) * kTL;
+    const int64_t pos0 = int64_t(blockIdx.y) * kTP;
+    const int tl = threadIdx.x % kTL;       // line within tile
+    const int tp = threadIdx.x / kTL;       // 0..3: 16 positions each
+    const int64_t line = line0 + tl;
+    int E = 0;
+    if (line < a.v.lines) {
+        int lm = a.line_max[line];
+        E = lm == kNegSentinel ? 0 : lm + 2;
+        if (blockIdx.y == 0 && tp == 0 && a.scale) a.scale[line] = E;
+    }
+    uint64_t bits[16];  // all loads in flight before any compute
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        int64_t pos = pos0 + tp * 16 + q;
+        bits[q] = (line < a.v.lines && pos < a.v.len) ? __double_as_longlong(__ldg(a.v.ptr + line + pos * a.v.ps))
+                                                       : 0ull;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {           // 4 chunks of 4 positions
+        const int pl = tp * 16 + c * 4;     // local position of the chunk
+        if (s <= 16) {
+            u128 X[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) X[q] = slice_word(bits[c * 4 + q], E, s);
+            for (int d = 0; d < nsl; ++d) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(digit_of(X[q], s, d))) << (8 * q);
+                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            }
+        } else {
+            int8_t dig[4][kMaxSlices];
+            for (int q = 0; q < 4; ++q) slice_digits_slow(bits[c * 4 + q], E, s, dig[q]);
+            for (int d = 0; d < nsl; ++d) {
+                uint32_t w = 0;
+                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(dig[q][d])) << (8 * q);
+                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            }
+        }
+    }
+    __syncthreads();
+    // write out: thread -> (line, 16-byte chunk)
+    const int ol = threadIdx.x / 4, oc = threadIdx.x % 4;
+    const int64_t oline = line0 + ol;
+    const int64_t opos = pos0 + oc * 16;
+    if (oline >= a.v.lines || opos >= a.v.len) return;
+    const int nvalid = a.v.len - opos < 16 ? int(a.v.len - opos) : 16;
+    const bool vec = nvalid == 16 && ((a.pitch | a.plane_stride) & 15) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(a.planes) & 15) == 0);
+    for (int d = 0; d < nsl; ++d) {
+        const uint8_t* src = tile + (d * kTL + ol) * kTStride + oc * 16;
+        int8_t* dst = a.planes + d * a.plane_stride + oline * a.pitch + opos;
+        if (vec) {
+            uint4 w;
+            w.x = *reinterpret_cast<const uint32_t*>(src);
+            w.y = *reinterpret_cast<const uint32_t*>(src + 4);
+            w.z = *reinterpret_cast<const uint32_t*>(src + 8);
+            w.w = *reinterpret_cast<const uint32_t*>(src + 12);
+            *reinterpret_cast<uint4*>(dst) = w;
+        } else {
+            for (int q = 0; q < nvalid; ++q) dst[q] = int8_t(src[q]);
+        }
+    }
+}
+
+}  // namespace
+
+void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
+                  int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
+                  uint64_t* nlaunch) {
+    if (v.lines == 0) return;
+    SliceArgs a{v, line_max, planes, pitch, plane_stride, scale, plan, slices_fixed};
+    const bool rows = v.ps == 1 || v.lines == 1 || v.len == 0;
+    if (rows) {
+        if (a.v.lines == 1) a.v.ls = 0;
+        int64_t groups = (v.len + 7) / 8;
+        if (groups == 0) groups = 1;
+        int64_t tasks = v.lines * groups;
+        int64_t want = (tasks + 255) / 256;
+        int grid = (int)(want < int64_t(num_sms()) * 32 ? want : int64_t(num_sms()) * 32);
+        if (grid < 1) grid = 1;
+        const bool vec = ((reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0) && ((v.ls & 1) == 0 || v.lines == 1) &&
+                         ((pitch & 7) == 0) && ((plane_stride & 7) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(planes) & 7) == 0);
+        if (vec) slice_rows_kernel<true><<<grid, 256, 0, st>>>(a);
+        else slice_rows_kernel<false><<<grid, 256, 0, st>>>(a);
+    } else {
+        const int max_planes = slices_fixed > 0 ? slices_fixed : (plane_cap > 0 ? plane_cap : kMaxSlices);
+        const size_t smem = size_t(max_planes) * kTL * kTStride;
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaFuncSetAttribute(slice_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kMaxSlices * kTL * kTStride);
+            attr_set = true;
+        }
+        dim3 grid((unsigned)((v.lines + kTL - 1) / kTL), (unsigned)((v.len + kTP - 1) / kTP));
+        slice_cols_kernel<<<grid, 256, smem, st>>>(a);
+    }
+    ++*nlaunch;
+}
+
+}  // namespace adpb200
