@@ -79,7 +79,7 @@ struct Layout {
 Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) {
     Layout L{};
     L.blocks = K == 0 ? 0 : (K + block_len - 1) / block_len;
-    L.pitch = (int64_t)align_up((size_t)std::max<int64_t>(K, 1), 16);
+    L.pitch = (int64_t)align_up((size_t)std::max<int64_t>(K, 1), 32);
     L.cap = cap;
     size_t off = 0;
     auto take = [&](size_t bytes) {
@@ -231,12 +231,12 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         int32_t* sa = at<int32_t>(h, Lw.scale_a);
         int32_t* sb = at<int32_t>(h, Lw.scale_b);
         tm.begin(3);
-        launch_slice(P.a, aline, pa, Lw.pitch, Lw.pitch * P.M, sa, plan, fixed_slices, cap, st, nl);
-        launch_slice(P.b, bline, pb, Lw.pitch, Lw.pitch * P.N, sb, plan, fixed_slices, cap, st, nl);
+        launch_slice(P.a, aline, pa, Lw.pitch, Lw.pitch * P.M, 1, sa, plan, fixed_slices, cap, st, nl);
+        launch_slice(P.b, bline, pb, Lw.pitch, Lw.pitch * P.N, 1, sb, plan, fixed_slices, cap, st, nl);
         tm.end(3);
         // K4/K5: one launch per GEMM variant; exactly one does work
         CUtensorMap ta;
-        if (!make_plane_map(&ta, pa, P.M, P.K, Lw.pitch, cap, 128))
+        if (!make_plane_map(&ta, pa, P.M, Lw.pitch / 32, cap, 128))
             return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for A planes");
         GemmArgs g{};
         g.plan = plan;
@@ -254,7 +254,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         g.partial = at<uint64_t>(h, Lw.partial);
         g.dump = dump;
         g.ndump = ndump;
-        int variants[3] = {64, 32, 16};
+        int variants[4] = {64, 32, 16, 8};
         tm.begin(4);
         for (int nb : variants) {
             if (fixed_slices > 0) {  // the host knows the variant
@@ -263,7 +263,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                 if (hp.variant != nb) continue;
             }
             CUtensorMap tb;
-            if (!make_plane_map(&tb, pb, P.N, P.K, Lw.pitch, cap, nb))
+            if (!make_plane_map(&tb, pb, P.N, Lw.pitch / 32, cap, nb))
                 return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for B planes");
             if (launch_igemm(nb, ta, tb, g, st, nl)) return fail(ADPB200_ERR_RUNTIME, "bad GEMM variant");
         }
@@ -636,7 +636,7 @@ int adpb200_decompose(adpb200_handle h, const double* A, int64_t rows, int64_t c
     if (rc) return rc;
     launch_stats(v, 256, bmax, bmin, lmax, counts, nullptr, 1, st, &h->launches);
     if (v.len > 0) {
-        launch_slice(v, lmax, digits, v.len, v.len * v.lines, scale_exp, nullptr, slices, slices, st, &h->launches);
+        launch_slice(v, lmax, digits, v.len, v.len * v.lines, 0, scale_exp, nullptr, slices, slices, st, &h->launches);
     } else {
         rc = cuda_check(cudaMemsetAsync(scale_exp, 0, size_t(v.lines) * 4, st), "cudaMemsetAsync(scale)");
         if (rc) return rc;

@@ -170,7 +170,8 @@ __host__ __device__ inline void fill_emulation_plan(Plan& p, int s, int pair_lim
     pair_stats(s, L, &pairs, &mpd);
     p.pairs = pairs;
     const int ndiag = L + 1;
-    p.variant = ndiag <= 8 ? 64 : (ndiag <= 16 ? 32 : 16);
+    // columns per diagonal accumulator so that ndiag * variant <= 512 TMEM columns
+    p.variant = ndiag <= 8 ? 64 : (ndiag <= 16 ? 32 : (ndiag <= 32 ? 16 : 8));
     const int64_t kc = int32_kchunk(mpd);
     p.kchunk = (int32_t)kc;
     p.nchunks = k == 0 ? 0 : (int32_t)((k + kc - 1) / kc);

@@ -27,8 +27,10 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
 // slices_fixed > 0 overrides the plan (stage exports); otherwise the kernel
 // reads s / nsl from the plan and does nothing unless the path is emulated.
 // plane_cap bounds nsl (sizes the transpose tile of the strided variant).
+// blocked = 1: plane d is [k-block of 32][line][32 B] (the GEMM's TMA layout),
+// zero-filled up to the next multiple of 32 positions; 0: [line][pitch].
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
-                  int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
+                  int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
                   uint64_t* nlaunch);
 
 }  // namespace adpb200

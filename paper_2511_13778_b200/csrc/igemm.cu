@@ -40,7 +40,8 @@ constexpr int kGroupM = 16;   // raster: 16 m-tiles per group
 template <int NB>
 struct Cfg {
     static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
-    static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : 5);  // exact fold limbs
+    // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
+    static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
     static constexpr int kCW = 64 / kNDMax >= 2 ? 64 / kNDMax : 2;  // columns per TMEM load batch
     static constexpr int kMaxGroup = 256 / NB;                 // B slices per MMA (N <= 256)
 };
@@ -241,10 +242,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sb = sa + a_bytes;
                     tc::mbar_expect_tx(&hdr->full[stage], stage_bytes);
                     for (int d = 0; d < nsl; ++d) {
-                        tc::tma_load_3d(sa + d * (kBM * kKB), &tmap_a, &hdr->full[stage], int(kb * kKB),
-                                        int(mt * kBM), d);
-                        tc::tma_load_3d(sb + d * (NB * kKB), &tmap_b, &hdr->full[stage], int(kb * kKB),
-                                        int(nt * NB), d);
+                        // blocked planes: (32 B, line, k-block, slice) -> one contiguous box
+                        tc::tma_load_4d(sa + d * (kBM * kKB), &tmap_a, &hdr->full[stage], 0, int(mt * kBM),
+                                        int(kb), d);
+                        tc::tma_load_4d(sb + d * (NB * kKB), &tmap_b, &hdr->full[stage], 0, int(nt * NB),
+                                        int(kb), d);
                     }
                     if (++stage == nstages) {
                         stage = 0;
@@ -278,11 +280,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const bool opens = first && da >= 1 && da + s - 1 <= L;
                             const int nb_main = opens ? nb - 1 : nb;
                             const uint32_t acc_main = (first && da == 0) ? 0u : 1u;
-                            for (int db = 0; db < nb_main; db += C::kMaxGroup) {
-                                const int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
+                            for (int db = 0; db < nb_main;) {
+                                int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
+                                if (NB == 8 && cnt > 1 && (cnt & 1)) --cnt;  // N = 8 or a multiple of 16
                                 tc::mma_i8(tmem_base + uint32_t((da + db) * NB), adesc,
                                            tc::smem_desc_sw32(sb + db * (NB * kKB)), tc::idesc_i8(kBM, cnt * NB),
                                            acc_main);
+                                db += cnt;
                             }
                             if (opens)
                                 tc::mma_i8(tmem_base + uint32_t((da + nb - 1) * NB), adesc,
@@ -406,16 +410,16 @@ void set_attr_once() {
 
 }  // namespace
 
-// Planes: [cap][lines][pitch] int8; box = 32 B of k x rows lines x 1 slice.
-bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t k, int64_t pitch, int cap,
-                    int box_rows) {
+// Blocked planes: plane d = [k-block][line][32 B]; a box is 32 B x box_rows
+// lines of one k-block of one slice = one contiguous run in HBM.
+bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t nkb, int cap, int box_rows) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[3] = {cuuint64_t(k), cuuint64_t(lines), cuuint64_t(cap)};
-    cuuint64_t strides[2] = {cuuint64_t(pitch), cuuint64_t(pitch * lines)};
-    cuuint32_t box[3] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(planes), dims, strides, box, estr,
+    cuuint64_t dims[4] = {cuuint64_t(kKB), cuuint64_t(lines), cuuint64_t(nkb), cuuint64_t(cap)};
+    cuuint64_t strides[3] = {cuuint64_t(kKB), cuuint64_t(kKB * lines), cuuint64_t(kKB * lines * nkb)};
+    cuuint32_t box[4] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -440,6 +444,10 @@ int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const Gem
         case 16:
             set_attr_once<16>();
             igemm_kernel<16><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            break;
+        case 8:
+            set_attr_once<8>();
+            igemm_kernel<8><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
             break;
         default:
             return -1;

@@ -28,9 +28,8 @@ struct GemmArgs {
     int smem_bytes;
 };
 
-bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t k, int64_t pitch, int cap,
-                    int box_rows);
-// nb in {64, 32, 16}; the kernel returns immediately unless plan->variant == nb.
+bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t nkb, int cap, int box_rows);
+// nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.
 int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st,
                  uint64_t* nlaunch);
 

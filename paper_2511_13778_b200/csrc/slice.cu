@@ -7,12 +7,22 @@
 // whose base-256 digits (lead signed, the rest unsigned) are exactly the
 // reference's extract_digits chain. The reference's least-significant-first
 // remap (c > 127 -> c - 256, carry 1) equals adding 0x80 to every sub-leading
-// byte and reading each back as (byte ^ 0x80): X = U + 0x8080...80,
-// digit_d = byte(X) ^ 0x80, lead = X >> 8(s-1). For s <= 16, U fits in a
-// signed 128-bit integer and the whole chain is ~20 integer instructions
-// per element; s in [17, 32] takes the per-digit restatement.
+// byte: with X = U + 0x8080...80 (s-1 bytes), digit 0 is byte s-1 of X read
+// as int8 and digit d >= 1 is byte s-1-d of X xor 0x80. So every plane byte
+// is a byte of X: s <= 8 needs one 64-bit integer per element, s <= 16 a
+// 128-bit one, s in [17, 32] takes the per-digit restatement of the
+// reference. The slice count is a compile-time constant of the inner loop
+// (dispatched once per CTA from the device plan), so byte selection is
+// static.
+//
+// Output layouts: "blocked" (the GEMM's TMA layout) stores plane d as
+// [k-block of 32][line][32 bytes], so one TMA box (32 B x 128 lines) is a
+// contiguous 4 KiB run; "pitched" (stage export) is the reference's
+// plane-major [line][len].
 //
 // HBM-bound: 8 B read + nsl B written per element (+4 B per line).
+#include <type_traits>
+
 #include "guard.cuh"
 
 namespace adpb200 {
@@ -22,30 +32,46 @@ namespace {
 typedef unsigned __int128 u128;
 typedef __int128 i128;
 
-// Fast path (s <= 16): returns X; digit d>=1 = byte(s-1-d) ^ 0x80, lead = X >> 8(s-1).
-__device__ __forceinline__ u128 slice_word(uint64_t bits, int E, int s) {
-    if ((bits << 1) == 0) {
-        // zero: U = 0 -> X = C
-        u128 C = 0;
-        for (int j = 0; j < s - 1; ++j) C |= u128(0x80) << (8 * j);
-        return C;
-    }
+template <int S>
+struct Word {
+    typedef typename std::conditional<(S <= 8), uint64_t, u128>::type T;
+};
+
+template <int S>
+__device__ __forceinline__ typename Word<S>::T slice_const() {
+    typedef typename Word<S>::T T;
+    T C = 0;
+#pragma unroll
+    for (int j = 0; j < S - 1; ++j) C |= T(0x80) << (8 * j);
+    return C;
+}
+
+// X = floor(v * 2^(7 + 8(S-1) - E)) + 0x80..80 (S <= 16)
+template <int S>
+__device__ __forceinline__ typename Word<S>::T slice_word(uint64_t bits, int E) {
+    typedef typename Word<S>::T T;
+    const T C = slice_const<S>();
+    if ((bits << 1) == 0) return C;
     const bool neg = (bits >> 63) != 0;
     const uint64_t M = norm_mant(bits);
     const int e = eff_exp(bits);
-    const int sh = 45 + E - e;             // >= 47 (E >= e + 2)
-    const int st = sh - 8 * (s - 1);      // net right shift of the mantissa
-    i128 U;
+    const int st = 45 + E - e - 8 * (S - 1);  // net right shift of the 53-bit mantissa
+    T U;
     if (st >= 0) {
-        uint64_t q = st >= 64 ? 0ull : ((neg ? M - 1 : M) >> st);
-        U = neg ? ~i128(q) : i128(q);      // floor(-x) = ~((M-1) >> st)
+        const uint64_t q = st >= 64 ? 0ull : ((neg ? M - 1 : M) >> st);
+        U = neg ? ~T(q) : T(q);  // floor(-M 2^-st) = ~((M-1) >> st)
     } else {
-        u128 w = u128(M) << (-st);         // exact, <= 126 bits
-        U = neg ? -i128(w) : i128(w);
+        const T w = T(M) << (-st);  // exact: -st <= 8(S-1) - 47
+        U = neg ? T(0) - w : w;
     }
-    u128 C = 0;
-    for (int j = 0; j < s - 1; ++j) C |= u128(0x80) << (8 * j);
-    return u128(U) + C;
+    return U + C;
+}
+
+// byte j of X as stored in plane d = S-1-j
+template <int S>
+__device__ __forceinline__ uint32_t plane_byte(typename Word<S>::T X, int d) {
+    const uint32_t b = uint32_t(X >> (8 * (S - 1 - d))) & 0xffu;
+    return d == 0 ? b : (b ^ 0x80u);
 }
 
 // Reference-form restatement for any s <= 32 (slicing.cpp:11-66).
@@ -91,21 +117,23 @@ __device__ void slice_digits_slow(uint64_t bits, int E, int s, int8_t* out) {
     out[0] = int8_t(lead + carry);
 }
 
-__device__ __forceinline__ int8_t digit_of(u128 X, int s, int d) {
-    if (d == 0) return int8_t(int(i128(X) >> (8 * (s - 1))));
-    return int8_t(uint8_t(X >> (8 * (s - 1 - d))) ^ 0x80u);
-}
-
 struct SliceArgs {
     LineView v;
     const int32_t* line_max;
     int8_t* planes;
-    int64_t pitch;         // bytes between lines inside a plane
+    int64_t pitch;         // pitched: bytes between lines; blocked: unused
     int64_t plane_stride;  // bytes between planes
+    int blocked;           // 1: [d][kb][line][32]
     int32_t* scale;
     const Plan* plan;
     int slices_fixed;
 };
+
+// byte offset of (d, line, pos) inside the planes
+__device__ __forceinline__ int64_t plane_off(const SliceArgs& a, int d, int64_t line, int64_t pos) {
+    if (a.blocked) return int64_t(d) * a.plane_stride + ((pos >> 5) * a.v.lines + line) * 32 + (pos & 31);
+    return int64_t(d) * a.plane_stride + line * a.pitch + pos;
+}
 
 __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
     if (a.slices_fixed > 0) {
@@ -119,13 +147,9 @@ __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
     return true;
 }
 
-// Lines contiguous (ps == 1): a thread slices 8 consecutive positions and
-// writes one 8-byte word per plane; a warp covers 256 positions of a line.
-template <bool kVec>
-__global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
-    int s, nsl;
-    if (!resolve(a, s, nsl)) return;
-    const int64_t groups = (a.v.len + 7) / 8;
+// ---- lines contiguous (ps == 1): a thread slices 8 consecutive positions ----------
+template <int S, bool kVec>
+__device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t groups, int64_t span) {
     const int64_t tasks = a.v.lines * groups;
     for (int64_t task = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; task < tasks;
          task += int64_t(gridDim.x) * blockDim.x) {
@@ -148,37 +172,94 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
             for (int q = 0; q < 8; ++q)
                 bits[q] = p0 + q < a.v.len ? __double_as_longlong(__ldg(lp + p0 + q)) : 0ull;
         }
-        int8_t* out = a.planes + line * a.pitch + p0;
-        const int nvalid = a.v.len - p0 < 8 ? int(a.v.len - p0) : 8;
-        if (s <= 16) {
-            u128 X[8];
+        const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
+        if constexpr (S <= 16) {
+            typename Word<S>::T X[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) X[q] = slice_word(bits[q], E, s);
-            for (int d = 0; d < nsl; ++d) {
-                uint64_t w = 0;
+            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[q], E);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) w |= uint64_t(uint8_t(digit_of(X[q], s, d))) << (8 * q);
+            for (int d = 0; d < S; ++d) {
+                if (d >= nsl) break;
+                uint32_t lo = 0, hi = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    lo |= plane_byte<S>(X[q], d) << (8 * q);
+                    hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
+                }
+                int8_t* out = a.planes + plane_off(a, d, line, p0);
                 if (kVec && nvalid == 8) {
-                    *reinterpret_cast<uint64_t*>(out + d * a.plane_stride) = w;
+                    *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
                 } else {
-                    for (int q = 0; q < nvalid; ++q) out[d * a.plane_stride + q] = int8_t(w >> (8 * q));
+                    const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+                    for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
                 }
             }
         } else {
             int8_t dig[kMaxSlices];
+            const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
             for (int q = 0; q < nvalid; ++q) {
                 slice_digits_slow(bits[q], E, s, dig);
-                for (int d = 0; d < nsl; ++d) out[d * a.plane_stride + q] = dig[d];
+                for (int d = 0; d < nsl; ++d) a.planes[plane_off(a, d, line, p0 + q)] = dig[d];
             }
         }
     }
 }
 
-// Lines adjacent (ls == 1), positions strided: 64 lines x 64 positions per
-// CTA. Loads are coalesced across lines; digits are transposed through
-// shared memory (row stride 68 B: conflict-free 32-bit writes) so every plane
-// is written K-major with 16-byte line segments.
+template <bool kVec>
+__global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
+    int s, nsl;
+    if (!resolve(a, s, nsl)) return;
+    // blocked planes are zero-filled up to the 32-byte k-block
+    const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
+    const int64_t groups = (span + 7) / 8;
+    switch (s) {
+#define ADPB200_ROWS_CASE(S) \
+    case S: rows_body<S, kVec>(a, nsl, groups, span); break;
+        ADPB200_ROWS_CASE(1) ADPB200_ROWS_CASE(2) ADPB200_ROWS_CASE(3) ADPB200_ROWS_CASE(4)
+        ADPB200_ROWS_CASE(5) ADPB200_ROWS_CASE(6) ADPB200_ROWS_CASE(7) ADPB200_ROWS_CASE(8)
+        ADPB200_ROWS_CASE(9) ADPB200_ROWS_CASE(10) ADPB200_ROWS_CASE(11) ADPB200_ROWS_CASE(12)
+        ADPB200_ROWS_CASE(13) ADPB200_ROWS_CASE(14) ADPB200_ROWS_CASE(15) ADPB200_ROWS_CASE(16)
+#undef ADPB200_ROWS_CASE
+        default: rows_body<32, kVec>(a, nsl, groups, span); break;
+    }
+}
+
+// ---- lines adjacent (ls == 1), positions strided: 64 lines x 64 positions ---------
+// Loads are coalesced across lines; digits are transposed through shared
+// memory (row stride 68 B: conflict-free 32-bit writes) so every plane is
+// written K-major in 16-byte line segments.
 constexpr int kTL = 64, kTP = 64, kTStride = 68;
+
+template <int S>
+__device__ __forceinline__ void cols_compute(const SliceArgs& a, int nsl, uint8_t* tile, const uint64_t (&bits)[16],
+                                             int E, int tl, int tp) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int pl = tp * 16 + c * 4;
+        if constexpr (S <= 16) {
+            typename Word<S>::T X[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) X[q] = slice_word<S>(bits[c * 4 + q], E);
+#pragma unroll
+            for (int d = 0; d < S; ++d) {
+                if (d >= nsl) break;
+                uint32_t w = 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w |= plane_byte<S>(X[q], d) << (8 * q);
+                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            }
+        } else {
+            const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
+            int8_t dig[4][kMaxSlices];
+            for (int q = 0; q < 4; ++q) slice_digits_slow(bits[c * 4 + q], E, s, dig[q]);
+            for (int d = 0; d < nsl; ++d) {
+                uint32_t w = 0;
+                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(dig[q][d])) << (8 * q);
+                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            }
+        }
+    }
+}
 
 __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
     int s, nsl;
@@ -186,8 +267,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
     extern __shared__ __align__(16) uint8_t tile[];  // nsl * kTL * kTStride
     const int64_t line0 = int64_t(blockIdx.x) * kTL;
     const int64_t pos0 = int64_t(blockIdx.y) * kTP;
-    const int tl = threadIdx.x % kTL;       // line within tile
-    const int tp = threadIdx.x / kTL;       // 0..3: 16 positions each
+    const int tl = threadIdx.x % kTL;  // line within tile
+    const int tp = threadIdx.x / kTL;  // 0..3: 16 positions each
     const int64_t line = line0 + tl;
     int E = 0;
     if (line < a.v.lines) {
@@ -202,41 +283,29 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
         bits[q] = (line < a.v.lines && pos < a.v.len) ? __double_as_longlong(__ldg(a.v.ptr + line + pos * a.v.ps))
                                                        : 0ull;
     }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {           // 4 chunks of 4 positions
-        const int pl = tp * 16 + c * 4;     // local position of the chunk
-        if (s <= 16) {
-            u128 X[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) X[q] = slice_word(bits[c * 4 + q], E, s);
-            for (int d = 0; d < nsl; ++d) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(digit_of(X[q], s, d))) << (8 * q);
-                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
-            }
-        } else {
-            int8_t dig[4][kMaxSlices];
-            for (int q = 0; q < 4; ++q) slice_digits_slow(bits[c * 4 + q], E, s, dig[q]);
-            for (int d = 0; d < nsl; ++d) {
-                uint32_t w = 0;
-                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(dig[q][d])) << (8 * q);
-                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
-            }
-        }
+    switch (s) {
+#define ADPB200_COLS_CASE(S) \
+    case S: cols_compute<S>(a, nsl, tile, bits, E, tl, tp); break;
+        ADPB200_COLS_CASE(1) ADPB200_COLS_CASE(2) ADPB200_COLS_CASE(3) ADPB200_COLS_CASE(4)
+        ADPB200_COLS_CASE(5) ADPB200_COLS_CASE(6) ADPB200_COLS_CASE(7) ADPB200_COLS_CASE(8)
+        ADPB200_COLS_CASE(9) ADPB200_COLS_CASE(10) ADPB200_COLS_CASE(11) ADPB200_COLS_CASE(12)
+        ADPB200_COLS_CASE(13) ADPB200_COLS_CASE(14) ADPB200_COLS_CASE(15) ADPB200_COLS_CASE(16)
+#undef ADPB200_COLS_CASE
+        default: cols_compute<32>(a, nsl, tile, bits, E, tl, tp); break;
     }
     __syncthreads();
     // write out: thread -> (line, 16-byte chunk)
     const int ol = threadIdx.x / 4, oc = threadIdx.x % 4;
     const int64_t oline = line0 + ol;
     const int64_t opos = pos0 + oc * 16;
-    if (oline >= a.v.lines || opos >= a.v.len) return;
-    const int nvalid = a.v.len - opos < 16 ? int(a.v.len - opos) : 16;
-    const bool vec = nvalid == 16 && ((a.pitch | a.plane_stride) & 15) == 0 &&
+    const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
+    if (oline >= a.v.lines || opos >= span) return;
+    const int nvalid = span - opos < 16 ? int(span - opos) : 16;
+    const bool vec = nvalid == 16 && (a.blocked || ((a.pitch | a.plane_stride) & 15) == 0) &&
                      ((reinterpret_cast<uintptr_t>(a.planes) & 15) == 0);
     for (int d = 0; d < nsl; ++d) {
         const uint8_t* src = tile + (d * kTL + ol) * kTStride + oc * 16;
-        int8_t* dst = a.planes + d * a.plane_stride + oline * a.pitch + opos;
+        int8_t* dst = a.planes + plane_off(a, d, oline, opos);
         if (vec) {
             uint4 w;
             w.x = *reinterpret_cast<const uint32_t*>(src);
@@ -253,21 +322,22 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
 }  // namespace
 
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
-                  int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
+                  int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
                   uint64_t* nlaunch) {
     if (v.lines == 0) return;
-    SliceArgs a{v, line_max, planes, pitch, plane_stride, scale, plan, slices_fixed};
+    SliceArgs a{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed};
     const bool rows = v.ps == 1 || v.lines == 1 || v.len == 0;
     if (rows) {
         if (a.v.lines == 1) a.v.ls = 0;
-        int64_t groups = (v.len + 7) / 8;
+        const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
+        int64_t groups = (span + 7) / 8;
         if (groups == 0) groups = 1;
         int64_t tasks = v.lines * groups;
         int64_t want = (tasks + 255) / 256;
-        int grid = (int)(want < int64_t(num_sms()) * 32 ? want : int64_t(num_sms()) * 32);
+        int grid = (int)(want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16);
         if (grid < 1) grid = 1;
         const bool vec = ((reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0) && ((v.ls & 1) == 0 || v.lines == 1) &&
-                         ((pitch & 7) == 0) && ((plane_stride & 7) == 0) &&
+                         (blocked || (((pitch & 7) == 0) && ((plane_stride & 7) == 0))) &&
                          ((reinterpret_cast<uintptr_t>(planes) & 7) == 0);
         if (vec) slice_rows_kernel<true><<<grid, 256, 0, st>>>(a);
         else slice_rows_kernel<false><<<grid, 256, 0, st>>>(a);
@@ -280,7 +350,8 @@ void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, in
                                  kMaxSlices * kTL * kTStride);
             attr_set = true;
         }
-        dim3 grid((unsigned)((v.lines + kTL - 1) / kTL), (unsigned)((v.len + kTP - 1) / kTP));
+        const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
+        dim3 grid((unsigned)((v.lines + kTL - 1) / kTL), (unsigned)((span + kTP - 1) / kTP));
         slice_cols_kernel<<<grid, 256, smem, st>>>(a);
     }
     ++*nlaunch;
