@@ -189,9 +189,9 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     tm.begin(0);
     if (!native_only && phase != 2) {
         if (P.M > 0)
-            launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, st, nl);
+            launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
         if (P.N > 0)
-            launch_stats(P.b, o.esc_block_len, bmax, bmin, bline, plan->counts + 3, &plan->exc, 2, st, nl);
+            launch_stats(P.b, o.esc_block_len, bmax, bmin, bline, plan->counts + 3, &plan->exc, 2, 1, st, nl);
     }
     tm.end(0);
     // K2: ESC, only where decide() can reach it (mode auto, or the forced
@@ -601,7 +601,8 @@ int adpb200_block_stats(adpb200_handle h, const double* A, int64_t rows, int64_t
         if (rc) return rc;
     }
     LineView v = orient ? LineView{A, cols, rows, 1, cols} : LineView{A, rows, cols, cols, 1};
-    if (v.lines > 0) launch_stats(v, block_len, max_exp, min_exp, line_max, counts, exceptional, 1, st, &h->launches);
+    if (v.lines > 0)
+        launch_stats(v, block_len, max_exp, min_exp, line_max, counts, exceptional, 1, 0, st, &h->launches);
     return cuda_check(cudaGetLastError(), "block_stats launch");
 }
 
@@ -612,7 +613,19 @@ int adpb200_esc_coarsened(adpb200_handle h, const int32_t* a_max, const int32_t*
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int rc = cuda_check(cudaMemsetAsync(out, 0, 3 * sizeof(int32_t), st), "cudaMemsetAsync(out)");
     if (rc) return rc;
-    launch_esc(a_max, a_min, a_line, b_max, b_min, b_line, m, n, blocks, nullptr, out, nullptr, st, &h->launches);
+    // the kernel consumes block-major stats; the export takes the reference's line-major ones
+    const size_t sa = align_up(size_t(m) * blocks * 4 + 16, 256), sb = align_up(size_t(n) * blocks * 4 + 16, 256);
+    rc = ensure_ws(h, 2 * sa + 2 * sb, st);
+    if (rc) return rc;
+    int32_t* tA = at<int32_t>(h, 0);
+    int32_t* tAn = at<int32_t>(h, sa);
+    int32_t* tB = at<int32_t>(h, 2 * sa);
+    int32_t* tBn = at<int32_t>(h, 2 * sa + sb);
+    launch_transpose_i32(a_max, m, blocks, tA, st, &h->launches);
+    launch_transpose_i32(a_min, m, blocks, tAn, st, &h->launches);
+    launch_transpose_i32(b_max, n, blocks, tB, st, &h->launches);
+    launch_transpose_i32(b_min, n, blocks, tBn, st, &h->launches);
+    launch_esc(tA, tAn, a_line, tB, tBn, b_line, m, n, blocks, nullptr, out, nullptr, st, &h->launches);
     launch_esc_finish(out, target_bits, st, &h->launches);
     return cuda_check(cudaGetLastError(), "esc launch");
 }
@@ -634,7 +647,7 @@ int adpb200_decompose(adpb200_handle h, const double* A, int64_t rows, int64_t c
     int32_t* lmax = at<int32_t>(h, 1024 + 2 * align_up(size_t(v.lines) * blocks * 4 + 64, 1024));
     rc = cuda_check(cudaMemsetAsync(counts, 0, 64, st), "cudaMemsetAsync");
     if (rc) return rc;
-    launch_stats(v, 256, bmax, bmin, lmax, counts, nullptr, 1, st, &h->launches);
+    launch_stats(v, 256, bmax, bmin, lmax, counts, nullptr, 1, 0, st, &h->launches);
     if (v.len > 0) {
         launch_slice(v, lmax, digits, v.len, v.len * v.lines, 0, scale_exp, nullptr, slices, slices, st, &h->launches);
     } else {

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmax_out,
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit) {
+                                                         int exc_bit, int transposed) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -112,8 +112,9 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
         bmin = warp_min(bmin);
         if (lane == 0) {
             bool any = bmax != kNegSentinel;
-            bmax_out[task] = any ? bmax : kNegSentinel;
-            bmin_out[task] = any ? bmin : kNegSentinel;
+            const int64_t o = transposed ? blk * v.lines + line : task;
+            bmax_out[o] = any ? bmax : kNegSentinel;
+            bmin_out[o] = any ? bmin : kNegSentinel;
         }
     }
     flush_counts(nan, inf, negz, counts, exc_flag, exc_bit);
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmax_out,
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit) {
+                                                         int exc_bit, int transposed) {
     int nan = 0, inf = 0, negz = 0;
     const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     for (int64_t blk = blockIdx.y; blk < blocks; blk += gridDim.y) {
@@ -160,8 +161,9 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                 }
             }
             bool any = bmax != kNegSentinel;
-            bmax_out[line * blocks + blk] = any ? bmax : kNegSentinel;
-            bmin_out[line * blocks + blk] = any ? bmin : kNegSentinel;
+            const int64_t o = transposed ? blk * v.lines + line : line * blocks + blk;
+            bmax_out[o] = any ? bmax : kNegSentinel;
+            bmin_out[o] = any ? bmin : kNegSentinel;
         }
     }
     flush_counts(nan, inf, negz, counts, exc_flag, exc_bit);
@@ -169,6 +171,15 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
 
 // line_max[line] = max over the line's block maxima (sentinel is the minimum,
 // so all-zero blocks drop out and all-zero lines stay sentinel).
+__global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lines, int64_t blocks,
+                                  int32_t* __restrict__ line_max) {
+    const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (line >= lines) return;
+    int mx = kNegSentinel;
+    for (int64_t b = 0; b < blocks; ++b) mx = max(mx, bmaxT[b * lines + line]);
+    line_max[line] = mx;
+}
+
 __global__ void line_max_kernel(const int32_t* __restrict__ bmax, int64_t lines, int64_t blocks,
                                 int32_t* __restrict__ line_max) {
     const int64_t line = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -195,91 +206,114 @@ __global__ void scan_kernel(const double* __restrict__ a, int64_t count, unsigne
 
 // ---- K2: coarsened ESC as a max-plus product over blocks --------------------------
 // z_ij = max_t max(Amax_it + Bmin_jt, Amin_it + Bmax_jt); span = lA_i + lB_j - z + 1.
-// Sentinel blocks are folded into the arithmetic: any sum with a sentinel is
-// <= -1000000 + 1023, far below every real sum (>= -2148), so it can never win
-// over a real candidate, and z stays below -900000 exactly when the
-// reference's z stays kNegSentinel (structurally zero dot product).
-// DPX __viaddmax_s32 fuses the add and the max.
-constexpr int kEscTI = 4, kEscTJ = 8;          // per-thread register tile
-constexpr int kEscBI = 64, kEscBJ = 128;       // CTA tile (16 x 16 threads)
+// The block stats arrive block-major ([t][line]) so each smem stage is a
+// straight coalesced copy. Exponents live in [-1074, 1023] and are packed two
+// per 32-bit word (int16x2); the reference's kNegSentinel becomes -16384. Any
+// sum involving a sentinel is <= -16384 + 1023 < -2148 <= every real sum, and
+// -16384 + -16384 = -32768 does not wrap, so sentinel blocks can never win a
+// max and z stays <= -15361 exactly when the reference's z stays kNegSentinel
+// (structurally zero dot product) — the exact same maximum, with no
+// per-block branches. DPX __viaddmax_s16x2 fuses add + max for two (i, j)
+// pairs per instruction.
+constexpr int kEscBI = 64, kEscBJ = 128;       // CTA tile (16 x 16 threads, 4 x 8 per thread)
 constexpr int kEscTB = 32;                     // blocks staged per smem round
+constexpr int kS16 = -16384;
 
-__global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ amax,
-                                                  const int32_t* __restrict__ amin,
+__device__ __forceinline__ uint32_t pack2(int lo, int hi) {
+    return (uint32_t(lo) & 0xffffu) | (uint32_t(hi) << 16);
+}
+__device__ __forceinline__ int to16(int v) { return v == kNegSentinel ? kS16 : v; }
+
+__global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ amaxT,
+                                                  const int32_t* __restrict__ aminT,
                                                   const int32_t* __restrict__ aline,
-                                                  const int32_t* __restrict__ bmax,
-                                                  const int32_t* __restrict__ bmin,
+                                                  const int32_t* __restrict__ bmaxT,
+                                                  const int32_t* __restrict__ bminT,
                                                   const int32_t* __restrict__ bline, int64_t m, int64_t n,
                                                   int64_t t, const Plan* plan, int32_t* esc_out,
                                                   int32_t* ran_flag) {
     if (plan && plan->exc) return;  // exceptional inputs never reach the ESC (adp.cpp:58-62)
-    __shared__ __align__(16) int32_t sAmax[kEscTB][kEscBI];
-    __shared__ __align__(16) int32_t sAmin[kEscTB][kEscBI];
-    __shared__ __align__(16) int32_t sBmax[kEscTB][kEscBJ];
-    __shared__ __align__(16) int32_t sBmin[kEscTB][kEscBJ];
+    // A words hold (a, a); B words hold (b_j, b_j+1) for the thread's j pairs
+    __shared__ __align__(16) uint32_t sAmx[kEscTB][kEscBI];
+    __shared__ __align__(16) uint32_t sAmn[kEscTB][kEscBI];
+    __shared__ __align__(16) uint32_t sBmx[kEscTB][kEscBJ / 2];
+    __shared__ __align__(16) uint32_t sBmn[kEscTB][kEscBJ / 2];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const int64_t i0 = int64_t(blockIdx.y) * kEscBI, j0 = int64_t(blockIdx.x) * kEscBJ;
-    int z[kEscTI][kEscTJ];
+    uint32_t z[4][4];  // [i][j pair]
 #pragma unroll
-    for (int a = 0; a < kEscTI; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < kEscTJ; ++b) z[a][b] = 2 * kNegSentinel;
+        for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
 
     for (int64_t tb = 0; tb < t; tb += kEscTB) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < kEscTB * kEscBI; idx += 256) {
-            int tt = idx % kEscTB, ii = idx / kEscTB;
-            int64_t gi = i0 + ii, gt = tb + tt;
-            bool ok = gi < m && gt < t;
-            sAmax[tt][ii] = ok ? amax[gi * t + gt] : kNegSentinel;
-            sAmin[tt][ii] = ok ? amin[gi * t + gt] : kNegSentinel;
+            const int ii = idx % kEscBI, tt = idx / kEscBI;
+            const int64_t gi = i0 + ii, gt = tb + tt;
+            const bool ok = gi < m && gt < t;
+            const int vx = ok ? to16(amaxT[gt * m + gi]) : kS16;
+            const int vn = ok ? to16(aminT[gt * m + gi]) : kS16;
+            sAmx[tt][ii] = pack2(vx, vx);
+            sAmn[tt][ii] = pack2(vn, vn);
         }
-        for (int idx = threadIdx.x; idx < kEscTB * kEscBJ; idx += 256) {
-            int tt = idx % kEscTB, jj = idx / kEscTB;
-            int64_t gj = j0 + jj, gt = tb + tt;
-            bool ok = gj < n && gt < t;
-            sBmax[tt][jj] = ok ? bmax[gj * t + gt] : kNegSentinel;
-            sBmin[tt][jj] = ok ? bmin[gj * t + gt] : kNegSentinel;
+        for (int idx = threadIdx.x; idx < kEscTB * kEscBJ / 2; idx += 256) {
+            const int jp = idx % (kEscBJ / 2), tt = idx / (kEscBJ / 2);
+            const int64_t gj = j0 + 2 * jp, gt = tb + tt;
+            const bool ok0 = gj < n && gt < t, ok1 = gj + 1 < n && gt < t;
+            sBmx[tt][jp] = pack2(ok0 ? to16(bmaxT[gt * n + gj]) : kS16, ok1 ? to16(bmaxT[gt * n + gj + 1]) : kS16);
+            sBmn[tt][jp] = pack2(ok0 ? to16(bminT[gt * n + gj]) : kS16, ok1 ? to16(bminT[gt * n + gj + 1]) : kS16);
         }
         __syncthreads();
 #pragma unroll 4
         for (int tt = 0; tt < kEscTB; ++tt) {
-            int4 a_mx = *reinterpret_cast<const int4*>(&sAmax[tt][ty * kEscTI]);
-            int4 a_mn = *reinterpret_cast<const int4*>(&sAmin[tt][ty * kEscTI]);
-            int4 b_mx0 = *reinterpret_cast<const int4*>(&sBmax[tt][tx * 4]);
-            int4 b_mx1 = *reinterpret_cast<const int4*>(&sBmax[tt][64 + tx * 4]);
-            int4 b_mn0 = *reinterpret_cast<const int4*>(&sBmin[tt][tx * 4]);
-            int4 b_mn1 = *reinterpret_cast<const int4*>(&sBmin[tt][64 + tx * 4]);
-            int amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
-            int amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
-            int bmx[8] = {b_mx0.x, b_mx0.y, b_mx0.z, b_mx0.w, b_mx1.x, b_mx1.y, b_mx1.z, b_mx1.w};
-            int bmn[8] = {b_mn0.x, b_mn0.y, b_mn0.z, b_mn0.w, b_mn1.x, b_mn1.y, b_mn1.z, b_mn1.w};
+            const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
+            const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
+            const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
+            const uint4 b_mn = *reinterpret_cast<const uint4*>(&sBmn[tt][tx * 4]);
+            const uint32_t amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
+            const uint32_t amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
+            const uint32_t bmx[4] = {b_mx.x, b_mx.y, b_mx.z, b_mx.w};
+            const uint32_t bmn[4] = {b_mn.x, b_mn.y, b_mn.z, b_mn.w};
 #pragma unroll
-            for (int a = 0; a < kEscTI; ++a)
+            for (int a = 0; a < 4; ++a)
 #pragma unroll
-                for (int b = 0; b < kEscTJ; ++b) {
-                    z[a][b] = __viaddmax_s32(amx[a], bmn[b], z[a][b]);
-                    z[a][b] = __viaddmax_s32(amn[a], bmx[b], z[a][b]);
+                for (int b = 0; b < 4; ++b) {
+                    z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
+                    z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
                 }
         }
     }
     int esc = 0;
 #pragma unroll
-    for (int a = 0; a < kEscTI; ++a) {
-        int64_t gi = i0 + ty * kEscTI + a;
+    for (int a = 0; a < 4; ++a) {
+        const int64_t gi = i0 + ty * 4 + a;
         if (gi >= m) continue;
-        int la = aline[gi];
+        const int la = aline[gi];
 #pragma unroll
-        for (int b = 0; b < kEscTJ; ++b) {
-            int64_t gj = j0 + (b < 4 ? tx * 4 + b : 64 + tx * 4 + (b - 4));
-            if (gj >= n) continue;
-            if (z[a][b] <= -900000) continue;  // structurally zero dot product
-            esc = max(esc, la + bline[gj] - z[a][b] + 1);
-        }
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gj = j0 + 2 * (tx * 4 + b) + h;
+                if (gj >= n) continue;
+                const int zz = int(int16_t(z[a][b] >> (16 * h)));
+                if (zz <= -8000) continue;  // structurally zero dot product
+                esc = max(esc, la + bline[gj] - zz + 1);
+            }
     }
     esc = warp_max(esc);
     if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(esc_out, esc);
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && ran_flag) *ran_flag = 1;
+}
+
+// [lines][blocks] -> [blocks][lines] (stage export of esc_coarsened, which
+// takes the reference's line-major stats).
+__global__ void transpose_i32_kernel(const int32_t* __restrict__ src, int64_t lines, int64_t blocks,
+                                     int32_t* __restrict__ dst) {
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= lines * blocks) return;
+    const int64_t line = i / blocks, b = i - line * blocks;
+    dst[b * lines + line] = src[i];
 }
 
 // Finalise a standalone esc_coarsened export: out = {esc, target+esc, slices}.
@@ -358,7 +392,7 @@ int num_sms() {
 }
 
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
-                  unsigned long long* counts, int32_t* exc_flag, int exc_bit, cudaStream_t st,
+                  unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
                   uint64_t* nlaunch) {
     const int64_t blocks = v.len == 0 ? 0 : (v.len + block_len - 1) / block_len;
     if (v.lines == 0) return;
@@ -372,16 +406,20 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
             if (grid < 1) grid = 1;
             // lines of a single row-major line: ps may be anything when len == 1
             stats_rows_kernel<<<grid, 256, 0, st>>>(w, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit);
+                                                    exc_bit, transposed);
         } else {
             dim3 grid((unsigned)((v.lines + 255) / 256), (unsigned)(blocks < 65535 ? blocks : 65535));
             stats_cols_kernel<<<grid, 256, 0, st>>>(v, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit);
+                                                    exc_bit, transposed);
         }
         ++*nlaunch;
     }
-    int lgrid = (int)((v.lines * 32 + 255) / 256);
-    line_max_kernel<<<lgrid, 256, 0, st>>>(bmax, v.lines, blocks, line_max);
+    if (transposed) {
+        line_max_t_kernel<<<(unsigned)((v.lines + 255) / 256), 256, 0, st>>>(bmax, v.lines, blocks, line_max);
+    } else {
+        int lgrid = (int)((v.lines * 32 + 255) / 256);
+        line_max_kernel<<<lgrid, 256, 0, st>>>(bmax, v.lines, blocks, line_max);
+    }
     ++*nlaunch;
 }
 
@@ -400,6 +438,13 @@ void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, 
     if (m == 0 || n == 0) return;
     dim3 grid((unsigned)((n + kEscBJ - 1) / kEscBJ), (unsigned)((m + kEscBI - 1) / kEscBI));
     esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, plan, esc_out, ran_flag);
+    ++*nlaunch;
+}
+
+void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int32_t* dst, cudaStream_t st,
+                          uint64_t* nlaunch) {
+    if (lines * blocks == 0) return;
+    transpose_i32_kernel<<<(unsigned)((lines * blocks + 255) / 256), 256, 0, st>>>(src, lines, blocks, dst);
     ++*nlaunch;
 }
 

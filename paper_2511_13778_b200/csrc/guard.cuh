@@ -6,16 +6,20 @@ namespace adpb200 {
 int num_sms();
 
 // K1: fused Inf/NaN/-0 counts + per-(line, block) exponent max/min + line max.
+// transposed = 1 stores the block stats block-major ([block][line], what the
+// ESC kernel consumes); 0 the reference's line-major [line][block].
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
-                  unsigned long long* counts, int32_t* exc_flag, int exc_bit, cudaStream_t st,
+                  unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
                   uint64_t* nlaunch);
 void launch_scan(const double* a, int64_t count, unsigned long long* counts, int32_t* exc, cudaStream_t st,
                  uint64_t* nlaunch);
-// K2: coarsened ESC (atomicMax into esc_out, which must start at 0).
+// K2: coarsened ESC over block-major stats (atomicMax into esc_out, which must start at 0).
 void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
                 const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
                 int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch);
 void launch_esc_finish(int32_t* out, int target_bits, cudaStream_t st, uint64_t* nlaunch);
+void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int32_t* dst, cudaStream_t st,
+                          uint64_t* nlaunch);
 // swap_ab: the internal operands are the user's B (A-lines) and A (B-lines).
 void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
                    int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch);

@@ -6,7 +6,7 @@
 //   recompose       proj/src/igemm.cpp:99-127  (exact combine, one RNE, alpha/beta)
 //   WideInt / round_mag_to_double   proj/include/ozadp/exactsum.hpp:50-158
 //
-// Structure (one persistent CTA per SM, 8 warps):
+// Structure (one persistent CTA per SM, 12 warps):
 //   warp 0      TMA producer: per 32-byte k-block, nsl A slice tiles
 //               (128 rows) + nsl B slice tiles (NB rows) into one stage.
 //   warp 1      MMA issuer (one thread). TMEM holds one int32 accumulator of
@@ -16,7 +16,8 @@
 //               instruction of N = c*NB whose output columns land exactly on
 //               diagonals d_a+d_b..d_a+d_b+c-1.
 //   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld the L+1 diagonals of a column batch,
+//   warps 4-11  epilogue (2 per TMEM lane quadrant, one column half each):
+//               tcgen05.ld the L+1 diagonals of a column batch,
 //               fold them exactly (Horner in NL 64-bit limbs), round once to
 //               FP64 (RNE, gradual underflow, overflow -> Inf), apply the
 //               row/column scales 2^(E_a+E_b-14-8L) and alpha/beta, store C.
@@ -31,7 +32,10 @@ namespace adpb200 {
 
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kFirstEpiWarp = 4;                  // warps 0-3: TMA, MMA, TMEM alloc, spare
+constexpr int kEpiWarps = 8;                      // 2 per TMEM lane quadrant
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreads = kFirstEpiWarp * 32 + kEpiThreads;
 constexpr int kBM = 128;      // rows of a tile (UMMA M)
 constexpr int kKB = 32;       // bytes of k per stage (one UMMA K step for int8)
 constexpr int kMaxStages = 8;
@@ -42,7 +46,7 @@ struct Cfg {
     static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
     // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
     static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
-    static constexpr int kCW = 64 / kNDMax >= 2 ? 64 / kNDMax : 2;  // columns per TMEM load batch
+    static constexpr int kCW = NB == 64 ? 8 : (NB == 32 ? 4 : (NB == 16 ? 2 : 1));  // columns per TMEM load batch
     static constexpr int kMaxGroup = 256 / NB;                 // B slices per MMA (N <= 256)
 };
 
@@ -183,6 +187,82 @@ __device__ __forceinline__ double round_limbs(uint64_t (&S)[NL], int exp2) {
     return __longlong_as_double((long long)bits);
 }
 
+// Fast path of the fold + rounding for the 8-diagonal variant (L <= 7): the
+// exact sum fits a signed 128-bit integer; normal results need one
+// normalising shift, the rounding increment is added to the packed
+// exponent|mantissa word (so a mantissa carry bumps the exponent and a carry
+// out of the largest finite value lands exactly on +/-Inf). Subnormal
+// results defer to the generic limb rounding.
+__device__ __forceinline__ double round_i128(__int128 S, int exp2) {
+    typedef unsigned __int128 u128;
+    if (S == 0) return 0.0;
+    const bool neg = S < 0;
+    const u128 mag = neg ? u128(-S) : u128(S);
+    const uint64_t hi = uint64_t(mag >> 64), lo = uint64_t(mag);
+    const int top = hi ? 127 - __clzll((long long)hi) : 63 - __clzll((long long)lo);
+    const int e = top + exp2;
+    if (e < -1022) {
+        uint64_t L2[2] = {uint64_t(S), uint64_t(u128(S) >> 64)};
+        return round_limbs<2>(L2, exp2);
+    }
+    const u128 W = mag << (127 - top);
+    const uint64_t wh = uint64_t(W >> 64);
+    const uint64_t m = wh >> 11;  // 53 bits, leading one at bit 52
+    const uint64_t sticky = (wh & 0x3FFull) | uint64_t(W);
+    const uint64_t inc = (wh >> 10) & 1 & ((sticky != 0) | (m & 1));
+    uint64_t bits = e > 1023 ? 0x7FF0000000000000ull : (uint64_t(e + 1022) << 52) + m + inc;
+    if (bits > 0x7FF0000000000000ull) bits = 0x7FF0000000000000ull;
+    if (neg) bits |= 1ull << 63;
+    return __longlong_as_double((long long)bits);
+}
+
+// One MMA of the per-k-block schedule: D[tmem col] (+)= A slice * stacked B slices.
+struct MmaOp {
+    uint32_t col;     // TMEM column of the first diagonal written
+    uint32_t a_off;   // byte offset of the A slice tile inside the stage
+    uint32_t b_off;   // byte offset of the first B slice tile inside the stage
+    uint32_t idesc;   // instruction descriptor (N = slices * NB)
+};
+constexpr int kMaxOps = 192;
+
+template <int NB>
+__device__ int build_schedule(int s, int L, bool first, MmaOp* ops, uint32_t* acc_mask) {
+    using C = Cfg<NB>;
+    int n = 0;
+    const int da_max = s - 1 < L ? s - 1 : L;
+    for (int da = 0; da <= da_max; ++da) {
+        const int nb = (s - 1 < L - da ? s - 1 : L - da) + 1;
+        // in the first k-block of an accumulation chunk, d_a >= 1 may open one
+        // new diagonal (d_b = s - 1) which must start with accumulate = 0
+        const bool opens = first && da >= 1 && da + s - 1 <= L;
+        const int nb_main = opens ? nb - 1 : nb;
+        const bool acc = !(first && da == 0);
+        for (int db = 0; db < nb_main;) {
+            int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
+            if (NB == 8 && cnt > 1 && (cnt & 1)) --cnt;  // N = 8 or a multiple of 16
+            ops[n] = MmaOp{uint32_t((da + db) * NB), uint32_t(da * (kBM * kKB)), uint32_t(db * (NB * kKB)),
+                           tc::idesc_i8(kBM, cnt * NB)};
+            if (acc) acc_mask[n >> 5] |= 1u << (n & 31);
+            ++n;
+            db += cnt;
+        }
+        if (opens) {
+            ops[n] = MmaOp{uint32_t((da + nb - 1) * NB), uint32_t(da * (kBM * kKB)), uint32_t((nb - 1) * (NB * kKB)),
+                           tc::idesc_i8(kBM, NB)};
+            ++n;
+        }
+    }
+    return n;
+}
+
+struct alignas(16) SmemSched {
+    MmaOp first[kMaxOps];
+    MmaOp rest[kMaxOps];
+    uint32_t first_acc[kMaxOps / 32];
+    uint32_t rest_acc[kMaxOps / 32];
+    int n_first, n_rest;
+};
+
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs g) {
@@ -201,10 +281,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     SmemHeader* hdr = reinterpret_cast<SmemHeader*>(smem);
-    uint8_t* stages = smem + 1024;
+    SmemSched* sched = reinterpret_cast<SmemSched*>(smem + 1024);
+    uint8_t* stages = smem + 1024 + ((sizeof(SmemSched) + 1023) / 1024) * 1024;
     const uint32_t a_bytes = uint32_t(nsl) * kBM * kKB;
     const uint32_t stage_bytes = uint32_t(nsl) * (kBM + NB) * kKB;
-    const uint32_t avail = uint32_t(g.smem_bytes) - 2048;
+    const uint32_t avail = uint32_t(g.smem_bytes) - 1024 - uint32_t(stages - smem);
     int nstages = int(avail / stage_bytes);
     if (nstages > kMaxStages) nstages = kMaxStages;
 
@@ -215,8 +296,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&hdr->empty[i], 1);
         }
         tc::mbar_init(&hdr->tmem_full, 1);
-        tc::mbar_init(&hdr->tmem_empty, 128);
+        tc::mbar_init(&hdr->tmem_empty, kEpiThreads);
         tc::fence_barrier_init();
+    }
+    if (threadIdx.x == 32) {
+        for (int i = 0; i < kMaxOps / 32; ++i) sched->first_acc[i] = sched->rest_acc[i] = 0;
+        sched->n_first = build_schedule<NB>(s, L, true, sched->first, sched->first_acc);
+        sched->n_rest = build_schedule<NB>(s, L, false, sched->rest, sched->rest_acc);
     }
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(&tmap_a);
@@ -256,11 +342,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
+        // ===== MMA issuer: replays the precomputed schedule every k-block =====
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
-            const int da_max = s - 1 < L ? s - 1 : L;
+            const int n_first = sched->n_first, n_rest = sched->n_rest;
+            const uint32_t stage0 = tc::smem_u32(stages);
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
                 for (int c = 0; c < nchunks; ++c) {
                     tc::mbar_wait(&hdr->tmem_empty, acc_phase ^ 1);
@@ -270,28 +357,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int64_t kb = kb0; kb < kb1; ++kb) {
                         tc::mbar_wait(&hdr->full[stage], phase);
                         tc::fence_after();
-                        const uint32_t sa = tc::smem_u32(stages + size_t(stage) * stage_bytes);
+                        const uint32_t sa = stage0 + uint32_t(stage) * stage_bytes;
                         const uint32_t sb = sa + a_bytes;
                         const bool first = kb == kb0;
-                        for (int da = 0; da <= da_max; ++da) {
-                            const int nb = (s - 1 < L - da ? s - 1 : L - da) + 1;
-                            const uint64_t adesc = tc::smem_desc_sw32(sa + da * (kBM * kKB));
-                            // in the first k-block, d_a >= 1 may open one new diagonal (d_b = s-1)
-                            const bool opens = first && da >= 1 && da + s - 1 <= L;
-                            const int nb_main = opens ? nb - 1 : nb;
-                            const uint32_t acc_main = (first && da == 0) ? 0u : 1u;
-                            for (int db = 0; db < nb_main;) {
-                                int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
-                                if (NB == 8 && cnt > 1 && (cnt & 1)) --cnt;  // N = 8 or a multiple of 16
-                                tc::mma_i8(tmem_base + uint32_t((da + db) * NB), adesc,
-                                           tc::smem_desc_sw32(sb + db * (NB * kKB)), tc::idesc_i8(kBM, cnt * NB),
-                                           acc_main);
-                                db += cnt;
-                            }
-                            if (opens)
-                                tc::mma_i8(tmem_base + uint32_t((da + nb - 1) * NB), adesc,
-                                           tc::smem_desc_sw32(sb + (nb - 1) * (NB * kKB)), tc::idesc_i8(kBM, NB),
-                                           0u);
+                        const MmaOp* ops = first ? sched->first : sched->rest;
+                        const uint32_t* accm = first ? sched->first_acc : sched->rest_acc;
+                        const int n = first ? n_first : n_rest;
+                        for (int i = 0; i < n; ++i) {
+                            const MmaOp op = ops[i];
+                            tc::mma_i8(tmem_base + op.col, tc::smem_desc_sw32(sa + op.a_off),
+                                       tc::smem_desc_sw32(sb + op.b_off), op.idesc, (accm[i >> 5] >> (i & 31)) & 1u);
                         }
                         tc::mma_commit(&hdr->empty[stage]);
                         if (++stage == nstages) {
@@ -304,9 +379,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp >= 4) {
-        // ===== epilogue =====
-        const int q = warp & 3;  // TMEM lane quadrant
+    } else if (warp >= kFirstEpiWarp) {
+        // ===== epilogue: 8 warps, (lane quadrant, column half) each =====
+        const int ew = warp - kFirstEpiWarp;
+        const int q = warp & 3;             // TMEM lane quadrant (warp id % 4)
+        const int jh = ew / 4;              // column half
+        constexpr int kCols = NB / 2;       // columns per epilogue warp
         uint32_t acc_phase = 0;
         const int exp_base = -14 - 8 * L;
         for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -320,7 +398,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::fence_after();
                 const bool last = c == nchunks - 1;
                 const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
-                for (int j0 = 0; j0 < NB; j0 += C::kCW) {
+#pragma unroll 1
+                for (int j0 = jh * kCols; j0 < (jh + 1) * kCols; j0 += C::kCW) {
+                    int eb[C::kCW];
+#pragma unroll
+                    for (int cc = 0; cc < C::kCW; ++cc) {
+                        const int64_t col = nt * NB + j0 + cc;
+                        eb[cc] = col < g.N ? __ldg(g.scale_b + col) : 0;
+                    }
                     uint32_t v[C::kNDMax][C::kCW];
 #pragma unroll
                     for (int D = 0; D < C::kNDMax; ++D)
@@ -338,14 +423,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                             continue;
                         }
                         uint64_t S[C::kNL];
-                        {
-                            int64_t x0 = int32_t(v[0][cc]);
+                        if constexpr (C::kNL == 2) {
+                            // S = sum_D acc_D 256^(L-D), L <= 7: two int64 Horner halves
+                            int64_t h = int32_t(v[0][cc]);
+#pragma unroll
+                            for (int D = 1; D < 4; ++D)
+                                if (D < ndiag) h = h * 256 + int32_t(v[D][cc]);
+                            __int128 S128 = h;
+                            if (ndiag > 4) {
+                                int64_t l = int32_t(v[4][cc]);
+#pragma unroll
+                                for (int D = 5; D < 8; ++D)
+                                    if (D < ndiag) l = l * 256 + int32_t(v[D][cc]);
+                                S128 = (__int128(h) << (8 * (L - 3))) + l;
+                            }
+                            S[0] = uint64_t(S128);
+                            S[1] = uint64_t((unsigned __int128)S128 >> 64);
+                        } else {
+                            const int64_t x0 = int32_t(v[0][cc]);
 #pragma unroll
                             for (int i = 0; i < C::kNL; ++i) S[i] = i == 0 ? uint64_t(x0) : (x0 < 0 ? ~0ull : 0ull);
-                        }
 #pragma unroll
-                        for (int D = 1; D < C::kNDMax; ++D)
-                            if (D < ndiag) limbs_shl8_add<C::kNL>(S, int64_t(int32_t(v[D][cc])));
+                            for (int D = 1; D < C::kNDMax; ++D)
+                                if (D < ndiag) limbs_shl8_add<C::kNL>(S, int64_t(int32_t(v[D][cc])));
+                        }
                         if (nchunks > 1) {
                             // per-CTA scratch: this CTA runs all chunks of the tile back to back
                             uint64_t* P = g.partial + size_t(blockIdx.x) * (C::kNL * NB * kBM) +
@@ -363,7 +464,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 continue;
                             }
                         }
-                        const double vv = round_limbs<C::kNL>(S, ea + g.scale_b[col] + exp_base);
+                        double vv;
+                        if constexpr (C::kNL == 2)
+                            vv = round_i128(__int128((unsigned __int128)S[1] << 64 | S[0]), ea + eb[cc] + exp_base);
+                        else
+                            vv = round_limbs<C::kNL>(S, ea + eb[cc] + exp_base);
                         double r = __dmul_rn(g.alpha, vv);
                         if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
                         g.c_out[row + col * g.ldc] = r;
