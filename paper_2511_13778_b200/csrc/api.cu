@@ -235,9 +235,6 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         launch_slice(P.b, bline, pb, Lw.pitch, Lw.pitch * P.N, 1, sb, plan, fixed_slices, cap, st, nl);
         tm.end(3);
         // K4/K5: one launch per GEMM variant; exactly one does work
-        CUtensorMap ta;
-        if (!make_plane_map(&ta, pa, P.M, Lw.pitch / 32, cap, 128))
-            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for A planes");
         GemmArgs g{};
         g.plan = plan;
         g.M = P.M;
@@ -262,10 +259,8 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                 fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
                 if (hp.variant != nb) continue;
             }
-            CUtensorMap tb;
-            if (!make_plane_map(&tb, pb, P.N, Lw.pitch / 32, cap, nb))
-                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for B planes");
-            if (launch_igemm(nb, ta, tb, g, st, nl)) return fail(ADPB200_ERR_RUNTIME, "bad GEMM variant");
+            if (launch_igemm(nb, pa, pb, Lw.pitch / 32, cap, g, st, nl))
+                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
         }
         tm.end(4);
     }

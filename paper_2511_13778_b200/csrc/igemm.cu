@@ -47,7 +47,6 @@ struct Cfg {
     // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
     static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
     static constexpr int kCW = NB == 64 ? 8 : (NB == 32 ? 4 : (NB == 16 ? 2 : 1));  // columns per TMEM load batch
-    static constexpr int kMaxGroup = 256 / NB;                 // B slices per MMA (N <= 256)
 };
 
 struct alignas(8) SmemHeader {
@@ -216,19 +215,29 @@ __device__ __forceinline__ double round_i128(__int128 S, int exp2) {
     return __longlong_as_double((long long)bits);
 }
 
-// One MMA of the per-k-block schedule: D[tmem col] (+)= A slice * stacked B slices.
+// ---- the per-k-block MMA schedule ------------------------------------------------
+// One MMA: D[tmem col] (+)= A slice d_a (128 x 32) * B slices d_b..d_b+c-1
+// stacked along N (c*NB x 32). The schedule is identical for every k-block
+// except the first of an accumulation chunk (accumulate flags). For the
+// common (s, L) pairs it is a compile-time constant, so the converged MMA
+// warp issues it fully unrolled with immediate descriptor offsets (a runtime
+// schedule costs ~200 cycles of elect/R2UR per tcgen05.mma, more than a
+// small-N MMA takes to execute).
 struct MmaOp {
-    uint32_t col;     // TMEM column of the first diagonal written
-    uint32_t a_off;   // byte offset of the A slice tile inside the stage
-    uint32_t b_off;   // byte offset of the first B slice tile inside the stage
-    uint32_t idesc;   // instruction descriptor (N = slices * NB)
+    uint32_t col;    // TMEM column of the first diagonal written
+    uint32_t a_off;  // byte offset of the A slice tile inside the stage
+    uint32_t b_off;  // byte offset of the first B slice tile inside the B region
+    uint32_t idesc;  // instruction descriptor (N = c*NB)
+    uint32_t acc;    // accumulate into D (0: overwrite)
 };
-constexpr int kMaxOps = 192;
+constexpr int kMaxOps = 160;
 
+// Writes the schedule into out[] and returns its length; usable at compile
+// time (StaticSched) and at run time (into shared memory).
 template <int NB>
-__device__ int build_schedule(int s, int L, bool first, MmaOp* ops, uint32_t* acc_mask) {
-    using C = Cfg<NB>;
+__host__ __device__ constexpr int fill_schedule(MmaOp* out, int s, int L, bool first) {
     int n = 0;
+    const int max_group = 256 / NB;
     const int da_max = s - 1 < L ? s - 1 : L;
     for (int da = 0; da <= da_max; ++da) {
         const int nb = (s - 1 < L - da ? s - 1 : L - da) + 1;
@@ -236,62 +245,180 @@ __device__ int build_schedule(int s, int L, bool first, MmaOp* ops, uint32_t* ac
         // new diagonal (d_b = s - 1) which must start with accumulate = 0
         const bool opens = first && da >= 1 && da + s - 1 <= L;
         const int nb_main = opens ? nb - 1 : nb;
-        const bool acc = !(first && da == 0);
+        const uint32_t acc = (first && da == 0) ? 0u : 1u;
         for (int db = 0; db < nb_main;) {
-            int cnt = nb_main - db < C::kMaxGroup ? nb_main - db : C::kMaxGroup;
+            int cnt = nb_main - db < max_group ? nb_main - db : max_group;
             if (NB == 8 && cnt > 1 && (cnt & 1)) --cnt;  // N = 8 or a multiple of 16
-            ops[n] = MmaOp{uint32_t((da + db) * NB), uint32_t(da * (kBM * kKB)), uint32_t(db * (NB * kKB)),
-                           tc::idesc_i8(kBM, cnt * NB)};
-            if (acc) acc_mask[n >> 5] |= 1u << (n & 31);
+            out[n] = MmaOp{uint32_t((da + db) * NB), uint32_t(da * (kBM * kKB)), uint32_t(db * (NB * kKB)),
+                           (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t((cnt * NB) >> 3) << 17) |
+                               (uint32_t(kBM >> 4) << 24),
+                           acc};
             ++n;
             db += cnt;
         }
         if (opens) {
-            ops[n] = MmaOp{uint32_t((da + nb - 1) * NB), uint32_t(da * (kBM * kKB)), uint32_t((nb - 1) * (NB * kKB)),
-                           tc::idesc_i8(kBM, NB)};
+            out[n] = MmaOp{uint32_t((da + nb - 1) * NB), uint32_t(da * (kBM * kKB)), uint32_t((nb - 1) * (NB * kKB)),
+                           (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(NB >> 3) << 17) | (uint32_t(kBM >> 4) << 24),
+                           0u};
             ++n;
         }
     }
     return n;
 }
 
+template <int NB, int S, int L, bool F>
+struct StaticSched {
+    MmaOp ops[kMaxOps];
+    int n;
+    __host__ __device__ constexpr StaticSched() : ops{}, n(fill_schedule<NB>(ops, S, L, F)) {}
+};
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// TMA boxes of 1..kMaxBox slices; a stage's nsl slices of A (or B) are one box.
+constexpr int kMaxBox = 18;
+struct PlaneMaps {
+    CUtensorMap a[kMaxBox];
+    CUtensorMap b[kMaxBox];
+};
+
 struct alignas(16) SmemSched {
     MmaOp first[kMaxOps];
     MmaOp rest[kMaxOps];
-    uint32_t first_acc[kMaxOps / 32];
-    uint32_t rest_acc[kMaxOps / 32];
     int n_first, n_rest;
 };
 
+// Loop state shared by the producer / MMA / epilogue roles.
+struct Loop {
+    int64_t tiles_m, tiles_n, ntiles, nkb, kb_per_chunk;
+    int nchunks, nstages;
+    uint32_t a_bytes, stage_bytes;
+};
+
+// The MMA role, converged warp; SCHED = compile-time (S, L) or runtime smem.
+template <int NB, int S, int L>
+__device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const SmemSched* sched, uint32_t stage0,
+                                         uint32_t tmem_base) {
+    constexpr bool kStatic = S > 0;
+    int stage = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
+        for (int c = 0; c < lp.nchunks; ++c) {
+            tc::mbar_wait(&hdr->tmem_empty, acc_phase ^ 1);
+            tc::fence_after();
+            const int64_t kb0 = int64_t(c) * lp.kb_per_chunk;
+            const int64_t kb1 = kb0 + lp.kb_per_chunk < lp.nkb ? kb0 + lp.kb_per_chunk : lp.nkb;
+            for (int64_t kb = kb0; kb < kb1; ++kb) {
+                tc::mbar_wait(&hdr->full[stage], phase);
+                tc::fence_after();
+                const uint32_t sa = stage0 + uint32_t(stage) * lp.stage_bytes;
+                const uint32_t sb = sa + lp.a_bytes;
+                const uint64_t da = tc::smem_desc_sw32(sa), db = tc::smem_desc_sw32(sb);
+                const bool first = kb == kb0;
+                if (elect_one()) {
+                    if constexpr (kStatic) {
+                        constexpr StaticSched<NB, S, L, true> F{};
+                        constexpr StaticSched<NB, S, L, false> R{};
+                        if (first) {
+#pragma unroll
+                            for (int i = 0; i < F.n; ++i)
+                                tc::mma_i8(tmem_base + F.ops[i].col, da + (F.ops[i].a_off >> 4),
+                                           db + (F.ops[i].b_off >> 4), F.ops[i].idesc, F.ops[i].acc);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < R.n; ++i)
+                                tc::mma_i8(tmem_base + R.ops[i].col, da + (R.ops[i].a_off >> 4),
+                                           db + (R.ops[i].b_off >> 4), R.ops[i].idesc, R.ops[i].acc);
+                        }
+                    } else {
+                        const MmaOp* ops = first ? sched->first : sched->rest;
+                        const int n = first ? sched->n_first : sched->n_rest;
+                        for (int i = 0; i < n; ++i) {
+                            const MmaOp op = ops[i];
+                            tc::mma_i8(tmem_base + op.col, da + (op.a_off >> 4), db + (op.b_off >> 4), op.idesc,
+                                       op.acc);
+                        }
+                    }
+                    tc::mma_commit(&hdr->empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == lp.nstages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (elect_one()) tc::mma_commit(&hdr->tmem_full);
+            __syncwarp();
+            acc_phase ^= 1;
+        }
+    }
+}
+
+// (S, L) pairs with a compile-time schedule: the ADPB200_PAIRS_TARGET
+// policy (L = s) and the reference's Full pair set (L = 2s - 2) for the slice
+// counts each variant serves; anything else runs the runtime schedule.
+template <int NB>
+__device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemHeader* hdr, const SmemSched* sched,
+                                             uint32_t stage0, uint32_t tmem_base) {
+#define ADPB200_MMA_CASE(S_, L_)                                          \
+    if (s == S_ && L == L_) {                                             \
+        mma_role<NB, S_, L_>(lp, hdr, sched, stage0, tmem_base);          \
+        return;                                                           \
+    }
+    if constexpr (NB == 64) {
+        ADPB200_MMA_CASE(1, 0) ADPB200_MMA_CASE(2, 2) ADPB200_MMA_CASE(3, 3) ADPB200_MMA_CASE(4, 4)
+        ADPB200_MMA_CASE(5, 5) ADPB200_MMA_CASE(6, 6) ADPB200_MMA_CASE(7, 7) ADPB200_MMA_CASE(3, 4)
+        ADPB200_MMA_CASE(4, 6)
+    } else if constexpr (NB == 32) {
+        ADPB200_MMA_CASE(8, 8) ADPB200_MMA_CASE(9, 9) ADPB200_MMA_CASE(10, 10) ADPB200_MMA_CASE(11, 11)
+        ADPB200_MMA_CASE(12, 12) ADPB200_MMA_CASE(13, 13) ADPB200_MMA_CASE(14, 14) ADPB200_MMA_CASE(15, 15)
+        ADPB200_MMA_CASE(5, 8) ADPB200_MMA_CASE(6, 10) ADPB200_MMA_CASE(7, 12) ADPB200_MMA_CASE(8, 14)
+    } else if constexpr (NB == 16) {
+        ADPB200_MMA_CASE(16, 16) ADPB200_MMA_CASE(17, 17) ADPB200_MMA_CASE(18, 18) ADPB200_MMA_CASE(9, 16)
+        ADPB200_MMA_CASE(10, 18) ADPB200_MMA_CASE(11, 20) ADPB200_MMA_CASE(12, 22)
+    }
+#undef ADPB200_MMA_CASE
+    mma_role<NB, 0, 0>(lp, hdr, sched, stage0, tmem_base);
+}
+
 template <int NB>
 __global__ void __launch_bounds__(kThreads, 1)
-    igemm_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b, GemmArgs g) {
+    igemm_kernel(const __grid_constant__ PlaneMaps maps, GemmArgs g) {
     using C = Cfg<NB>;
     const Plan* plan = g.plan;
     if (plan->path != ADPB200_PATH_EMULATED || plan->variant != NB) return;
     const int s = plan->slices, L = plan->L, nsl = plan->nsl;
     const int ndiag = L + 1;
-    const int64_t kchunk = plan->kchunk;
-    const int64_t nkb = (g.K + kKB - 1) / kKB;
-    const int64_t kb_per_chunk = kchunk / kKB;
-    const int nchunks = (int)((nkb + kb_per_chunk - 1) / kb_per_chunk);
-    const int64_t tiles_m = (g.M + kBM - 1) / kBM, tiles_n = (g.N + NB - 1) / NB;
-    const int64_t ntiles = tiles_m * tiles_n;
+    Loop lp;
+    lp.nkb = (g.K + kKB - 1) / kKB;
+    lp.kb_per_chunk = plan->kchunk / kKB;
+    lp.nchunks = (int)((lp.nkb + lp.kb_per_chunk - 1) / lp.kb_per_chunk);
+    lp.tiles_m = (g.M + kBM - 1) / kBM;
+    lp.tiles_n = (g.N + NB - 1) / NB;
+    lp.ntiles = lp.tiles_m * lp.tiles_n;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     SmemHeader* hdr = reinterpret_cast<SmemHeader*>(smem);
     SmemSched* sched = reinterpret_cast<SmemSched*>(smem + 1024);
     uint8_t* stages = smem + 1024 + ((sizeof(SmemSched) + 1023) / 1024) * 1024;
-    const uint32_t a_bytes = uint32_t(nsl) * kBM * kKB;
-    const uint32_t stage_bytes = uint32_t(nsl) * (kBM + NB) * kKB;
+    lp.a_bytes = uint32_t(nsl) * kBM * kKB;
+    lp.stage_bytes = uint32_t(nsl) * (kBM + NB) * kKB;
     const uint32_t avail = uint32_t(g.smem_bytes) - 1024 - uint32_t(stages - smem);
-    int nstages = int(avail / stage_bytes);
-    if (nstages > kMaxStages) nstages = kMaxStages;
+    lp.nstages = int(avail / lp.stage_bytes);
+    if (lp.nstages > kMaxStages) lp.nstages = kMaxStages;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < nstages; ++i) {
+        for (int i = 0; i < lp.nstages; ++i) {
             tc::mbar_init(&hdr->full[i], 1);
             tc::mbar_init(&hdr->empty[i], 1);
         }
@@ -300,13 +427,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::fence_barrier_init();
     }
     if (threadIdx.x == 32) {
-        for (int i = 0; i < kMaxOps / 32; ++i) sched->first_acc[i] = sched->rest_acc[i] = 0;
-        sched->n_first = build_schedule<NB>(s, L, true, sched->first, sched->first_acc);
-        sched->n_rest = build_schedule<NB>(s, L, false, sched->rest, sched->rest_acc);
+        sched->n_first = fill_schedule<NB>(sched->first, s, L, true);
+        sched->n_rest = fill_schedule<NB>(sched->rest, s, L, false);
     }
+    const bool boxed = nsl <= kMaxBox;
+    const CUtensorMap* map_a = &maps.a[boxed ? nsl - 1 : 0];
+    const CUtensorMap* map_b = &maps.b[boxed ? nsl - 1 : 0];
     if (warp == 0 && lane == 0) {
-        tc::tma_prefetch(&tmap_a);
-        tc::tma_prefetch(&tmap_b);
+        tc::tma_prefetch(map_a);
+        tc::tma_prefetch(map_b);
     }
     if (warp == 2) tc::tmem_alloc(&hdr->tmem_slot, 512);
     tc::fence_before();
@@ -315,88 +444,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = hdr->tmem_slot;
 
     if (warp == 0) {
-        // ===== TMA producer =====
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                int64_t mt, nt;
-                tile_coords(tile, tiles_m, tiles_n, mt, nt);
-                for (int64_t kb = 0; kb < nkb; ++kb) {
-                    tc::mbar_wait(&hdr->empty[stage], phase ^ 1);
-                    uint8_t* sa = stages + size_t(stage) * stage_bytes;
-                    uint8_t* sb = sa + a_bytes;
-                    tc::mbar_expect_tx(&hdr->full[stage], stage_bytes);
-                    for (int d = 0; d < nsl; ++d) {
-                        // blocked planes: (32 B, line, k-block, slice) -> one contiguous box
-                        tc::tma_load_4d(sa + d * (kBM * kKB), &tmap_a, &hdr->full[stage], 0, int(mt * kBM),
-                                        int(kb), d);
-                        tc::tma_load_4d(sb + d * (NB * kKB), &tmap_b, &hdr->full[stage], 0, int(nt * NB),
-                                        int(kb), d);
+        // ===== TMA producer (converged warp, one elected lane issues) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
+            int64_t mt, nt;
+            tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
+            for (int64_t kb = 0; kb < lp.nkb; ++kb) {
+                tc::mbar_wait(&hdr->empty[stage], phase ^ 1);
+                if (elect_one()) {
+                    uint8_t* sa = stages + size_t(stage) * lp.stage_bytes;
+                    uint8_t* sb = sa + lp.a_bytes;
+                    tc::mbar_expect_tx(&hdr->full[stage], lp.stage_bytes);
+                    if (boxed) {
+                        // blocked planes (32 B, line, k-block, slice): all nsl slices in one box
+                        tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * kBM), int(kb), 0);
+                        tc::tma_load_4d(sb, map_b, &hdr->full[stage], 0, int(nt * NB), int(kb), 0);
+                    } else {
+                        for (int d = 0; d < nsl; ++d) {
+                            tc::tma_load_4d(sa + d * (kBM * kKB), map_a, &hdr->full[stage], 0, int(mt * kBM),
+                                            int(kb), d);
+                            tc::tma_load_4d(sb + d * (NB * kKB), map_b, &hdr->full[stage], 0, int(nt * NB),
+                                            int(kb), d);
+                        }
                     }
-                    if (++stage == nstages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+                }
+                __syncwarp();
+                if (++stage == lp.nstages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer: replays the precomputed schedule every k-block =====
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            const int n_first = sched->n_first, n_rest = sched->n_rest;
-            const uint32_t stage0 = tc::smem_u32(stages);
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < nchunks; ++c) {
-                    tc::mbar_wait(&hdr->tmem_empty, acc_phase ^ 1);
-                    tc::fence_after();
-                    const int64_t kb0 = int64_t(c) * kb_per_chunk;
-                    const int64_t kb1 = kb0 + kb_per_chunk < nkb ? kb0 + kb_per_chunk : nkb;
-                    for (int64_t kb = kb0; kb < kb1; ++kb) {
-                        tc::mbar_wait(&hdr->full[stage], phase);
-                        tc::fence_after();
-                        const uint32_t sa = stage0 + uint32_t(stage) * stage_bytes;
-                        const uint32_t sb = sa + a_bytes;
-                        const bool first = kb == kb0;
-                        const MmaOp* ops = first ? sched->first : sched->rest;
-                        const uint32_t* accm = first ? sched->first_acc : sched->rest_acc;
-                        const int n = first ? n_first : n_rest;
-                        for (int i = 0; i < n; ++i) {
-                            const MmaOp op = ops[i];
-                            tc::mma_i8(tmem_base + op.col, tc::smem_desc_sw32(sa + op.a_off),
-                                       tc::smem_desc_sw32(sb + op.b_off), op.idesc, (accm[i >> 5] >> (i & 31)) & 1u);
-                        }
-                        tc::mma_commit(&hdr->empty[stage]);
-                        if (++stage == nstages) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                    }
-                    tc::mma_commit(&hdr->tmem_full);
-                    acc_phase ^= 1;
-                }
-            }
-        }
+        // ===== MMA issuer (converged warp, one elected lane issues) =====
+        mma_dispatch<NB>(s, L, lp, hdr, sched, tc::smem_u32(stages), tmem_base);
     } else if (warp >= kFirstEpiWarp) {
         // ===== epilogue: 8 warps, (lane quadrant, column half) each =====
         const int ew = warp - kFirstEpiWarp;
-        const int q = warp & 3;             // TMEM lane quadrant (warp id % 4)
-        const int jh = ew / 4;              // column half
-        constexpr int kCols = NB / 2;       // columns per epilogue warp
+        const int q = warp & 3;        // TMEM lane quadrant (warp id % 4)
+        const int jh = ew / 4;         // column half
+        constexpr int kCols = NB / 2;  // columns per epilogue warp
         uint32_t acc_phase = 0;
         const int exp_base = -14 - 8 * L;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
             int64_t mt, nt;
-            tile_coords(tile, tiles_m, tiles_n, mt, nt);
+            tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
             const int64_t row = mt * kBM + q * 32 + lane;
             const bool row_ok = row < g.M;
             const int ea = row_ok ? g.scale_a[row] : 0;
-            for (int c = 0; c < nchunks; ++c) {
+            for (int c = 0; c < lp.nchunks; ++c) {
                 tc::mbar_wait(&hdr->tmem_full, acc_phase);
                 tc::fence_after();
-                const bool last = c == nchunks - 1;
+                const bool last = c == lp.nchunks - 1;
                 const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
 #pragma unroll 1
                 for (int j0 = jh * kCols; j0 < (jh + 1) * kCols; j0 += C::kCW) {
@@ -447,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int D = 1; D < C::kNDMax; ++D)
                                 if (D < ndiag) limbs_shl8_add<C::kNL>(S, int64_t(int32_t(v[D][cc])));
                         }
-                        if (nchunks > 1) {
+                        if (lp.nchunks > 1) {
                             // per-CTA scratch: this CTA runs all chunks of the tile back to back
                             uint64_t* P = g.partial + size_t(blockIdx.x) * (C::kNL * NB * kBM) +
                                           size_t(j0 + cc) * kBM + (q * 32 + lane);
@@ -504,6 +604,23 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+// Blocked planes: plane d = [k-block][line][32 B]; a box is 32 B x box_rows
+// lines of one k-block x box_slices consecutive slices — box_slices
+// contiguous runs of box_rows*32 B in HBM, landing slice-major in smem.
+bool encode_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t nkb, int cap, int box_rows,
+                      int box_slices) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {cuuint64_t(kKB), cuuint64_t(lines), cuuint64_t(nkb), cuuint64_t(cap)};
+    cuuint64_t strides[3] = {cuuint64_t(kKB), cuuint64_t(kKB * lines), cuuint64_t(kKB * lines * nkb)};
+    cuuint32_t box[4] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1, cuuint32_t(box_slices)};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 template <int NB>
 void set_attr_once() {
     static bool done = false;
@@ -513,25 +630,42 @@ void set_attr_once() {
     }
 }
 
+// Encoded maps are cached per (planes, shape, variant): re-encoding ~90 maps
+// per call would cost ~0.1 ms of host time.
+struct MapCacheEntry {
+    const int8_t* pa = nullptr;
+    const int8_t* pb = nullptr;
+    int64_t M = -1, N = -1, nkb = -1;
+    int cap = -1, nb = -1;
+    PlaneMaps maps;
+};
+
 }  // namespace
 
-// Blocked planes: plane d = [k-block][line][32 B]; a box is 32 B x box_rows
-// lines of one k-block of one slice = one contiguous run in HBM.
-bool make_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t nkb, int cap, int box_rows) {
-    EncodeTiledFn enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[4] = {cuuint64_t(kKB), cuuint64_t(lines), cuuint64_t(nkb), cuuint64_t(cap)};
-    cuuint64_t strides[3] = {cuuint64_t(kKB), cuuint64_t(kKB * lines), cuuint64_t(kKB * lines * nkb)};
-    cuuint32_t box[4] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1, 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
-int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t st,
-                 uint64_t* nlaunch) {
+int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t nkb, int cap, const GemmArgs& g,
+                 cudaStream_t st, uint64_t* nlaunch) {
+    static thread_local MapCacheEntry cache[4];
+    const int slot = nb == 64 ? 0 : (nb == 32 ? 1 : (nb == 16 ? 2 : 3));
+    MapCacheEntry& e = cache[slot];
+    if (e.pa != planes_a || e.pb != planes_b || e.M != g.M || e.N != g.N || e.nkb != nkb || e.cap != cap ||
+        e.nb != nb) {
+        const int nbox = cap < kMaxBox ? cap : kMaxBox;
+        for (int i = 0; i < kMaxBox; ++i) {
+            const int bs = i < nbox ? i + 1 : 1;
+            if (!encode_plane_map(&e.maps.a[i], planes_a, g.M, nkb, cap, kBM, bs) ||
+                !encode_plane_map(&e.maps.b[i], planes_b, g.N, nkb, cap, nb, bs)) {
+                e.pa = nullptr;
+                return -1;
+            }
+        }
+        e.pa = planes_a;
+        e.pb = planes_b;
+        e.M = g.M;
+        e.N = g.N;
+        e.nkb = nkb;
+        e.cap = cap;
+        e.nb = nb;
+    }
     const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + nb - 1) / nb);
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
@@ -540,22 +674,22 @@ int launch_igemm(int nb, const CUtensorMap& ta, const CUtensorMap& tb, const Gem
     switch (nb) {
         case 64:
             set_attr_once<64>();
-            igemm_kernel<64><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            igemm_kernel<64><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 32:
             set_attr_once<32>();
-            igemm_kernel<32><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            igemm_kernel<32><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 16:
             set_attr_once<16>();
-            igemm_kernel<16><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            igemm_kernel<16><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 8:
             set_attr_once<8>();
-            igemm_kernel<8><<<grid, kThreads, kGemmSmemBytes, st>>>(ta, tb, a);
+            igemm_kernel<8><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         default:
-            return -1;
+            return -2;
     }
     ++*nlaunch;
     return 0;
