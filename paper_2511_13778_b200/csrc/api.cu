@@ -251,7 +251,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         g.partial = at<uint64_t>(h, Lw.partial);
         g.dump = dump;
         g.ndump = ndump;
-        int variants[4] = {64, 32, 16, 8};
+        int variants[5] = {64, 48, 32, 16, 8};
         tm.begin(4);
         for (int nb : variants) {
             if (fixed_slices > 0) {  // the host knows the variant

@@ -171,7 +171,7 @@ __host__ __device__ inline void fill_emulation_plan(Plan& p, int s, int pair_lim
     p.pairs = pairs;
     const int ndiag = L + 1;
     // columns per diagonal accumulator so that ndiag * variant <= 512 TMEM columns
-    p.variant = ndiag <= 8 ? 64 : (ndiag <= 16 ? 32 : (ndiag <= 32 ? 16 : 8));
+    p.variant = ndiag <= 8 ? 64 : (ndiag <= 10 ? 48 : (ndiag <= 16 ? 32 : (ndiag <= 32 ? 16 : 8)));
     const int64_t kc = int32_kchunk(mpd);
     p.kchunk = (int32_t)kc;
     p.nchunks = k == 0 ? 0 : (int32_t)((k + kc - 1) / kc);

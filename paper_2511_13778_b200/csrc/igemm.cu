@@ -45,8 +45,8 @@ template <int NB>
 struct Cfg {
     static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
     // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
-    static constexpr int kNL = NB == 64 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
-    static constexpr int kCW = NB == 64 ? 8 : (NB == 32 ? 4 : (NB == 16 ? 2 : 1));  // columns per TMEM load batch
+    static constexpr int kNL = NB >= 48 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
+    static constexpr int kCW = NB >= 48 ? 8 : (NB == 32 ? 4 : (NB == 16 ? 2 : 1));  // columns per TMEM load batch
 };
 
 struct alignas(8) SmemHeader {
@@ -377,10 +377,12 @@ __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemH
         ADPB200_MMA_CASE(1, 0) ADPB200_MMA_CASE(2, 2) ADPB200_MMA_CASE(3, 3) ADPB200_MMA_CASE(4, 4)
         ADPB200_MMA_CASE(5, 5) ADPB200_MMA_CASE(6, 6) ADPB200_MMA_CASE(7, 7) ADPB200_MMA_CASE(3, 4)
         ADPB200_MMA_CASE(4, 6)
+    } else if constexpr (NB == 48) {
+        ADPB200_MMA_CASE(8, 8) ADPB200_MMA_CASE(9, 9) ADPB200_MMA_CASE(5, 8)
     } else if constexpr (NB == 32) {
-        ADPB200_MMA_CASE(8, 8) ADPB200_MMA_CASE(9, 9) ADPB200_MMA_CASE(10, 10) ADPB200_MMA_CASE(11, 11)
-        ADPB200_MMA_CASE(12, 12) ADPB200_MMA_CASE(13, 13) ADPB200_MMA_CASE(14, 14) ADPB200_MMA_CASE(15, 15)
-        ADPB200_MMA_CASE(5, 8) ADPB200_MMA_CASE(6, 10) ADPB200_MMA_CASE(7, 12) ADPB200_MMA_CASE(8, 14)
+        ADPB200_MMA_CASE(10, 10) ADPB200_MMA_CASE(11, 11) ADPB200_MMA_CASE(12, 12) ADPB200_MMA_CASE(13, 13)
+        ADPB200_MMA_CASE(14, 14) ADPB200_MMA_CASE(15, 15) ADPB200_MMA_CASE(6, 10) ADPB200_MMA_CASE(7, 12)
+        ADPB200_MMA_CASE(8, 14)
     } else if constexpr (NB == 16) {
         ADPB200_MMA_CASE(16, 16) ADPB200_MMA_CASE(17, 17) ADPB200_MMA_CASE(18, 18) ADPB200_MMA_CASE(9, 16)
         ADPB200_MMA_CASE(10, 18) ADPB200_MMA_CASE(11, 20) ADPB200_MMA_CASE(12, 22)
@@ -524,18 +526,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         uint64_t S[C::kNL];
                         if constexpr (C::kNL == 2) {
-                            // S = sum_D acc_D 256^(L-D), L <= 7: two int64 Horner halves
+                            // S = sum_D acc_D 256^(L-D), L <= 9: int64 Horner over groups of
+                            // <= 4 diagonals (< 2^57 each), groups joined in 128 bits
                             int64_t h = int32_t(v[0][cc]);
 #pragma unroll
                             for (int D = 1; D < 4; ++D)
                                 if (D < ndiag) h = h * 256 + int32_t(v[D][cc]);
                             __int128 S128 = h;
-                            if (ndiag > 4) {
-                                int64_t l = int32_t(v[4][cc]);
 #pragma unroll
-                                for (int D = 5; D < 8; ++D)
-                                    if (D < ndiag) l = l * 256 + int32_t(v[D][cc]);
-                                S128 = (__int128(h) << (8 * (L - 3))) + l;
+                            for (int g0 = 4; g0 < C::kNDMax; g0 += 4) {
+                                if (g0 < ndiag) {
+                                    int64_t l = int32_t(v[g0][cc]);
+                                    int len = 1;
+#pragma unroll
+                                    for (int D = g0 + 1; D < g0 + 4 && D < C::kNDMax; ++D)
+                                        if (D < ndiag) {
+                                            l = l * 256 + int32_t(v[D][cc]);
+                                            ++len;
+                                        }
+                                    S128 = (S128 << (8 * len)) + l;
+                                }
                             }
                             S[0] = uint64_t(S128);
                             S[1] = uint64_t((unsigned __int128)S128 >> 64);
@@ -644,8 +654,8 @@ struct MapCacheEntry {
 
 int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t nkb, int cap, const GemmArgs& g,
                  cudaStream_t st, uint64_t* nlaunch) {
-    static thread_local MapCacheEntry cache[4];
-    const int slot = nb == 64 ? 0 : (nb == 32 ? 1 : (nb == 16 ? 2 : 3));
+    static thread_local MapCacheEntry cache[5];
+    const int slot = nb == 64 ? 0 : (nb == 48 ? 1 : (nb == 32 ? 2 : (nb == 16 ? 3 : 4)));
     MapCacheEntry& e = cache[slot];
     if (e.pa != planes_a || e.pb != planes_b || e.M != g.M || e.N != g.N || e.nkb != nkb || e.cap != cap ||
         e.nb != nb) {
@@ -675,6 +685,10 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
         case 64:
             set_attr_once<64>();
             igemm_kernel<64><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            break;
+        case 48:
+            set_attr_once<48>();
+            igemm_kernel<48><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 32:
             set_attr_once<32>();

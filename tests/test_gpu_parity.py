@@ -130,7 +130,7 @@ def test_decompose_uniform_strided(gpu, port):
 
 # ---- K4: int32 slice products on tcgen05 (per-diagonal int64) --------------------------------
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (128, 64, 32), (130, 70, 100), (257, 129, 300), (64, 300, 1000)])
-@pytest.mark.parametrize("slices,limit", [(1, -1), (2, -1), (3, -1), (4, -1), (7, 7), (7, -1), (8, 8),
+@pytest.mark.parametrize("slices,limit", [(1, -1), (2, -1), (3, -1), (4, -1), (5, -1), (6, -1), (7, 7), (7, -1), (8, 8),
                                           (9, 9), (12, 5), (8, -1), (17, 17)])
 def test_slice_pair_mm(gpu, port, m, n, k, slices, limit):
     if m * n * k * slices * slices > 4e8:
@@ -151,7 +151,7 @@ def test_slice_pair_mm_multichunk(gpu, port):
 
 # ---- K5: fused exact epilogue (emulated_gemm) -------------------------------------------------
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (33, 17, 513), (128, 128, 128), (200, 150, 333)])
-@pytest.mark.parametrize("slices,limit", [(7, -1), (7, 7), (8, 8), (9, -1), (4, 2), (16, 16), (18, 18)])
+@pytest.mark.parametrize("slices,limit", [(7, -1), (7, 7), (8, 8), (9, -1), (4, 2), (16, 16), (18, 18), (9, 9), (5, -1), (6, 3)])
 def test_emulated_gemm(gpu, port, m, n, k, slices, limit):
     if m * n * k * slices * slices > 4e8:
         pytest.skip("oracle too slow for this size")
