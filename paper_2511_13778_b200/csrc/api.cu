@@ -72,7 +72,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Layout {
     size_t plan, stats_a_max, stats_a_min, line_a, stats_b_max, stats_b_min, line_b, scale_a, scale_b, planes_a,
         planes_b, partial, scratch, total;
-    int64_t blocks, pitch;
+    int64_t blocks, pitch, slots_a, slots_b;
     int cap;
 };
 
@@ -96,8 +96,11 @@ Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) 
     L.line_b = take(size_t(N) * 4);
     L.scale_a = take(size_t(M) * 4);
     L.scale_b = take(size_t(N) * 4);
-    L.planes_a = take(cap ? size_t(cap) * M * L.pitch : 0);
-    L.planes_b = take(cap ? size_t(cap) * N * L.pitch : 0);
+    // blocked planes: line slots rounded to 4 (the 128-byte TMA rows hold 4 lines)
+    L.slots_a = (M + 3) / 4 * 4;
+    L.slots_b = (N + 3) / 4 * 4;
+    L.planes_a = take(cap ? size_t(cap) * L.slots_a * L.pitch : 0);
+    L.planes_b = take(cap ? size_t(cap) * L.slots_b * L.pitch : 0);
     L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
     L.scratch = take(4096);
     L.total = off;
@@ -231,8 +234,8 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         int32_t* sa = at<int32_t>(h, Lw.scale_a);
         int32_t* sb = at<int32_t>(h, Lw.scale_b);
         tm.begin(3);
-        launch_slice(P.a, aline, pa, Lw.pitch, Lw.pitch * P.M, 1, sa, plan, fixed_slices, cap, st, nl);
-        launch_slice(P.b, bline, pb, Lw.pitch, Lw.pitch * P.N, 1, sb, plan, fixed_slices, cap, st, nl);
+        launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, plan, fixed_slices, cap, st, nl);
+        launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, fixed_slices, cap, st, nl);
         tm.end(3);
         // K4/K5: one launch per GEMM variant; exactly one does work
         GemmArgs g{};
@@ -259,7 +262,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                 fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
                 if (hp.variant != nb) continue;
             }
-            if (launch_igemm(nb, pa, pb, Lw.pitch / 32, cap, g, st, nl))
+            if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
                 return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
         }
         tm.end(4);

@@ -8,7 +8,8 @@
 //
 // Structure (one persistent CTA per SM, 12 warps):
 //   warp 0      TMA producer: per 32-byte k-block, nsl A slice tiles
-//               (128 rows) + nsl B slice tiles (NB rows) into one stage.
+//               (128 rows) + nsl B slice tiles (NB rows) into one stage —
+//               one linear box per operand (planes are pre-swizzled by K3).
 //   warp 1      MMA issuer (one thread). TMEM holds one int32 accumulator of
 //               128 x NB per diagonal D = d_a + d_b (D <= L, (L+1)*NB <= 512
 //               columns). B slices are stacked along N inside a stage, so the
@@ -458,15 +459,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* sa = stages + size_t(stage) * lp.stage_bytes;
                     uint8_t* sb = sa + lp.a_bytes;
                     tc::mbar_expect_tx(&hdr->full[stage], lp.stage_bytes);
+                    // pre-swizzled blocked planes viewed as (128 B = 4 lines, line/4, k-block,
+                    // slice): a stage is one linear box per operand, 128-byte requests
                     if (boxed) {
-                        // blocked planes (32 B, line, k-block, slice): all nsl slices in one box
-                        tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * kBM), int(kb), 0);
-                        tc::tma_load_4d(sb, map_b, &hdr->full[stage], 0, int(nt * NB), int(kb), 0);
+                        tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
+                        tc::tma_load_4d(sb, map_b, &hdr->full[stage], 0, int(nt * (NB / 4)), int(kb), 0);
                     } else {
                         for (int d = 0; d < nsl; ++d) {
-                            tc::tma_load_4d(sa + d * (kBM * kKB), map_a, &hdr->full[stage], 0, int(mt * kBM),
+                            tc::tma_load_4d(sa + d * (kBM * kKB), map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)),
                                             int(kb), d);
-                            tc::tma_load_4d(sb + d * (NB * kKB), map_b, &hdr->full[stage], 0, int(nt * NB),
+                            tc::tma_load_4d(sb + d * (NB * kKB), map_b, &hdr->full[stage], 0, int(nt * (NB / 4)),
                                             int(kb), d);
                         }
                     }
@@ -614,19 +616,21 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
-// Blocked planes: plane d = [k-block][line][32 B]; a box is 32 B x box_rows
-// lines of one k-block x box_slices consecutive slices — box_slices
-// contiguous runs of box_rows*32 B in HBM, landing slice-major in smem.
-bool encode_plane_map(CUtensorMap* map, const int8_t* planes, int64_t lines, int64_t nkb, int cap, int box_rows,
+// Blocked planes: plane d = [k-block][line slot][32 B], already in the UMMA
+// 32-byte-swizzle order (K3 writes it so), `slots` a multiple of 4. Viewed as
+// (128 B, slots/4, k-block, slice), a box of box_rows lines x box_slices
+// slices is box_slices contiguous runs of box_rows*32 B that TMA copies
+// linearly (no TMA swizzle) with 128-byte requests, landing slice-major.
+bool encode_plane_map(CUtensorMap* map, const int8_t* planes, int64_t slots, int64_t nkb, int cap, int box_rows,
                       int box_slices) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
-    cuuint64_t dims[4] = {cuuint64_t(kKB), cuuint64_t(lines), cuuint64_t(nkb), cuuint64_t(cap)};
-    cuuint64_t strides[3] = {cuuint64_t(kKB), cuuint64_t(kKB * lines), cuuint64_t(kKB * lines * nkb)};
-    cuuint32_t box[4] = {cuuint32_t(kKB), cuuint32_t(box_rows), 1, cuuint32_t(box_slices)};
+    cuuint64_t dims[4] = {cuuint64_t(4 * kKB), cuuint64_t(slots / 4), cuuint64_t(nkb), cuuint64_t(cap)};
+    cuuint64_t strides[3] = {cuuint64_t(4 * kKB), cuuint64_t(kKB * slots), cuuint64_t(kKB * slots * nkb)};
+    cuuint32_t box[4] = {cuuint32_t(4 * kKB), cuuint32_t(box_rows / 4), 1, cuuint32_t(box_slices)};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<int8_t*>(planes), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -652,26 +656,26 @@ struct MapCacheEntry {
 
 }  // namespace
 
-int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t nkb, int cap, const GemmArgs& g,
-                 cudaStream_t st, uint64_t* nlaunch) {
+int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t slots_a, int64_t slots_b,
+                 int64_t nkb, int cap, const GemmArgs& g, cudaStream_t st, uint64_t* nlaunch) {
     static thread_local MapCacheEntry cache[5];
     const int slot = nb == 64 ? 0 : (nb == 48 ? 1 : (nb == 32 ? 2 : (nb == 16 ? 3 : 4)));
     MapCacheEntry& e = cache[slot];
-    if (e.pa != planes_a || e.pb != planes_b || e.M != g.M || e.N != g.N || e.nkb != nkb || e.cap != cap ||
+    if (e.pa != planes_a || e.pb != planes_b || e.M != slots_a || e.N != slots_b || e.nkb != nkb || e.cap != cap ||
         e.nb != nb) {
         const int nbox = cap < kMaxBox ? cap : kMaxBox;
         for (int i = 0; i < kMaxBox; ++i) {
             const int bs = i < nbox ? i + 1 : 1;
-            if (!encode_plane_map(&e.maps.a[i], planes_a, g.M, nkb, cap, kBM, bs) ||
-                !encode_plane_map(&e.maps.b[i], planes_b, g.N, nkb, cap, nb, bs)) {
+            if (!encode_plane_map(&e.maps.a[i], planes_a, slots_a, nkb, cap, kBM, bs) ||
+                !encode_plane_map(&e.maps.b[i], planes_b, slots_b, nkb, cap, nb, bs)) {
                 e.pa = nullptr;
                 return -1;
             }
         }
         e.pa = planes_a;
         e.pb = planes_b;
-        e.M = g.M;
-        e.N = g.N;
+        e.M = slots_a;
+        e.N = slots_b;
         e.nkb = nkb;
         e.cap = cap;
         e.nb = nb;

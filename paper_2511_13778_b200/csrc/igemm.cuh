@@ -29,9 +29,10 @@ struct GemmArgs {
 };
 
 // nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.
-// planes_a / planes_b: blocked slice planes (cap planes of nkb k-blocks).
-int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t nkb, int cap, const GemmArgs& g,
-                 cudaStream_t st, uint64_t* nlaunch);
+// planes_a / planes_b: blocked, pre-swizzled slice planes (cap planes of nkb
+// k-blocks of slots_a / slots_b line slots, slots a multiple of 4).
+int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t slots_a, int64_t slots_b,
+                 int64_t nkb, int cap, const GemmArgs& g, cudaStream_t st, uint64_t* nlaunch);
 
 // K6: native FP64 fallback in the reference's summation order (ascending k,
 // separate multiply and add: oracle.cpp:7-28). Runs iff the plan says

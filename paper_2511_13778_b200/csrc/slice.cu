@@ -16,9 +16,11 @@
 // static.
 //
 // Output layouts: "blocked" (the GEMM's TMA layout) stores plane d as
-// [k-block of 32][line][32 bytes], so one TMA box (32 B x 128 lines) is a
-// contiguous 4 KiB run; "pitched" (stage export) is the reference's
-// plane-major [line][len].
+// [k-block of 32][line slot][32 bytes], PRE-SWIZZLED with the UMMA 32-byte
+// K-major pattern (16-byte half index ^= bit 2 of the line), so a GEMM stage
+// is a plain linear copy of contiguous 4 KiB runs that TMA moves with
+// 128-byte requests; "pitched" (stage export) is the reference's plane-major
+// [line][len].
 //
 // HBM-bound: 8 B read + nsl B written per element (+4 B per line).
 #include <type_traits>
@@ -121,7 +123,7 @@ struct SliceArgs {
     LineView v;
     const int32_t* line_max;
     int8_t* planes;
-    int64_t pitch;         // pitched: bytes between lines; blocked: unused
+    int64_t pitch;         // pitched: bytes between lines; blocked: line slots per k-block
     int64_t plane_stride;  // bytes between planes
     int blocked;           // 1: [d][kb][line][32]
     int32_t* scale;
@@ -131,7 +133,8 @@ struct SliceArgs {
 
 // byte offset of (d, line, pos) inside the planes
 __device__ __forceinline__ int64_t plane_off(const SliceArgs& a, int d, int64_t line, int64_t pos) {
-    if (a.blocked) return int64_t(d) * a.plane_stride + ((pos >> 5) * a.v.lines + line) * 32 + (pos & 31);
+    if (a.blocked)  // SW32: the 16-byte half of a 32-byte row flips on bit 2 of the row (line)
+        return int64_t(d) * a.plane_stride + ((pos >> 5) * a.pitch + line) * 32 + ((pos & 31) ^ ((line & 4) << 2));
     return int64_t(d) * a.plane_stride + line * a.pitch + pos;
 }
 
