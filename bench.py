@@ -62,7 +62,7 @@ class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, device: int):
         self.device = device
@@ -93,7 +93,7 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         rows = [s for (t, s) in self.samples if t0 - 0.2 <= t <= t1 + 0.2] or [s for _, s in self.samples[-5:]]
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, pw = [], 0.0, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             parts = [x.strip() for x in r.split(",")]
@@ -107,10 +107,14 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            try:
+                pw.append(float(parts[7]))
+            except (ValueError, IndexError):
+                pass
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------------

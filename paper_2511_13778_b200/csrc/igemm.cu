@@ -25,6 +25,7 @@
 // k longer than the int32-safe chunk (see int32_kchunk) is split into chunks;
 // each chunk's exact partial sum is kept in a limb workspace in HBM.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "igemm.cuh"
 #include "tc.cuh"
@@ -307,7 +308,7 @@ struct Loop {
 // The MMA role, converged warp; SCHED = compile-time (S, L) or runtime smem.
 template <int NB, int S, int L>
 __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const SmemSched* sched, uint32_t stage0,
-                                         uint32_t tmem_base) {
+                                         uint32_t tmem_base, int debug) {
     constexpr bool kStatic = S > 0;
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
@@ -325,7 +326,9 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
                 const uint64_t da = tc::smem_desc_sw32(sa), db = tc::smem_desc_sw32(sb);
                 const bool first = kb == kb0;
                 if (elect_one()) {
-                    if constexpr (kStatic) {
+                    if (debug & 1) {
+                        // diagnostics: data movement only
+                    } else if constexpr (kStatic) {
                         constexpr StaticSched<NB, S, L, true> F{};
                         constexpr StaticSched<NB, S, L, false> R{};
                         if (first) {
@@ -368,10 +371,10 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
 // counts each variant serves; anything else runs the runtime schedule.
 template <int NB>
 __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemHeader* hdr, const SmemSched* sched,
-                                             uint32_t stage0, uint32_t tmem_base) {
+                                             uint32_t stage0, uint32_t tmem_base, int debug) {
 #define ADPB200_MMA_CASE(S_, L_)                                          \
     if (s == S_ && L == L_) {                                             \
-        mma_role<NB, S_, L_>(lp, hdr, sched, stage0, tmem_base);          \
+        mma_role<NB, S_, L_>(lp, hdr, sched, stage0, tmem_base, debug);   \
         return;                                                           \
     }
     if constexpr (NB == 64) {
@@ -389,7 +392,7 @@ __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemH
         ADPB200_MMA_CASE(10, 18) ADPB200_MMA_CASE(11, 20) ADPB200_MMA_CASE(12, 22)
     }
 #undef ADPB200_MMA_CASE
-    mma_role<NB, 0, 0>(lp, hdr, sched, stage0, tmem_base);
+    mma_role<NB, 0, 0>(lp, hdr, sched, stage0, tmem_base, debug);
 }
 
 template <int NB>
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ===== MMA issuer (converged warp, one elected lane issues) =====
-        mma_dispatch<NB>(s, L, lp, hdr, sched, tc::smem_u32(stages), tmem_base);
+        mma_dispatch<NB>(s, L, lp, hdr, sched, tc::smem_u32(stages), tmem_base, g.debug);
     } else if (warp >= kFirstEpiWarp) {
         // ===== epilogue: 8 warps, (lane quadrant, column half) each =====
         const int ew = warp - kFirstEpiWarp;
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int cc = 0; cc < C::kCW; ++cc) {
                         const int64_t col = nt * NB + j0 + cc;
-                        if (!row_ok || col >= g.N) continue;
+                        if (!row_ok || col >= g.N || (g.debug & 2)) continue;
                         if (g.dump) {
                             int64_t* dst = g.dump + (row * g.N + col) * g.ndump;
 #pragma unroll
@@ -684,6 +687,11 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
     GemmArgs a = g;
+    static const int debug = [] {
+        const char* e = getenv("ADPB200_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    a.debug = debug;
     a.smem_bytes = kGemmSmemBytes;
     switch (nb) {
         case 64:

@@ -26,6 +26,7 @@ struct GemmArgs {
     int64_t* dump;           // stage export: acc[(i*N + j)*ndump + D] += diagonal D
     int ndump;
     int smem_bytes;
+    int debug;  // timing diagnostics only (ADPB200_DEBUG): 1 skip MMAs, 2 skip epilogue math
 };
 
 // nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.

@@ -227,39 +227,44 @@ __global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
     }
 }
 
-// ---- lines adjacent (ls == 1), positions strided: 64 lines x 64 positions ---------
-// Loads are coalesced across lines; digits are transposed through shared
-// memory (row stride 68 B: conflict-free 32-bit writes) so every plane is
-// written K-major in 16-byte line segments.
-constexpr int kTL = 64, kTP = 64, kTStride = 68;
+// ---- lines adjacent (ls == 1), positions strided: 64 lines x 32 positions ---------
+// The FP64 tile is transposed through shared memory (loads coalesced across
+// lines, 16.6 KiB per CTA whatever s is); each thread then slices 8
+// consecutive positions of one line exactly like the contiguous variant, so a
+// warp stores 8 lines x 32 B = one contiguous 256-byte run per plane in the
+// blocked layout.
+constexpr int kTL = 64, kTP = 32, kTPad = kTL + 1;
 
 template <int S>
-__device__ __forceinline__ void cols_compute(const SliceArgs& a, int nsl, uint8_t* tile, const uint64_t (&bits)[16],
-                                             int E, int tl, int tp) {
+__device__ __forceinline__ void cols_body(const SliceArgs& a, int nsl, const uint64_t (&bits)[8], int E,
+                                          int64_t line, int64_t p0, int nvalid) {
+    if constexpr (S <= 16) {
+        typename Word<S>::T X[8];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int pl = tp * 16 + c * 4;
-        if constexpr (S <= 16) {
-            typename Word<S>::T X[4];
+        for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[q], E);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) X[q] = slice_word<S>(bits[c * 4 + q], E);
+        for (int d = 0; d < S; ++d) {
+            if (d >= nsl) break;
+            uint32_t lo = 0, hi = 0;
 #pragma unroll
-            for (int d = 0; d < S; ++d) {
-                if (d >= nsl) break;
-                uint32_t w = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) w |= plane_byte<S>(X[q], d) << (8 * q);
-                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            for (int q = 0; q < 4; ++q) {
+                lo |= plane_byte<S>(X[q], d) << (8 * q);
+                hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
             }
-        } else {
-            const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
-            int8_t dig[4][kMaxSlices];
-            for (int q = 0; q < 4; ++q) slice_digits_slow(bits[c * 4 + q], E, s, dig[q]);
-            for (int d = 0; d < nsl; ++d) {
-                uint32_t w = 0;
-                for (int q = 0; q < 4; ++q) w |= uint32_t(uint8_t(dig[q][d])) << (8 * q);
-                *reinterpret_cast<uint32_t*>(tile + (d * kTL + tl) * kTStride + pl) = w;
+            int8_t* out = a.planes + plane_off(a, d, line, p0);
+            if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
+                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+            } else {
+                const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+                for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, d, line, p0 + q)] = int8_t(w >> (8 * q));
             }
+        }
+    } else {
+        int8_t dig[kMaxSlices];
+        const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
+        for (int q = 0; q < nvalid; ++q) {
+            slice_digits_slow(bits[q], E, s, dig);
+            for (int d = 0; d < nsl; ++d) a.planes[plane_off(a, d, line, p0 + q)] = dig[d];
         }
     }
 }
@@ -267,58 +272,45 @@ __device__ __forceinline__ void cols_compute(const SliceArgs& a, int nsl, uint8_
 __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
     int s, nsl;
     if (!resolve(a, s, nsl)) return;
-    extern __shared__ __align__(16) uint8_t tile[];  // nsl * kTL * kTStride
+    __shared__ uint64_t tile[kTP][kTPad];
     const int64_t line0 = int64_t(blockIdx.x) * kTL;
     const int64_t pos0 = int64_t(blockIdx.y) * kTP;
-    const int tl = threadIdx.x % kTL;  // line within tile
-    const int tp = threadIdx.x / kTL;  // 0..3: 16 positions each
-    const int64_t line = line0 + tl;
-    int E = 0;
-    if (line < a.v.lines) {
-        int lm = a.line_max[line];
-        E = lm == kNegSentinel ? 0 : lm + 2;
-        if (blockIdx.y == 0 && tp == 0 && a.scale) a.scale[line] = E;
-    }
-    uint64_t bits[16];  // all loads in flight before any compute
+    {
+        const int tl = threadIdx.x % kTL, tp = threadIdx.x / kTL;  // 4 position rows per pass
+        const int64_t line = line0 + tl;
+        uint64_t v[kTP / 4];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        int64_t pos = pos0 + tp * 16 + q;
-        bits[q] = (line < a.v.lines && pos < a.v.len) ? __double_as_longlong(__ldg(a.v.ptr + line + pos * a.v.ps))
-                                                       : 0ull;
+        for (int i = 0; i < kTP / 4; ++i) {
+            const int64_t pos = pos0 + tp + 4 * i;
+            v[i] = (line < a.v.lines && pos < a.v.len) ? __double_as_longlong(__ldg(a.v.ptr + line + pos * a.v.ps))
+                                                        : 0ull;
+        }
+#pragma unroll
+        for (int i = 0; i < kTP / 4; ++i) tile[tp + 4 * i][tl] = v[i];
     }
+    __syncthreads();
+    const int ol = threadIdx.x / 4, og = threadIdx.x % 4;  // line, group of 8 positions
+    const int64_t line = line0 + ol;
+    if (line >= a.v.lines) return;
+    const int lm = a.line_max[line];
+    const int E = lm == kNegSentinel ? 0 : lm + 2;
+    if (blockIdx.y == 0 && og == 0 && a.scale) a.scale[line] = E;
+    const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
+    const int64_t p0 = pos0 + og * 8;
+    if (p0 >= span) return;
+    const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
+    uint64_t bits[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) bits[q] = tile[og * 8 + q][ol];
     switch (s) {
 #define ADPB200_COLS_CASE(S) \
-    case S: cols_compute<S>(a, nsl, tile, bits, E, tl, tp); break;
+    case S: cols_body<S>(a, nsl, bits, E, line, p0, nvalid); break;
         ADPB200_COLS_CASE(1) ADPB200_COLS_CASE(2) ADPB200_COLS_CASE(3) ADPB200_COLS_CASE(4)
         ADPB200_COLS_CASE(5) ADPB200_COLS_CASE(6) ADPB200_COLS_CASE(7) ADPB200_COLS_CASE(8)
         ADPB200_COLS_CASE(9) ADPB200_COLS_CASE(10) ADPB200_COLS_CASE(11) ADPB200_COLS_CASE(12)
         ADPB200_COLS_CASE(13) ADPB200_COLS_CASE(14) ADPB200_COLS_CASE(15) ADPB200_COLS_CASE(16)
 #undef ADPB200_COLS_CASE
-        default: cols_compute<32>(a, nsl, tile, bits, E, tl, tp); break;
-    }
-    __syncthreads();
-    // write out: thread -> (line, 16-byte chunk)
-    const int ol = threadIdx.x / 4, oc = threadIdx.x % 4;
-    const int64_t oline = line0 + ol;
-    const int64_t opos = pos0 + oc * 16;
-    const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
-    if (oline >= a.v.lines || opos >= span) return;
-    const int nvalid = span - opos < 16 ? int(span - opos) : 16;
-    const bool vec = nvalid == 16 && (a.blocked || ((a.pitch | a.plane_stride) & 15) == 0) &&
-                     ((reinterpret_cast<uintptr_t>(a.planes) & 15) == 0);
-    for (int d = 0; d < nsl; ++d) {
-        const uint8_t* src = tile + (d * kTL + ol) * kTStride + oc * 16;
-        int8_t* dst = a.planes + plane_off(a, d, oline, opos);
-        if (vec) {
-            uint4 w;
-            w.x = *reinterpret_cast<const uint32_t*>(src);
-            w.y = *reinterpret_cast<const uint32_t*>(src + 4);
-            w.z = *reinterpret_cast<const uint32_t*>(src + 8);
-            w.w = *reinterpret_cast<const uint32_t*>(src + 12);
-            *reinterpret_cast<uint4*>(dst) = w;
-        } else {
-            for (int q = 0; q < nvalid; ++q) dst[q] = int8_t(src[q]);
-        }
+        default: cols_body<32>(a, nsl, bits, E, line, p0, nvalid); break;
     }
 }
 
@@ -345,17 +337,9 @@ void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, in
         if (vec) slice_rows_kernel<true><<<grid, 256, 0, st>>>(a);
         else slice_rows_kernel<false><<<grid, 256, 0, st>>>(a);
     } else {
-        const int max_planes = slices_fixed > 0 ? slices_fixed : (plane_cap > 0 ? plane_cap : kMaxSlices);
-        const size_t smem = size_t(max_planes) * kTL * kTStride;
-        static bool attr_set = false;
-        if (!attr_set) {
-            cudaFuncSetAttribute(slice_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kMaxSlices * kTL * kTStride);
-            attr_set = true;
-        }
         const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
         dim3 grid((unsigned)((v.lines + kTL - 1) / kTL), (unsigned)((span + kTP - 1) / kTP));
-        slice_cols_kernel<<<grid, 256, smem, st>>>(a);
+        slice_cols_kernel<<<grid, 256, 0, st>>>(a);
     }
     ++*nlaunch;
 }

@@ -166,7 +166,11 @@ static void run(const char* name, int iters, int runtime_ops) {
     cudaFree(dcyc);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1) {  // sustained: ~4 s of back-to-back N=256 MMAs (power-capped steady state)
+        run<0>("sustained_n256_static", 30000000, 0);
+        return 0;
+    }
     run<0>("peak_n256_static", 400000, 0);
     run<1>("n128_static", 400000, 0);
     run<2>("n64_static", 400000, 0);
