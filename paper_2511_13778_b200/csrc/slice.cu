@@ -53,6 +53,20 @@ template <int S>
 __device__ __forceinline__ typename Word<S>::T slice_word(uint64_t bits, int E) {
     typedef typename Word<S>::T T;
     const T C = slice_const<S>();
+    if constexpr (S <= 8) {
+        // normal numbers, branch-free: with x = M * 2^9 (< 2^62) the net right
+        // shift t = st + 9 = (E + 1077 - 8(S-1)) - biased_exp is >= 0 because
+        // st >= 47 - 8(S-1) >= -9; floor(-x / 2^t) = ~((x - 1) >> t).
+        const uint32_t ex = uint32_t(bits >> 52) & 0x7ffu;
+        if (ex != 0) {
+            const uint64_t neg = bits >> 63;
+            const uint64_t x = ((bits & 0xFFFFFFFFFFFFFull) | (1ull << 52)) << 9;
+            int t = E + 1077 - 8 * (S - 1) - int(ex);
+            t = t < 63 ? t : 63;  // (x - neg) < 2^62: a shift of 63 already gives 0
+            const uint64_t q = (x - neg) >> t;
+            return (q ^ (0ull - neg)) + C;
+        }
+    }
     if ((bits << 1) == 0) return C;
     const bool neg = (bits >> 63) != 0;
     const uint64_t M = norm_mant(bits);
@@ -74,6 +88,33 @@ template <int S>
 __device__ __forceinline__ uint32_t plane_byte(typename Word<S>::T X, int d) {
     const uint32_t b = uint32_t(X >> (8 * (S - 1 - d))) & 0xffu;
     return d == 0 ? b : (b ^ 0x80u);
+}
+
+// Plane d's bytes of 8 consecutive elements, packed into two words with
+// byte permutes (d is a compile-time constant after unrolling).
+template <int S>
+__device__ __forceinline__ void pack_plane(const typename Word<S>::T (&X)[8], int d, uint32_t& lo, uint32_t& hi) {
+    if constexpr (S <= 8) {
+        const int j = S - 1 - d;  // byte of X
+        uint32_t w[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) w[q] = j < 4 ? uint32_t(X[q]) : uint32_t(X[q] >> 32);
+        const uint32_t b = uint32_t(j & 3);
+        const uint32_t sel = b | ((4 + b) << 4);  // byte b of x -> byte 0, byte b of y -> byte 1
+        lo = __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410);
+        hi = __byte_perm(__byte_perm(w[4], w[5], sel), __byte_perm(w[6], w[7], sel), 0x5410);
+        if (d != 0) {
+            lo ^= 0x80808080u;
+            hi ^= 0x80808080u;
+        }
+    } else {
+        lo = hi = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            lo |= plane_byte<S>(X[q], d) << (8 * q);
+            hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
+        }
+    }
 }
 
 // Reference-form restatement for any s <= 32 (slicing.cpp:11-66).
@@ -183,12 +224,8 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
 #pragma unroll
             for (int d = 0; d < S; ++d) {
                 if (d >= nsl) break;
-                uint32_t lo = 0, hi = 0;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    lo |= plane_byte<S>(X[q], d) << (8 * q);
-                    hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
-                }
+                uint32_t lo, hi;
+                pack_plane<S>(X, d, lo, hi);
                 int8_t* out = a.planes + plane_off(a, d, line, p0);
                 if (kVec && nvalid == 8) {
                     *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
@@ -245,12 +282,8 @@ __device__ __forceinline__ void cols_body(const SliceArgs& a, int nsl, const uin
 #pragma unroll
         for (int d = 0; d < S; ++d) {
             if (d >= nsl) break;
-            uint32_t lo = 0, hi = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                lo |= plane_byte<S>(X[q], d) << (8 * q);
-                hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
-            }
+            uint32_t lo, hi;
+            pack_plane<S>(X, d, lo, hi);
             int8_t* out = a.planes + plane_off(a, d, line, p0);
             if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
                 *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
