@@ -123,6 +123,19 @@ int adpb200_adp_gemm(adpb200_handle handle, int64_t m, int64_t n, int64_t k, dou
                      double* out, const adpb200_options* opt, adpb200_trace* trace,
                      void* stream);
 
+/* Host-buffer variants (A, B, C, trace in HOST memory; page-locked buffers
+ * recommended): copy the operands in, run the pipeline, copy C out while the
+ * slice GEMM still computes (row chunks), return when C is on the host. The
+ * end-to-end path the reference's value-returning adp_gemm corresponds to. */
+int adpb200_dgemm_host(adpb200_handle handle, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                       double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
+                       double beta, double* C, int64_t ldc, const adpb200_options* opt,
+                       adpb200_trace* trace, void* stream);
+int adpb200_adp_gemm_host(adpb200_handle handle, int64_t m, int64_t n, int64_t k, double alpha,
+                          const double* A, const double* B, double beta, const double* c_in,
+                          double* out, const adpb200_options* opt, adpb200_trace* trace,
+                          void* stream);
+
 /* Row-block partition across ranks (one process per GPU): this rank owns rows
  * [r0, r0+m) of C / op(A) of a global m_global x n x k product and all of
  * op(B). phase 1 runs the guardrails (scan, exponent stats, ESC) on the local

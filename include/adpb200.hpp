@@ -204,19 +204,12 @@ inline std::pair<MatrixF64, AdpTrace> adp_gemm(const MatrixF64& a, const MatrixF
     const std::size_t m = a.rows(), n = b.cols(), k = a.cols();
     adpb200_handle h = default_handle(device);
     detail::cuda(cudaSetDevice(device), "cudaSetDevice");
-    detail::DevBuf da(a.size() * 8), db(b.size() * 8), dc(c ? c->size() * 8 : 0), dout(m * n * 8),
-        dtr(sizeof(adpb200_trace));
-    if (a.size()) detail::cuda(cudaMemcpy(da.p, a.data(), a.size() * 8, cudaMemcpyHostToDevice), "H2D A");
-    if (b.size()) detail::cuda(cudaMemcpy(db.p, b.data(), b.size() * 8, cudaMemcpyHostToDevice), "H2D B");
-    if (c && c->size()) detail::cuda(cudaMemcpy(dc.p, c->data(), c->size() * 8, cudaMemcpyHostToDevice), "H2D C");
     adpb200_options o = config.to_c();
-    detail::check(adpb200_adp_gemm(h, int64_t(m), int64_t(n), int64_t(k), alpha, static_cast<const double*>(da.p),
-                                   static_cast<const double*>(db.p), beta, static_cast<const double*>(dc.p),
-                                   static_cast<double*>(dout.p), &o, static_cast<adpb200_trace*>(dtr.p), nullptr));
     MatrixF64 out(m, n);
     adpb200_trace t;
-    if (out.size()) detail::cuda(cudaMemcpy(out.data(), dout.p, out.size() * 8, cudaMemcpyDeviceToHost), "D2H C");
-    detail::cuda(cudaMemcpy(&t, dtr.p, sizeof(t), cudaMemcpyDeviceToHost), "D2H trace");
+    // host-buffer entry point: copies in, computes, copies C out while the GEMM runs
+    detail::check(adpb200_adp_gemm_host(h, int64_t(m), int64_t(n), int64_t(k), alpha, a.data(), b.data(), beta,
+                                        c ? c->data() : nullptr, out.data(), &o, &t, nullptr));
     return {std::move(out), AdpTrace::from_c(t)};
 }
 

@@ -16,6 +16,7 @@ from .adp import (  # noqa: F401
     decide,
     decompose,
     dgemm,
+    dgemm_host,
     emulated_gemm,
     esc_coarsened,
     native_gemm,

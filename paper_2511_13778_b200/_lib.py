@@ -90,6 +90,9 @@ def lib() -> C.CDLL:
         "adpb200_dgemm": (C.c_int, [vp, C.c_char, C.c_char, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64,
                                     popt, vp, vp]),
         "adpb200_adp_gemm": (C.c_int, [vp, i64, i64, i64, f64, vp, vp, f64, vp, vp, popt, vp, vp]),
+        "adpb200_dgemm_host": (C.c_int, [vp, C.c_char, C.c_char, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64,
+                                         popt, vp, vp]),
+        "adpb200_adp_gemm_host": (C.c_int, [vp, i64, i64, i64, f64, vp, vp, f64, vp, vp, popt, vp, vp]),
         "adpb200_dgemm_rows": (C.c_int, [vp, C.c_int, i64, C.c_char, C.c_char, i64, i64, i64, f64, vp, i64, vp,
                                          i64, f64, vp, i64, popt, vp, vp, vp]),
         "adpb200_scan": (C.c_int, [vp, vp, i64, vp, vp]),
@@ -113,7 +116,8 @@ def lib() -> C.CDLL:
 EXPORTED = (
     "adpb200_version", "adpb200_last_error", "adpb200_status_string", "adpb200_default_options",
     "adpb200_validate_options", "adpb200_create", "adpb200_destroy", "adpb200_launch_count",
-    "adpb200_decide_host", "adpb200_dgemm", "adpb200_adp_gemm", "adpb200_dgemm_rows", "adpb200_scan", "adpb200_block_stats",
+    "adpb200_decide_host", "adpb200_dgemm", "adpb200_adp_gemm", "adpb200_dgemm_rows", "adpb200_dgemm_host",
+    "adpb200_adp_gemm_host", "adpb200_scan", "adpb200_block_stats",
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",
     "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read",
 )

@@ -29,7 +29,7 @@ from . import _lib
 from ._lib import PAIRS_FULL, PAIRS_TARGET, check, lib
 
 __all__ = [
-    "AdpMode", "AdpConfig", "AdpTrace", "Handle", "parse_mode", "decide", "adp_gemm", "dgemm",
+    "AdpMode", "AdpConfig", "AdpTrace", "Handle", "parse_mode", "decide", "adp_gemm", "dgemm", "dgemm_host",
     "emulated_gemm", "slice_pair_mm", "decompose", "block_exponent_stats", "scan_matrix", "esc_coarsened",
     "native_gemm", "required_slices", "PAIRS_FULL", "PAIRS_TARGET",
 ]
@@ -254,6 +254,18 @@ def adp_gemm(a, b, alpha: float = 1.0, beta: float = 0.0, c=None, config: Option
         raise ValueError("adp_gemm: C shape mismatch")
     dev = _device(a.device.index if isinstance(a, torch.Tensor) else None)
     handle = handle or Handle.default(dev.index)
+    if host and out is None:
+        # host in, host out: the library copies in, overlaps the copy-out with the GEMM
+        A = np.ascontiguousarray(a, dtype=np.float64)
+        B = np.ascontiguousarray(b, dtype=np.float64)
+        Cin = np.ascontiguousarray(c, dtype=np.float64) if c is not None else None
+        res = np.empty((m, n), dtype=np.float64)
+        tr = _lib.Trace()
+        o = config.to_c()
+        p = lambda x: None if x is None or x.size == 0 else C.c_void_p(x.ctypes.data)  # noqa: E731
+        check(lib().adpb200_adp_gemm_host(handle.h, m, n, k, float(alpha), p(A), p(B), float(beta), p(Cin), p(res),
+                                          C.byref(o), C.byref(tr), _stream(dev)))
+        return res, AdpTrace.from_c(tr)
     A, B = _to_dev(a, dev), _to_dev(b, dev)
     Cin = _to_dev(c, dev) if c is not None else None
     if out is None:
@@ -287,6 +299,22 @@ def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A: tor
     check(lib().adpb200_dgemm(handle.h, transa.encode()[:1], transb.encode()[:1], m, n, k, float(alpha),
                               _ptr(A), lda, _ptr(B), ldb, float(beta), _ptr(C_), ldc, C.byref(o),
                               None if trace is None else C.c_void_p(trace.data_ptr()), _stream(dev)))
+
+
+def dgemm_host(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
+               B: torch.Tensor, ldb: int, beta: float, C_: torch.Tensor, ldc: int, config: Optional[AdpConfig] = None,
+               handle: Optional[Handle] = None, device: int = 0) -> AdpTrace:
+    """dgemm on HOST (CPU, ideally pinned) float64 storage: operands copied in,
+    C copied out while the slice GEMM still runs; returns when C is on the host."""
+    config = config or AdpConfig()
+    handle = handle or Handle.default(device)
+    o = config.to_c()
+    tr = _lib.Trace()
+    p = lambda x: C.c_void_p(x.data_ptr()) if x.numel() else None  # noqa: E731
+    check(lib().adpb200_dgemm_host(handle.h, transa.encode()[:1], transb.encode()[:1], m, n, k, float(alpha), p(A),
+                                   lda, p(B), ldb, float(beta), p(C_), ldc, C.byref(o), C.byref(tr),
+                                   _stream(torch.device("cuda", device))))
+    return AdpTrace.from_c(tr)
 
 
 def emulated_gemm(a, b, slices: int = 7, alpha: float = 1.0, beta: float = 0.0, c=None,

@@ -32,6 +32,12 @@ struct adpb200_context {
     int prof_cap = 0, prof_calls = 0;
     cudaEvent_t* prof_ev = nullptr;  // [cap][kStages][2]
     bool prof_used[kStages] = {};
+    // host-buffer entry points: device copies of the operands + a D2H stream
+    void* io = nullptr;
+    size_t io_bytes = 0;
+    cudaStream_t d2h = nullptr;
+    cudaEvent_t chunk_ev[16] = {};
+    int chunk_next = 0;
 };
 
 namespace {
@@ -160,6 +166,26 @@ int plane_cap(const adpb200_options& o, int fixed_slices, int fixed_limit) {
     return cap;
 }
 
+constexpr int kHostChunks = 4;  // row chunks of the host-buffer path (GEMM chunk i || D2H chunk i-1)
+
+// Destination of C on the host for the host-buffer entry points.
+struct HostOut {
+    double* host_c;
+    int64_t ldc_host;
+    // copy internal rows [r0, r1) of C (all N columns) once the work queued on st is done
+    int copy_rows(adpb200_context* h, int64_t r0, int64_t r1, const Problem& P, cudaStream_t st) const {
+        if (r1 <= r0 || P.N == 0) return ADPB200_OK;
+        cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
+        int rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
+        if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent");
+        if (!rc)
+            rc = cuda_check(cudaMemcpy2DAsync(host_c + r0, size_t(ldc_host) * 8, P.c_out + r0, size_t(P.ldc) * 8,
+                                              size_t(r1 - r0) * 8, size_t(P.N), cudaMemcpyDeviceToHost, h->d2h),
+                            "cudaMemcpy2DAsync(D2H C)");
+        return rc;
+    }
+};
+
 // phase 0: the whole pipeline. Multi-GPU row partition: phase 1 runs the
 // guardrails (K1, K2) on this rank's rows and exports {exc, esc_raw} to xchg
 // (device int32[2]) for a max-allreduce across ranks; phase 2 imports the
@@ -167,7 +193,7 @@ int plane_cap(const adpb200_options& o, int fixed_slices, int fixed_limit) {
 // takes the same decision with the same s (C bit-identical for any rank count).
 int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace,
                  cudaStream_t st, int fixed_slices, int fixed_limit, int64_t* dump, int ndump, int phase = 0,
-                 int32_t* xchg = nullptr) {
+                 int32_t* xchg = nullptr, const HostOut* hout = nullptr) {
     const int cap = plane_cap(o, fixed_slices, fixed_limit);
     const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
     int rc = ensure_ws(h, Lw.total, st);
@@ -255,17 +281,35 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         g.dump = dump;
         g.ndump = ndump;
         int variants[5] = {64, 48, 32, 16, 8};
+        if (hout) {
+            // host-buffer path: the (predicated) fallback first, then the GEMM in
+            // row chunks, each chunk's C rows copied to the host on a second stream
+            // while the next chunk computes
+            launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+        }
+        const int64_t mtiles = (P.M + 127) / 128;
+        const int nchunk = hout ? int(std::min<int64_t>(mtiles, kHostChunks)) : 1;
         tm.begin(4);
-        for (int nb : variants) {
-            if (fixed_slices > 0) {  // the host knows the variant
-                Plan hp{};
-                fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
-                if (hp.variant != nb) continue;
+        for (int c = 0; c < nchunk; ++c) {
+            g.mt_begin = mtiles * c / nchunk;
+            g.mt_end = hout ? mtiles * (c + 1) / nchunk : 0;
+            for (int nb : variants) {
+                if (fixed_slices > 0) {  // the host knows the variant
+                    Plan hp{};
+                    fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
+                    if (hp.variant != nb) continue;
+                }
+                if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
+                    return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
             }
-            if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
-                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+            if (hout) {
+                const int64_t r0 = g.mt_begin * 128, r1 = std::min<int64_t>(g.mt_end * 128, P.M);
+                int rc2 = hout->copy_rows(h, r0, r1, P, st);
+                if (rc2) return rc2;
+            }
         }
         tm.end(4);
+        if (hout) return cuda_check(cudaGetLastError(), "kernel launch");
     }
     // K6: native fallback (predicated); with k == 0 both paths reduce to
     // alpha*(+0.0) (+ beta*C), so it runs unconditionally.
@@ -275,6 +319,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, pred, st, nl);
         tm.end(5);
     }
+    if (hout && P.M > 0 && P.N > 0) return hout->copy_rows(h, 0, P.M, P, st);
     return cuda_check(cudaGetLastError(), "kernel launch");
 }
 
@@ -366,6 +411,16 @@ int adpb200_create(adpb200_handle* handle, int device) {
 int adpb200_destroy(adpb200_handle h) {
     if (!h) return ADPB200_OK;
     adpb200_profile_enable(h, 0);
+    if (h->d2h) {
+        cudaStreamSynchronize(h->d2h);
+        for (auto& e : h->chunk_ev)
+            if (e) cudaEventDestroy(e);
+        cudaStreamDestroy(h->d2h);
+    }
+    if (h->io) {
+        cudaDeviceSynchronize();
+        cudaFree(h->io);
+    }
     if (h->ws) {
         cudaDeviceSynchronize();
         cudaFree(h->ws);
@@ -520,6 +575,132 @@ int adpb200_adp_gemm(adpb200_handle h, int64_t m, int64_t n, int64_t k, double a
     Problem P = rowmajor_problem(m, n, k, alpha, A, B, beta, c_in, out);
     cudaSetDevice(h->device);
     return run_pipeline(h, P, o, trace, static_cast<cudaStream_t>(stream), 0, 0, nullptr, 0);
+}
+
+namespace {
+// H2D of a rows x cols column-major block (leading dimension ld) into a compact device copy.
+int h2d_block(void* dst, const double* src, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return ADPB200_OK;
+    return cuda_check(cudaMemcpy2DAsync(dst, size_t(rows) * 8, src, size_t(ld) * 8, size_t(rows) * 8, size_t(cols),
+                                        cudaMemcpyHostToDevice, st),
+                      "cudaMemcpy2DAsync(H2D)");
+}
+
+int prepare_io(adpb200_context* h, size_t bytes, cudaStream_t st) {
+    if (!h->d2h) {
+        int rc = cuda_check(cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (rc) return rc;
+        for (auto& e : h->chunk_ev) {
+            rc = cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            if (rc) return rc;
+        }
+    }
+    if (h->io_bytes >= bytes) return ADPB200_OK;
+    if (h->io) cudaFreeAsync(h->io, st);
+    h->io = nullptr;
+    h->io_bytes = 0;
+    const size_t want = align_up(bytes, size_t(1) << 21);
+    int rc = cuda_check(cudaMallocAsync(&h->io, want, st), "cudaMallocAsync(io)");
+    if (!rc) h->io_bytes = want;
+    return rc;
+}
+
+int finish_host(adpb200_context* h, adpb200_trace* trace_host, const adpb200_trace* trace_dev, cudaStream_t st) {
+    int rc = ADPB200_OK;
+    if (trace_host)
+        rc = cuda_check(cudaMemcpyAsync(trace_host, trace_dev, sizeof(adpb200_trace), cudaMemcpyDeviceToHost, st),
+                        "D2H trace");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(h->d2h), "cudaStreamSynchronize(d2h)");
+    return rc;
+}
+}  // namespace
+
+int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                       const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                       const adpb200_options* opt, adpb200_trace* trace, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_host: null handle");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (!trans_ok(transa) || !trans_ok(transb)) return fail(3, "dgemm: bad trans flag");
+    if (m < 0 || n < 0 || k < 0) return fail(3, "dgemm: negative dimension");
+    const int64_t arows = is_n(transa) ? m : k, acols = is_n(transa) ? k : m;
+    const int64_t brows = is_n(transb) ? k : n, bcols = is_n(transb) ? n : k;
+    if (lda < std::max<int64_t>(1, arows)) return fail(3, "dgemm: lda too small");
+    if (ldb < std::max<int64_t>(1, brows)) return fail(3, "dgemm: ldb too small");
+    if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
+    if (m > 0 && n > 0 && !C) return fail(3, "dgemm: C is null");
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t ta = align_up(sizeof(adpb200_trace), 256), sa = align_up(size_t(arows) * acols * 8, 256),
+                 sb = align_up(size_t(brows) * bcols * 8, 256), sc = align_up(size_t(m) * n * 8, 256);
+    rc = prepare_io(h, ta + sa + sb + sc, st);
+    if (rc) return rc;
+    char* io = static_cast<char*>(h->io);
+    adpb200_trace* tdev = reinterpret_cast<adpb200_trace*>(io);
+    double* dA = reinterpret_cast<double*>(io + ta);
+    double* dB = reinterpret_cast<double*>(io + ta + sa);
+    double* dC = reinterpret_cast<double*>(io + ta + sa + sb);
+    // B first: its statistics do not wait for A
+    if ((rc = h2d_block(dB, B, brows, bcols, ldb, st))) return rc;
+    if ((rc = h2d_block(dA, A, arows, acols, lda, st))) return rc;
+    if (beta != 0.0 && (rc = h2d_block(dC, C, m, n, ldc, st))) return rc;
+    Problem P{};
+    P.M = m;
+    P.N = n;
+    P.K = k;
+    P.a = is_n(transa) ? LineView{dA, m, k, 1, arows} : LineView{dA, m, k, arows, 1};
+    P.b = is_n(transb) ? LineView{dB, n, k, brows, 1} : LineView{dB, n, k, 1, brows};
+    P.alpha = alpha;
+    P.beta = beta;
+    P.c_in = dC;
+    P.ldc_in = m;
+    P.c_out = dC;
+    P.ldc = m;
+    P.tm = m;
+    P.tn = n;
+    P.tk = k;
+    HostOut out{C, ldc};
+    rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &out);
+    if (rc) return rc;
+    return finish_host(h, trace, tdev, st);
+}
+
+int adpb200_adp_gemm_host(adpb200_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,
+                          const double* B, double beta, const double* c_in, double* out,
+                          const adpb200_options* opt, adpb200_trace* trace, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "adp_gemm_host: null handle");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (m < 0 || n < 0 || k < 0) return fail(3, "adp_gemm: negative dimension");
+    if (beta != 0.0 && !c_in) return fail(3, "adp_gemm: beta != 0 requires C");  // adp.cpp:143
+    if (m > 0 && n > 0 && !out) return fail(3, "adp_gemm: out is null");
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t ta = align_up(sizeof(adpb200_trace), 256), sa = align_up(size_t(m) * k * 8, 256),
+                 sb = align_up(size_t(k) * n * 8, 256), sc = align_up(size_t(m) * n * 8, 256);
+    rc = prepare_io(h, ta + sa + sb + sc, st);
+    if (rc) return rc;
+    char* io = static_cast<char*>(h->io);
+    adpb200_trace* tdev = reinterpret_cast<adpb200_trace*>(io);
+    double* dA = reinterpret_cast<double*>(io + ta);
+    double* dB = reinterpret_cast<double*>(io + ta + sa);
+    double* dC = reinterpret_cast<double*>(io + ta + sa + sb);
+    // row-major buffers are column-major transposes: copy them as such
+    if ((rc = h2d_block(dB, B, n, k, n, st))) return rc;
+    if ((rc = h2d_block(dA, A, k, m, k, st))) return rc;
+    if (beta != 0.0 && (rc = h2d_block(dC, c_in, n, m, n, st))) return rc;
+    Problem P = rowmajor_problem(m, n, k, alpha, dA, dB, beta, dC, dC);
+    HostOut hout{out, n};
+    rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &hout);
+    if (rc) return rc;
+    return finish_host(h, trace, tdev, st);
 }
 
 int adpb200_emulated_gemm(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,

@@ -407,7 +407,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     lp.nkb = (g.K + kKB - 1) / kKB;
     lp.kb_per_chunk = plan->kchunk / kKB;
     lp.nchunks = (int)((lp.nkb + lp.kb_per_chunk - 1) / lp.kb_per_chunk);
-    lp.tiles_m = (g.M + kBM - 1) / kBM;
+    // m-tile range [mt_begin, mt_end) (row chunks of the host-buffer path; mt_end 0 = all)
+    const int64_t mt_total = (g.M + kBM - 1) / kBM;
+    const int64_t mt_end = g.mt_end > 0 && g.mt_end < mt_total ? g.mt_end : mt_total;
+    const int64_t mt_off = g.mt_begin;
+    lp.tiles_m = mt_end > mt_off ? mt_end - mt_off : 0;
     lp.tiles_n = (g.N + NB - 1) / NB;
     lp.ntiles = lp.tiles_m * lp.tiles_n;
 
@@ -456,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
             int64_t mt, nt;
             tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
+            mt += mt_off;
             for (int64_t kb = 0; kb < lp.nkb; ++kb) {
                 tc::mbar_wait(&hdr->empty[stage], phase ^ 1);
                 if (elect_one()) {
@@ -497,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
             int64_t mt, nt;
             tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
+            mt += mt_off;
             const int64_t row = mt * kBM + q * 32 + lane;
             const bool row_ok = row < g.M;
             const int ea = row_ok ? g.scale_a[row] : 0;
@@ -683,7 +689,9 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
         e.cap = cap;
         e.nb = nb;
     }
-    const int64_t tiles = ((g.M + kBM - 1) / kBM) * ((g.N + nb - 1) / nb);
+    const int64_t mt_total = (g.M + kBM - 1) / kBM;
+    const int64_t mt_end = g.mt_end > 0 && g.mt_end < mt_total ? g.mt_end : mt_total;
+    const int64_t tiles = (mt_end - g.mt_begin) * ((g.N + nb - 1) / nb);
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
     GemmArgs a = g;
