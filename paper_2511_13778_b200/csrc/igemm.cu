@@ -506,6 +506,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t row = mt * kBM + q * 32 + lane;
             const bool row_ok = row < g.M;
             const int ea = row_ok ? g.scale_a[row] : 0;
+            // the warp's column scales, one per lane (kCols <= 32), fetched before
+            // waiting for the accumulators and shuffled out per element
+            const int64_t lane_col = nt * NB + jh * kCols + lane;
+            const int eb_lane = (lane < kCols && lane_col < g.N) ? __ldg(g.scale_b + lane_col) : 0;
             for (int c = 0; c < lp.nchunks; ++c) {
                 tc::mbar_wait(&hdr->tmem_full, acc_phase);
                 tc::fence_after();
@@ -515,15 +519,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int j0 = jh * kCols; j0 < (jh + 1) * kCols; j0 += C::kCW) {
                     int eb[C::kCW];
 #pragma unroll
-                    for (int cc = 0; cc < C::kCW; ++cc) {
-                        const int64_t col = nt * NB + j0 + cc;
-                        eb[cc] = col < g.N ? __ldg(g.scale_b + col) : 0;
-                    }
+                    for (int cc = 0; cc < C::kCW; ++cc) eb[cc] = __shfl_sync(0xffffffffu, eb_lane, j0 - jh * kCols + cc);
                     uint32_t v[C::kNDMax][C::kCW];
 #pragma unroll
                     for (int D = 0; D < C::kNDMax; ++D)
                         if (D < ndiag) tc::tmem_ld<C::kCW>(trow + uint32_t(D * NB + j0), v[D]);
                     tc::tmem_wait_ld();
+                    if (j0 + C::kCW >= (jh + 1) * kCols) {
+                        // every accumulator this warp needs is in registers: hand TMEM back
+                        // to the MMA warp now, the last batch's math overlaps its next tile
+                        tc::fence_before();
+                        tc::mbar_arrive(&hdr->tmem_empty);
+                    }
 #pragma unroll
                     for (int cc = 0; cc < C::kCW; ++cc) {
                         const int64_t col = nt * NB + j0 + cc;
@@ -595,8 +602,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         g.c_out[row + col * g.ldc] = r;
                     }
                 }
-                tc::fence_before();
-                tc::mbar_arrive(&hdr->tmem_empty);
                 acc_phase ^= 1;
             }
         }
