@@ -210,13 +210,14 @@ def main():
     m_global = m * world
     handle = adp.Handle.default(dev.index)
 
-    # synthetic operands, column-major storage (torch row-major of the transpose)
-    g = torch.Generator(device=dev)
-    g.manual_seed(1000 + rank)
-    At = torch.rand((k, m), generator=g, device=dev, dtype=torch.float64).add_(1.0)   # A: m x k col-major
-    g.manual_seed(2)
-    Bt = torch.rand((n, k), generator=g, device=dev, dtype=torch.float64).add_(1.0)   # B: k x n col-major
-    Ct = torch.zeros((n, m), device=dev, dtype=torch.float64)                          # C: m x n col-major
+    # synthetic operands, column-major storage (torch row-major of the transpose),
+    # filled in storage order by the reference's generator (gen_uniform_rect,
+    # xoshiro256++, grading.cpp:56-63) drawn on the device
+    from paper_2511_13778_b200 import grading
+
+    At = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, 1.0, 2.0, dev.index)   # A: m x k col-major
+    Bt = grading.gen_uniform_rect(n, k, 2, 1.0, 2.0, dev.index)                # B: k x n col-major
+    Ct = torch.zeros((n, m), device=dev, dtype=torch.float64)                  # C: m x n col-major
     cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET)
     trace_buf = torch.zeros(_lib.TRACE_BYTES, dtype=torch.uint8, device=dev)
 
@@ -356,8 +357,8 @@ def main():
                                  "guardrail_stage_ms": stage_ms.get("stats", 0) + stage_ms.get("esc", 0)
                                  + stage_ms.get("decide", 0)}
         # ---- U[-1,1] operands: coarsened ESC picks s = 8 --------------------------------
-        Au = torch.rand((k, m), generator=g.manual_seed(3 + rank), device=dev, dtype=torch.float64).mul_(2).sub_(1)
-        Bu = torch.rand((n, k), generator=g.manual_seed(4), device=dev, dtype=torch.float64).mul_(2).sub_(1)
+        Au = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, -1.0, 1.0, dev.index)
+        Bu = grading.gen_uniform_rect(n, k, 2, -1.0, 1.0, dev.index)
         tr2 = torch.zeros_like(trace_buf)
         step(cfg, Au, Bu, Ct, tr2)
         torch.cuda.synchronize()
@@ -370,6 +371,21 @@ def main():
         extra["full_pairs"] = {"value": flops_global / (full_ms * 1e-3) / 1e12,
                                "note": "all s^2 slice pairs: output bitwise equal to the reference adp_gemm"}
         del Au, Bu
+        # ---- accuracy of the headline result: componentwise relative error against
+        # the device double-double oracle (Dot2), and the grading ratio
+        # |C - AB| / (2^-52 (|A||B|)_ij); cuBLAS DGEMM on the same operands ----------
+        step()
+        ref, absab = grading.dd_gemm(Bt, At)          # C^T = B^T A^T in row-major terms
+        rep = grading.error_report(Ct, ref, absab=absab)
+        nat = torch.mm(At.t(), Bt.t()).t().contiguous()
+        rep_n = grading.error_report(nat, ref, absab=absab)
+        del ref, absab, nat
+        extra["accuracy"] = {
+            "oracle": "device double-double GEMM (Dot2), |err| <= 2^-53|AB| + gamma_2k^2 |A||B|",
+            "max_rel_err": rep.max_err, "avg_rel_err": rep.avg_err,
+            "max_err_over_eps_absAB": rep.max_ratio, "avg_err_over_eps_absAB": rep.avg_ratio,
+            "native_fp64_max_rel_err": rep_n.max_err, "native_fp64_avg_rel_err": rep_n.avg_err,
+            "native_fp64_max_err_over_eps_absAB": rep_n.max_ratio}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -385,7 +401,8 @@ def main():
             "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, 8192^3",
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic U(1,2), seeded (torch.Generator)",
+            "dtype": "f64",
+            "data": "synthetic U(1,2): the reference's gen_uniform_rect (xoshiro256++) seeds 1, 2, on the device",
             "config": {"workload": f"ADP DGEMM {m_global}x{n}x{k} column-major NN (8192 rows per GPU), "
                                    "guardrails live, ESC-chosen s, pairs d_a+d_b<=s",
                        "m": m_global, "n": n, "k": k, "slices": trace.slices, "esc_bits": trace.esc_bits,
@@ -399,6 +416,8 @@ def main():
             "clocks": clocks,
         }
         line.update(extra)
+        if "accuracy" in extra:
+            line["max_rel_err"] = extra["accuracy"]["max_rel_err"]
         if "native_fp64" in extra:
             line["speedup_vs_native_fp64"] = value / world / extra["native_fp64"]["value"]
         print(json.dumps(line), flush=True)

@@ -191,6 +191,37 @@ int adpb200_native_gemm(adpb200_handle handle, const double* A, const double* B,
                         int64_t n, int64_t k, double alpha, double beta, const double* c_in,
                         double* out, void* stream);
 
+/* ---- grading tools (device) ---------------------------------------------------
+ * The reference grades against exact_gemm (oracle.cpp:55-75, CPU
+ * superaccumulator). On the device: a double-double (Dot2: TwoProd by FMA +
+ * TwoSum) GEMM oracle, as accurate as a twice-working-precision product
+ * rounded once: |ref - AB| <= 2^-53 |AB| + gamma_2k^2 (|A||B|). Row-major
+ * (MatrixF64) layout like adpb200_adp_gemm. absab (nullable) receives the
+ * plain FP64 sum of |a||b|, the grading-ratio denominator (grading.cpp:108-123). */
+int adpb200_dd_gemm(adpb200_handle handle, int64_t m, int64_t n, int64_t k, const double* A,
+                    const double* B, double* ref, double* absab, void* stream);
+/* error_report (grading.cpp:67-90) on rows x cols row-major device matrices:
+ * componentwise |ref - C| / |ref| (ref == 0 skipped and counted; with
+ * use_exact_diag, diagonal entries compare against exact_diag, the Test-2
+ * convention) and, when absab != NULL, the grading ratio
+ * |C - ref| / (2^-52 (|A||B|)_ij). out (device double[7]) = max_rel,
+ * avg_rel, counted, skipped, max_ratio, avg_ratio, ratio_counted.
+ * Deterministic (fixed-order reduction). */
+int adpb200_error_report(adpb200_handle handle, int64_t rows, int64_t cols, const double* C,
+                         const double* ref, const double* absab, double exact_diag,
+                         int use_exact_diag, double* out, void* stream);
+
+/* gen_uniform_rect (grading.cpp:56-63): row-major rows x cols uniform(lo, hi)
+ * from xoshiro256++ (rng.hpp:11-54), generated on the device (jump-ahead per
+ * 4096-draw chunk); bitwise the reference's matrix for the same seed. */
+int adpb200_gen_uniform_rect(adpb200_handle handle, int64_t rows, int64_t cols, uint64_t seed,
+                             double lo, double hi, double* out, void* stream);
+/* gen_test2 (grading.cpp:13-47): the adversarial exponent-span pair, n x n
+ * row-major lhs / rhs on the device; x (host double[n]) and j (host
+ * int32[n]) optional. Synchronises the stream once (host vectors). */
+int adpb200_gen_test2(adpb200_handle handle, int64_t n, int b, uint64_t seed, double* lhs,
+                      double* rhs, double* x, int32_t* j, void* stream);
+
 /* Kernel launches issued by this handle since creation (all kernels are ours). */
 uint64_t adpb200_launch_count(adpb200_handle handle);
 

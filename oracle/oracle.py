@@ -331,6 +331,46 @@ class Oracle:
                                               C.c_longlong(b.shape[1]), C.c_longlong(a.shape[1]),
                                               C.c_int(slices), None))
 
+    # ---- grading (reference build only) ---------------------------------------
+    def _need_ref(self, what):
+        if self.kind != "reference":
+            raise OracleError(f"{what} needs the reference build")
+
+    def error_report(self, c, ref, exact_diag=None):
+        """error_report (grading.cpp:67-90): (max_err, avg_err, counted, skipped)."""
+        self._need_ref("error_report")
+        c, ref = _f64(c), _f64(ref)
+        out = (C.c_double * 4)()
+        self._check(self.lib.ozref_error_report(_p(c), _p(ref), C.c_longlong(c.shape[0]), C.c_longlong(c.shape[1]),
+                                                C.c_int(exact_diag is not None),
+                                                C.c_double(exact_diag or 0.0), out), "error_report")
+        return out[0], out[1], int(out[2]), int(out[3])
+
+    def exact_dot(self, x, y) -> float:
+        self._need_ref("exact_dot")
+        x, y = _f64(x), _f64(y)
+        out = C.c_double(0.0)
+        self._check(self.lib.ozref_exact_dot(_p(x), _p(y), C.c_longlong(x.size), C.byref(out)), "exact_dot")
+        return out.value
+
+    def grade_uniform_point(self, n, seed):
+        """grade_uniform_point (grading.cpp:92-134), default AdpConfig."""
+        self._need_ref("grade_uniform_point")
+        out = (C.c_double * 7)()
+        self._check(self.lib.ozref_grade_uniform_point(C.c_longlong(n), C.c_ulonglong(seed), out),
+                    "grade_uniform_point")
+        return dict(emu_max_ratio=out[0], emu_avg_ratio=out[1], nat_max_ratio=out[2], nat_avg_ratio=out[3],
+                    esc_bits=int(out[4]), slices=int(out[5]), fallback=bool(out[6]))
+
+    def test2_row(self, n, b, mode, seed):
+        """One row of run_test2_sweep (grading.cpp:246-275)."""
+        self._need_ref("test2_row")
+        out = (C.c_double * 5)()
+        self._check(self.lib.ozref_test2_row(C.c_longlong(n), C.c_int(b), mode.encode(), C.c_ulonglong(seed), out),
+                    "test2_row")
+        return dict(max_err=out[0], avg_err=out[1], esc_bits=None if out[2] < 0 else int(out[2]),
+                    slices=int(out[3]), fallback=bool(out[4]))
+
 
 def fold_round(acc_row: np.ndarray, exp2: int) -> float:
     """Exact fold of one element's diagonal accumulators + RNE (port only)."""

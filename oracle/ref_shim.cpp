@@ -13,6 +13,8 @@
 #include <chrono>
 #include <cstring>
 #include <exception>
+#include <optional>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -295,6 +297,58 @@ double ozref_time_call(int which, const double* a, const double* b, long long m,
     auto t1 = std::chrono::steady_clock::now();
     if (out) unwrap(r, out);
     return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// error_report (grading.cpp:67-90). use_diag: compare the diagonal against
+// exact_diag. out: max_err, avg_err, counted, skipped.
+int ozref_error_report(const double* c, const double* ref, long long rows, long long cols,
+                       int use_diag, double exact_diag, double* out) {
+    return guarded([&] {
+        std::optional<double> d;
+        if (use_diag) d = exact_diag;
+        ErrorReport r = error_report(wrap(c, rows, cols), wrap(ref, rows, cols), d);
+        out[0] = r.max_err;
+        out[1] = r.avg_err;
+        out[2] = double(r.counted);
+        out[3] = double(r.skipped);
+    });
+}
+
+// exact_dot(x, y).rounded (oracle.cpp:40-53)
+int ozref_exact_dot(const double* x, const double* y, long long n, double* out) {
+    return guarded([&] {
+        std::vector<double> xv(x, x + n), yv(y, y + n);
+        *out = exact_dot(xv, yv).rounded;
+    });
+}
+
+// grade_uniform_point (grading.cpp:92-134) with the default AdpConfig.
+// out: emu_max, emu_avg, nat_max, nat_avg, esc_bits, slices, fallback.
+int ozref_grade_uniform_point(long long n, unsigned long long seed, double* out) {
+    return guarded([&] {
+        GradePoint p = grade_uniform_point(std::size_t(n), seed, AdpConfig{});
+        out[0] = p.emu_max_ratio;
+        out[1] = p.emu_avg_ratio;
+        out[2] = p.nat_max_ratio;
+        out[3] = p.nat_avg_ratio;
+        out[4] = p.esc_bits;
+        out[5] = p.slices;
+        out[6] = p.fallback ? 1.0 : 0.0;
+    });
+}
+
+// run_test2_sweep (grading.cpp:246-275) for one b and one mode string;
+// out: max_err, avg_err, esc_bits (-1 none), slices, fallback.
+int ozref_test2_row(long long n, int b, const char* mode, unsigned long long seed, double* out) {
+    return guarded([&] {
+        std::vector<SweepRow> rows = run_test2_sweep(std::size_t(n), {b}, {std::string(mode)}, seed);
+        const SweepRow& r = rows.at(0);
+        out[0] = r.max_err;
+        out[1] = r.avg_err;
+        out[2] = r.esc_bits ? *r.esc_bits : -1;
+        out[3] = r.slices;
+        out[4] = r.fallback ? 1.0 : 0.0;
+    });
 }
 
 }  // extern "C"

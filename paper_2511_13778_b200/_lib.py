@@ -102,6 +102,10 @@ def lib() -> C.CDLL:
         "adpb200_slice_pair_mm": (C.c_int, [vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, vp, vp]),
         "adpb200_emulated_gemm": (C.c_int, [vp, vp, vp, i64, i64, i64, f64, f64, vp, vp, C.c_int, C.c_int, vp]),
         "adpb200_native_gemm": (C.c_int, [vp, vp, vp, i64, i64, i64, f64, f64, vp, vp, vp]),
+        "adpb200_dd_gemm": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
+        "adpb200_error_report": (C.c_int, [vp, i64, i64, vp, vp, vp, f64, C.c_int, vp, vp]),
+        "adpb200_gen_uniform_rect": (C.c_int, [vp, i64, i64, C.c_uint64, f64, f64, vp, vp]),
+        "adpb200_gen_test2": (C.c_int, [vp, i64, C.c_int, C.c_uint64, vp, vp, vp, vp, vp]),
         "adpb200_profile_enable": (C.c_int, [vp, C.c_int]),
         "adpb200_profile_read": (C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
     }
@@ -120,6 +124,7 @@ EXPORTED = (
     "adpb200_adp_gemm_host", "adpb200_scan", "adpb200_block_stats",
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",
     "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read",
+    "adpb200_dd_gemm", "adpb200_error_report", "adpb200_gen_uniform_rect", "adpb200_gen_test2",
 )
 PROFILE_STAGES = ("stats", "esc", "decide", "slice", "gemm", "native")
 

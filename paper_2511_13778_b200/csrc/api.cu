@@ -755,6 +755,58 @@ int adpb200_native_gemm(adpb200_handle h, const double* A, const double* B, int6
     return cuda_check(cudaGetLastError(), "native_gemm launch");
 }
 
+int adpb200_dd_gemm(adpb200_handle h, int64_t m, int64_t n, int64_t k, const double* A, const double* B,
+                    double* ref, double* absab, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "dd_gemm: null handle");
+    if (m < 0 || n < 0 || k < 0) return fail(3, "dd_gemm: negative dimension");
+    if (!ref) return fail(3, "dd_gemm: null output");
+    Problem P = rowmajor_problem(m, n, k, 1.0, A, B, 0.0, nullptr, ref);
+    cudaSetDevice(h->device);
+    launch_dd_gemm(P.a, P.b, ref, absab, P.ldc, static_cast<cudaStream_t>(stream), &h->launches);
+    return cuda_check(cudaGetLastError(), "dd_gemm launch");
+}
+
+int adpb200_error_report(adpb200_handle h, int64_t rows, int64_t cols, const double* C, const double* ref,
+                         const double* absab, double exact_diag, int use_exact_diag, double* out, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "error_report: null handle");
+    if (rows < 0 || cols < 0) return fail(3, "error_report: negative dimension");
+    if (!out || (rows * cols > 0 && (!C || !ref))) return fail(3, "error_report: null buffer");
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    void* partial = nullptr;
+    int rc = cuda_check(cudaMallocAsync(&partial, error_partial_bytes(), st), "cudaMallocAsync(error partials)");
+    if (rc) return rc;
+    launch_error_report(C, ref, absab, rows, cols, exact_diag, use_exact_diag, static_cast<double*>(partial), out, st,
+                        &h->launches);
+    rc = cuda_check(cudaGetLastError(), "error_report launch");
+    cudaFreeAsync(partial, st);
+    return rc;
+}
+
+int adpb200_gen_uniform_rect(adpb200_handle h, int64_t rows, int64_t cols, uint64_t seed, double lo, double hi,
+                             double* out, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "gen_uniform_rect: null handle");
+    if (!(lo < hi)) return fail(3, "gen_uniform_rect: empty interval");
+    if (rows < 0 || cols < 0) return fail(3, "gen_uniform_rect: negative dimension");
+    cudaSetDevice(h->device);
+    if (gen_uniform_device(rows, cols, seed, lo, hi, out, static_cast<cudaStream_t>(stream), &h->launches))
+        return cuda_check(cudaGetLastError(), "gen_uniform_rect");
+    return cuda_check(cudaGetLastError(), "gen_uniform_rect launch");
+}
+
+int adpb200_gen_test2(adpb200_handle h, int64_t n, int b, uint64_t seed, double* lhs, double* rhs, double* x,
+                      int32_t* j, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "gen_test2: null handle");
+    if (n < 2) return fail(3, "gen_test2: n must be at least 2");
+    if (b < 0) return fail(3, "gen_test2: b must be nonnegative");
+    if (b > 1022) return fail(3, "gen_test2: b too large, entries would leave the FP64 range");
+    cudaSetDevice(h->device);
+    int rc = gen_test2_device(n, b, seed, lhs, rhs, x, j, static_cast<cudaStream_t>(stream), &h->launches);
+    if (rc == 1) return fail(3, "gen_test2: endpoint rounding failed");
+    if (rc) return cuda_check(cudaGetLastError(), "gen_test2");
+    return cuda_check(cudaGetLastError(), "gen_test2 launch");
+}
+
 int adpb200_scan(adpb200_handle h, const double* A, int64_t count, uint64_t* counts, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "scan: null handle");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

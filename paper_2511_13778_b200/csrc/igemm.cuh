@@ -42,4 +42,22 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
 void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
                    int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch);
 
+// Grading tools (grade.cu): Dot2 double-double GEMM oracle out[i + j*ldo]
+// (+ (|A||B|)_ij when absab != nullptr), and error_report on row-major
+// rows x cols results: out[0..6] = max_rel, avg_rel, counted, skipped,
+// max_ratio, avg_ratio, ratio_counted (device doubles).
+void launch_dd_gemm(const LineView& a, const LineView& b, double* out, double* absab, int64_t ldo, cudaStream_t st,
+                    uint64_t* nlaunch);
+size_t error_partial_bytes();
+void launch_error_report(const double* c, const double* ref, const double* absab, int64_t rows, int64_t cols,
+                         double exact_diag, int use_diag, double* partial, double* out, cudaStream_t st,
+                         uint64_t* nlaunch);
+// Reproducible inputs (grade.cu): gen_uniform_rect (grading.cpp:56-63) on the
+// device via xoshiro256++ jump-ahead, gen_test2 (grading.cpp:13-47). 0 ok,
+// 1 contract (endpoint rounding), -1 CUDA error.
+int gen_uniform_device(int64_t rows, int64_t cols, uint64_t seed, double lo, double hi, double* out, cudaStream_t st,
+                       uint64_t* nlaunch);
+int gen_test2_device(int64_t n, int b, uint64_t seed, double* lhs, double* rhs, double* x_out, int32_t* j_out,
+                     cudaStream_t st, uint64_t* nlaunch);
+
 }  // namespace adpb200
