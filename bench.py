@@ -387,6 +387,26 @@ def main():
             "native_fp64_max_rel_err": rep_n.max_err, "native_fp64_avg_rel_err": rep_n.avg_err,
             "native_fp64_max_err_over_eps_absAB": rep_n.max_ratio}
 
+        # ---- BASELINE config 5 (rectangular / long-k), U[-1,1] reference inputs -----------
+        rect = {}
+        for name, (rm, rn, rk) in (("c5a_4096x4096x65536", (4096, 4096, 65536)),
+                                   ("c5b_65536x1024x1024", (65536, 1024, 1024))):
+            Ar = grading.gen_uniform_rect(rm, rk, 1, -1.0, 1.0, dev.index)
+            Br = grading.gen_uniform_rect(rk, rn, 2, -1.0, 1.0, dev.index)
+            Cr = torch.empty((rm, rn), dtype=torch.float64, device=dev)
+            _, tr = adp.adp_gemm(Ar, Br, config=cfg, handle=handle, out=Cr)
+            r_ms = timed(lambda: adp.adp_gemm(Ar, Br, config=cfg, handle=handle, out=Cr), 5, 1)
+            f7 = adp.AdpConfig(mode=adp.AdpMode.ForceEmulate, forced_slices=7, pair_limit=adp.PAIRS_TARGET)
+            r7_ms = timed(lambda: adp.adp_gemm(Ar, Br, config=f7, handle=handle, out=Cr), 5, 1)
+            rn_ms = timed(lambda: torch.mm(Ar, Br, out=Cr), 5, 1)
+            fl = 2.0 * rm * rn * rk
+            rect[name] = {"adp_tflops": fl / r_ms / 1e9, "slices": tr.slices, "esc_bits": tr.esc_bits,
+                          "pairs": tr.pairs, "k_chunks": tr.k_chunks, "emulate7_tflops": fl / r7_ms / 1e9,
+                          "cublas_dgemm_tflops": fl / rn_ms / 1e9, "adp_vs_cublas": rn_ms / r_ms}
+            del Ar, Br, Cr
+        torch.cuda.empty_cache()
+        extra["rectangular"] = rect
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

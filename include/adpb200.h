@@ -149,6 +149,38 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
                        const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                        const adpb200_options* opt, adpb200_trace* trace, int32_t* xchg, void* stream);
 
+/* B-distributed row partition (the north star's multi-GPU layout): rank r
+ * of `world` owns rows [r0, r0+m) of op(A) and C (all n columns) and the
+ * column slab r of B: k x (n/world), column-major, leading dimension k.
+ * n/world must be a multiple of 8. Four stream-ordered phases; the caller runs
+ * the collectives between them (NCCL over NVLink; sizes from
+ * adpb200_dist_sizes, out[0..3] = bstats record int32 count, slab header
+ * bytes, bytes per slab plane, slab capacity bytes):
+ *   phase 1  exponent stats of the A rows and of the B slab -> bstats_local
+ *            (record int32[out[0]])            -> all-gather into bstats_all
+ *   phase 2  ESC of the local rows against every B column -> xchg (int32[2])
+ *                                              -> max-allreduce xchg
+ *   phase 3  decision with the global dimensions; slice the A rows; slice the
+ *            B slab into `slab` = [scale | planes]. The caller copies xchg to
+ *            the host and calls adpb200_dist_decision -> nsl planes:
+ *              nsl > 0: all-gather the first out[1] + nsl*out[2] bytes of slab
+ *              nsl = 0 (native fallback): all-gather the FP64 B slabs (= B)
+ *   phase 4  gathered records -> the GEMM's plane layout, tcgen05 GEMM of the
+ *            local rows (or the native GEMM against the gathered B).
+ * Same decision and slice count on every rank: the assembled C is
+ * bit-identical to the single-GPU adpb200_dgemm('N'/transa, 'N'). */
+int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]);
+/* decide() on the reduced xchg (host copy): out = path, slices, nsl (planes to
+ * gather; 0 on the native path), GEMM variant. */
+int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global,
+                          int64_t n, int64_t k, int32_t out[4]);
+int adpb200_dgemm_dist(adpb200_handle handle, int phase, int64_t m_global, int world, char transa,
+                       int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                       const double* B_slab, double beta, double* C, int64_t ldc,
+                       const adpb200_options* opt, adpb200_trace* trace, int32_t* bstats_local,
+                       const int32_t* bstats_all, int32_t* xchg, int8_t* slab,
+                       const void* gathered, int nsl, void* stream);
+
 /* ---- stage exports (parity surface; row-major device buffers) --------------- */
 
 /* decide() (adp.cpp:46-96) evaluated on the HOST by the same code the

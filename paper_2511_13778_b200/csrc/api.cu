@@ -323,6 +323,122 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     return cuda_check(cudaGetLastError(), "kernel launch");
 }
 
+// ---- B-distributed multi-GPU path (adpb200_dgemm_dist) -------------------------------
+// Rank r of `world` owns rows of op(A) / C and a column slab of B (k x nr,
+// column-major, compact). Phases (collectives between them are the caller's):
+//   1  stats(A rows) -> workspace; stats(B slab) -> bstats_local      | all-gather bstats
+//   2  ESC(A rows x all B columns) -> xchg = {exc, esc}               | max-allreduce xchg
+//   3  decide (global dims) ; slice A rows ; slice B slab -> slab     | all-gather slab prefix
+//                                                                       (or B itself on fallback)
+//   4  gathered records -> global B planes + scales ; tcgen05 GEMM   (or native GEMM)
+struct DistIO {
+    int world;
+    int64_t nr;              // B columns per rank
+    int32_t* bstats_local;   // [bmax t x nr][bmin t x nr][bline nr]
+    const int32_t* bstats_all;
+    int32_t* xchg;
+    int8_t* slab;            // [scale nr int32 | pad to kSlabHdr][cap planes of nkb x nr x 32 B]
+    const void* gathered;    // phase 4: world slab records of nsl planes, or the FP64 B (k x n)
+    int nsl;                 // planes per gathered record; 0 = native fallback
+};
+
+int64_t slab_hdr(int64_t nr) { return (int64_t)align_up(size_t(nr) * 4, 1024); }
+
+int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace, cudaStream_t st,
+             int phase, const DistIO& io) {
+    const int cap = plane_cap(o, 0, 0);
+    const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
+    int rc = ensure_ws(h, Lw.total, st);
+    if (rc) return rc;
+    uint64_t* nl = &h->launches;
+    StageTimer tm(h, st);
+    Plan* plan = at<Plan>(h, Lw.plan);
+    int32_t* amax = at<int32_t>(h, Lw.stats_a_max);
+    int32_t* amin = at<int32_t>(h, Lw.stats_a_min);
+    int32_t* aline = at<int32_t>(h, Lw.line_a);
+    const int64_t t = Lw.blocks, nr = io.nr;
+    const int64_t rec = 2 * t * nr + nr;
+    const bool native_only = o.mode == ADPB200_MODE_NATIVE;
+    const int64_t mn = std::min(std::min(P.tm, P.tn), P.tk);
+    const bool esc_expected = (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
+                              mn >= o.min_dim;
+    const LineView bslab{P.b.ptr, nr, P.K, P.K, 1};
+    if (phase == 1) {
+        rc = cuda_check(cudaMemsetAsync(plan, 0, sizeof(Plan), st), "cudaMemsetAsync(plan)");
+        if (rc) return rc;
+        tm.begin(0);
+        if (!native_only) {
+            if (P.M > 0) launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
+            launch_stats(bslab, o.esc_block_len, io.bstats_local, io.bstats_local + t * nr, io.bstats_local + 2 * t * nr,
+                         plan->counts + 3, &plan->exc, 2, 1, st, nl);
+        }
+        tm.end(0);
+        return cuda_check(cudaGetLastError(), "dist phase 1");
+    }
+    if (phase == 2) {
+        tm.begin(1);
+        if (esc_expected && P.M > 0)
+            launch_esc(amax, amin, aline, io.bstats_all, io.bstats_all + t * nr, io.bstats_all + 2 * t * nr, P.M, P.N,
+                       t, plan, &plan->esc_raw, &plan->esc_ran, st, nl, nr, rec);
+        tm.end(1);
+        rc = cuda_check(cudaMemcpyAsync(io.xchg, &plan->exc, 8, cudaMemcpyDeviceToDevice, st), "export xchg");
+        return rc ? rc : cuda_check(cudaGetLastError(), "dist phase 2");
+    }
+    if (phase == 3) {
+        rc = cuda_check(cudaMemcpyAsync(&plan->exc, io.xchg, 8, cudaMemcpyDeviceToDevice, st), "import xchg");
+        if (rc) return rc;
+        tm.begin(2);
+        launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, 0, trace, st, nl);
+        tm.end(2);
+        if (cap > 0) {
+            tm.begin(3);
+            launch_slice(P.a, aline, at<int8_t>(h, Lw.planes_a), Lw.slots_a, Lw.pitch * Lw.slots_a, 1,
+                         at<int32_t>(h, Lw.scale_a), plan, 0, cap, st, nl);
+            launch_slice(bslab, io.bstats_local + 2 * t * nr, io.slab + slab_hdr(nr), nr, Lw.pitch * nr, 1,
+                         reinterpret_cast<int32_t*>(io.slab), plan, 0, cap, st, nl);
+            tm.end(3);
+        }
+        return cuda_check(cudaGetLastError(), "dist phase 3");
+    }
+    // phase 4
+    if (io.nsl > 0) {
+        int8_t* pa = at<int8_t>(h, Lw.planes_a);
+        int8_t* pb = at<int8_t>(h, Lw.planes_b);
+        int32_t* sb = at<int32_t>(h, Lw.scale_b);
+        const int64_t nkb = Lw.pitch / 32;
+        const int64_t rec_bytes = slab_hdr(nr) + int64_t(io.nsl) * nkb * nr * 32;
+        tm.begin(3);
+        launch_gather_planes(static_cast<const int8_t*>(io.gathered), rec_bytes, slab_hdr(nr), io.world, nr, nkb,
+                             io.nsl, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb, st, nl);
+        tm.end(3);
+        GemmArgs g{};
+        g.plan = plan;
+        g.M = P.M;
+        g.N = P.N;
+        g.K = P.K;
+        g.scale_a = at<int32_t>(h, Lw.scale_a);
+        g.scale_b = sb;
+        g.alpha = P.alpha;
+        g.beta = P.beta;
+        g.c_out = P.c_out;
+        g.ldc = P.ldc;
+        g.c_in = P.c_in;
+        g.ldc_in = P.ldc_in;
+        g.partial = at<uint64_t>(h, Lw.partial);
+        tm.begin(4);
+        for (int nb : {64, 48, 32, 16, 8})
+            if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, nkb, cap, g, st, nl))
+                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+        tm.end(4);
+    } else {
+        const LineView bfull{static_cast<const double*>(io.gathered), P.N, P.K, P.K, 1};
+        tm.begin(5);
+        launch_native(P.a, bfull, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+        tm.end(5);
+    }
+    return cuda_check(cudaGetLastError(), "dist phase 4");
+}
+
 // Row-major product out = alpha*A*B + beta*c_in (MatrixF64 layout) expressed
 // in the internal orientation by the exact operand swap C^T = B^T A^T:
 // internal A-lines = columns of B, B-lines = rows of A, out(i,j) = C[j][i].
@@ -558,6 +674,89 @@ int adpb200_dgemm_rows(adpb200_handle h, int phase, int64_t m_global, char trans
     P.tk = k;
     cudaSetDevice(h->device);
     return run_pipeline(h, P, o, trace, static_cast<cudaStream_t>(stream), 0, 0, nullptr, 0, phase, xchg);
+}
+
+int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]) {
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    if (world < 1 || n <= 0 || k <= 0 || n % world != 0 || (n / world) % 8 != 0)
+        return fail(3, "dist: need n, k > 0 and n divisible by world with n / world a multiple of 8");
+    const int64_t nr = n / world;
+    const int64_t t = (k + o.esc_block_len - 1) / o.esc_block_len;
+    const int64_t pitch = (int64_t)align_up(size_t(k), 32);
+    out[0] = 2 * t * nr + nr;
+    out[1] = slab_hdr(nr);
+    out[2] = pitch * nr;
+    out[3] = out[1] + int64_t(plane_cap(o, 0, 0)) * out[2];
+    return ADPB200_OK;
+}
+
+int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global, int64_t n, int64_t k,
+                          int32_t out[4]) {
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int rc = adpb200_validate_options(&o);
+    if (rc) return rc;
+    DecideInput in{xchg[0] & 1, (xchg[0] >> 1) & 1, m_global, n, k, xchg[1]};
+    DecideOutput d = decide(in, o);
+    out[0] = d.path;
+    out[1] = d.path == ADPB200_PATH_EMULATED ? d.slices : 0;
+    out[2] = 0;
+    out[3] = 0;
+    if (d.path == ADPB200_PATH_EMULATED) {
+        Plan p{};
+        fill_emulation_plan(p, d.slices, o.pair_limit, k);
+        out[2] = p.nsl;
+        out[3] = p.variant;
+    }
+    return ADPB200_OK;
+}
+
+int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world, char transa, int64_t m, int64_t n,
+                       int64_t k, double alpha, const double* A, int64_t lda, const double* B_slab, double beta,
+                       double* C, int64_t ldc, const adpb200_options* opt, adpb200_trace* trace,
+                       int32_t* bstats_local, const int32_t* bstats_all, int32_t* xchg, int8_t* slab,
+                       const void* gathered, int nsl, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_dist: null handle");
+    if (phase < 1 || phase > 4) return fail(3, "dgemm_dist: phase must be 1..4");
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    int64_t sz[4];
+    int rc = adpb200_dist_sizes(n, k, world, &o, sz);
+    if (rc) return rc;
+    if (!trans_ok(transa)) return fail(3, "dgemm: bad trans flag");
+    if (m < 0 || m_global < m) return fail(3, "dgemm_dist: bad m / m_global");
+    const int64_t arows = is_n(transa) ? m : k;
+    if (lda < std::max<int64_t>(1, arows)) return fail(3, "dgemm: lda too small");
+    if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
+    if (beta != 0.0 && !C) return fail(3, "dgemm_dist: beta != 0 needs C");
+    if ((phase == 1 && !bstats_local) || (phase == 2 && (!bstats_all || !xchg)) ||
+        (phase == 3 && (!xchg || !slab || !bstats_local)) || (phase == 4 && !gathered))
+        return fail(3, "dgemm_dist: missing exchange buffer for this phase");
+    if (phase == 4 && (nsl < 0 || nsl > plane_cap(o, 0, 0))) return fail(3, "dgemm_dist: bad nsl");
+    Problem P{};
+    P.M = m;
+    P.N = n;
+    P.K = k;
+    P.a = is_n(transa) ? LineView{A, m, k, 1, lda} : LineView{A, m, k, lda, 1};
+    P.b = LineView{B_slab, n / world, k, k, 1};
+    P.alpha = alpha;
+    P.beta = beta;
+    P.c_in = C;
+    P.ldc_in = ldc;
+    P.c_out = C;
+    P.ldc = ldc;
+    P.tm = m_global;
+    P.tn = n;
+    P.tk = k;
+    DistIO io{world, n / world, bstats_local, bstats_all, xchg, slab, gathered, nsl};
+    cudaSetDevice(h->device);
+    return run_dist(h, P, o, trace, static_cast<cudaStream_t>(stream), phase, io);
 }
 
 int adpb200_adp_gemm(adpb200_handle h, int64_t m, int64_t n, int64_t k, double alpha, const double* A,

@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
                                                   const int32_t* __restrict__ bmaxT,
                                                   const int32_t* __restrict__ bminT,
                                                   const int32_t* __restrict__ bline, int64_t m, int64_t n,
-                                                  int64_t t, const Plan* plan, int32_t* esc_out,
-                                                  int32_t* ran_flag) {
+                                                  int64_t t, int64_t nr, int64_t rec, const Plan* plan,
+                                                  int32_t* esc_out, int32_t* ran_flag) {
     if (plan && plan->exc) return;  // exceptional inputs never reach the ESC (adp.cpp:58-62)
     // A words hold (a, a); B words hold (b_j, b_j+1) for the thread's j pairs
     __shared__ __align__(16) uint32_t sAmx[kEscTB][kEscBI];
@@ -261,12 +261,19 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
             const int jp = idx % (kEscBJ / 2), tt = idx / (kEscBJ / 2);
             const int64_t gj = j0 + 2 * jp, gt = tb + tt;
             const bool ok0 = gj < n && gt < t, ok1 = gj + 1 < n && gt < t;
-            sBmx[tt][jp] = pack2(ok0 ? to16(bmaxT[gt * n + gj]) : kS16, ok1 ? to16(bmaxT[gt * n + gj + 1]) : kS16);
-            sBmn[tt][jp] = pack2(ok0 ? to16(bminT[gt * n + gj]) : kS16, ok1 ? to16(bminT[gt * n + gj + 1]) : kS16);
+            // B stats of column slabs of nr lines, one record of `rec` int32 per slab
+            // (the all-gathered layout of the B-distributed path; nr = n: one slab)
+            const int64_t r0 = gj / nr, r1 = (gj + 1) / nr;
+            const int64_t o0 = r0 * rec + gt * nr + (gj - r0 * nr), o1 = r1 * rec + gt * nr + (gj + 1 - r1 * nr);
+            sBmx[tt][jp] = pack2(ok0 ? to16(bmaxT[o0]) : kS16, ok1 ? to16(bmaxT[o1]) : kS16);
+            sBmn[tt][jp] = pack2(ok0 ? to16(bminT[o0]) : kS16, ok1 ? to16(bminT[o1]) : kS16);
         }
         __syncthreads();
+        // only the staged blocks (short k, e.g. 4 blocks at k = 1024, would
+        // otherwise spend 7/8 of the max-plus on sentinel padding)
+        const int tcount = t - tb < kEscTB ? int(t - tb) : kEscTB;
 #pragma unroll 4
-        for (int tt = 0; tt < kEscTB; ++tt) {
+        for (int tt = 0; tt < tcount; ++tt) {
             const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
             const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
             const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
@@ -298,7 +305,8 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
                 if (gj >= n) continue;
                 const int zz = int(int16_t(z[a][b] >> (16 * h)));
                 if (zz <= -8000) continue;  // structurally zero dot product
-                esc = max(esc, la + bline[gj] - zz + 1);
+                const int64_t rj = gj / nr;
+                esc = max(esc, la + bline[rj * rec + (gj - rj * nr)] - zz + 1);
             }
     }
     esc = warp_max(esc);
@@ -434,10 +442,13 @@ void launch_scan(const double* a, int64_t count, unsigned long long* counts, int
 
 void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
                 const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
-                int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch) {
+                int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch, int64_t b_nr,
+                int64_t b_rec) {
     if (m == 0 || n == 0) return;
+    if (b_nr <= 0) b_nr = n;
     dim3 grid((unsigned)((n + kEscBJ - 1) / kEscBJ), (unsigned)((m + kEscBI - 1) / kEscBI));
-    esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, plan, esc_out, ran_flag);
+    esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, plan, esc_out,
+                                     ran_flag);
     ++*nlaunch;
 }
 

@@ -14,9 +14,20 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
 void launch_scan(const double* a, int64_t count, unsigned long long* counts, int32_t* exc, cudaStream_t st,
                  uint64_t* nlaunch);
 // K2: coarsened ESC over block-major stats (atomicMax into esc_out, which must start at 0).
+// B stats may come as column slabs of b_nr lines, slab r's record starting at
+// r * b_rec int32 (bmax/bmin/bline pointers at their offsets inside record 0);
+// b_nr = 0: one slab of all n lines.
 void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
                 const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
-                int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch);
+                int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch, int64_t b_nr = 0,
+                int64_t b_rec = 0);
+
+// Multi-GPU B-distributed path: copy all-gathered slab records
+// ([scale int32 x nr | pad to hdr][nsl planes of nkb x nr x 32 B]) into the
+// GEMM's blocked plane layout (global line = r * nr + local) and scale_b.
+void launch_gather_planes(const int8_t* recs, int64_t rec_bytes, int64_t hdr, int world, int64_t nr, int64_t nkb,
+                          int nsl, int8_t* planes, int64_t slots, int64_t plane_stride, int32_t* scale,
+                          cudaStream_t st, uint64_t* nlaunch);
 void launch_esc_finish(int32_t* out, int target_bits, cudaStream_t st, uint64_t* nlaunch);
 void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int32_t* dst, cudaStream_t st,
                           uint64_t* nlaunch);

@@ -1,11 +1,19 @@
 """Row-block partition of one large DGEMM across the GPUs of a node.
 
 One process per GPU (torch.distributed, NCCL over NVLink). Rank r owns the
-rows rows_of(r) of op(A) and C and a full copy of op(B). The only exchange
-on the data path is the ADP decision input: a max-allreduce of
-{exceptional, esc_bits} (two int32) between the guardrail phase and the
-compute phase of adpb200_dgemm_rows, so every rank decides identically and
-uses the same slice count — C is bit-identical to the single-GPU result.
+rows rows_of(r) of op(A) and C. Two layouts of B:
+
+* dgemm_rows: every rank holds all of op(B). The only exchange is the ADP
+  decision input, a max-allreduce of {exceptional, esc_bits} (two int32)
+  between the guardrail and compute phases of adpb200_dgemm_rows.
+* dgemm_dist: rank r holds the column slab cols_of(r) of B. The B exponent
+  statistics are all-gathered (so each rank's ESC covers every column), the
+  decision input is max-allreduced, and each rank's B slice planes (int8,
+  s/8 of the FP64 bytes) are all-gathered before the tcgen05 GEMM — or, on
+  the native fallback, the FP64 B slabs themselves.
+
+Every rank takes the same decision with the same slice count, so the
+assembled C is bit-identical to the single-GPU result.
 """
 from __future__ import annotations
 
@@ -58,3 +66,113 @@ def dgemm_rows(transa: str, transb: str, m_global: int, m: int, n: int, k: int, 
     check(lib().adpb200_dgemm_rows(handle.h, 1, *args))
     reduce_xchg(xchg, group)
     check(lib().adpb200_dgemm_rows(handle.h, 2, *args))
+
+
+# ---- B distributed by column slabs, slice planes all-gathered ---------------------
+def cols_of(rank: int, world: int, n: int) -> Tuple[int, int]:
+    """[start, stop) of rank's B column slab (equal slabs; n/world must be a multiple of 8)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if n % world or (n // world) % 8:
+        raise ValueError("cols_of: n must split into equal slabs of a multiple of 8 columns")
+    nr = n // world
+    return rank * nr, (rank + 1) * nr
+
+
+def dist_sizes(n: int, k: int, world: int, config: Optional[AdpConfig] = None):
+    """(bstats record int32 count, slab header bytes, bytes per slab plane, slab capacity bytes)."""
+    o = (config or AdpConfig()).to_c()
+    out = (C.c_int64 * 4)()
+    check(lib().adpb200_dist_sizes(n, k, world, C.byref(o), out))
+    return tuple(int(x) for x in out)
+
+
+def dist_decision(xchg_host, m_global: int, n: int, k: int, config: Optional[AdpConfig] = None):
+    """decide() on the reduced exchange block: (path, slices, nsl planes to gather, GEMM variant)."""
+    o = (config or AdpConfig()).to_c()
+    x = (C.c_int32 * 2)(int(xchg_host[0]), int(xchg_host[1]))
+    out = (C.c_int32 * 4)()
+    check(lib().adpb200_dist_decision(C.byref(o), x, m_global, n, k, out))
+    return tuple(int(v) for v in out)
+
+
+def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
+                     A: torch.Tensor, lda: int, B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int,
+                     config: Optional[AdpConfig] = None, handle: Optional[Handle] = None,
+                     trace: Optional[torch.Tensor] = None):
+    """The B-distributed ADP DGEMM of one rank as a generator of collective
+    requests, so that the same orchestration runs under torch.distributed
+    (dgemm_dist) and under a single-process multi-rank driver (the tests):
+
+        ("all_gather", out, inp)   out = concatenation over ranks of inp
+        ("all_reduce_max", t)      t = elementwise max over ranks (in place)
+
+    Rank owns rows of op(A) / C (column-major local block, ldc) and the B
+    column slab B_slab (k x n/world column-major, compact: a (n/world, k)
+    row-major torch tensor). Stream-ordered except for one 8-byte host read of
+    the reduced decision input (it sizes the plane all-gather)."""
+    config = config or AdpConfig()
+    dev = C_.device
+    handle = handle or Handle.default(dev.index)
+    o = config.to_c()
+    nrec, hdr, plane_bytes, cap_bytes = dist_sizes(n, k, world, config)
+    bl = torch.empty(nrec, dtype=torch.int32, device=dev)
+    ba = torch.empty(nrec * world, dtype=torch.int32, device=dev)
+    xchg = torch.zeros(2, dtype=torch.int32, device=dev)
+    slab = torch.empty(cap_bytes, dtype=torch.int8, device=dev)
+    st = _stream(dev)
+    tr = None if trace is None else C.c_void_p(trace.data_ptr())
+
+    def phase(p, gathered=None, nsl=0):
+        check(lib().adpb200_dgemm_dist(handle.h, p, m_global, world, transa.encode()[:1], m, n, k, float(alpha),
+                                       _ptr(A), lda, _ptr(B_slab), float(beta), _ptr(C_), ldc, C.byref(o), tr,
+                                       _ptr(bl), _ptr(ba), _ptr(xchg), _ptr(slab), gathered, int(nsl), st))
+
+    phase(1)
+    yield ("all_gather", ba, bl)
+    phase(2)
+    yield ("all_reduce_max", xchg)
+    phase(3)
+    path, s, nsl, _ = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)
+    if nsl > 0:
+        rec = hdr + nsl * plane_bytes
+        gathered = torch.empty(rec * world, dtype=torch.int8, device=dev)
+        yield ("all_gather", gathered, slab[:rec])
+    else:
+        gathered = torch.empty((n, k), dtype=torch.float64, device=dev)  # column-major B, ldb = k
+        yield ("all_gather", gathered.view(-1), B_slab.reshape(-1))
+    phase(4, C.c_void_p(gathered.data_ptr()), nsl)
+    return (path, s, nsl)
+
+
+def dgemm_dist(transa: str, m_global: int, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
+               B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int, config: Optional[AdpConfig] = None,
+               handle: Optional[Handle] = None, group=None, trace: Optional[torch.Tensor] = None):
+    """This rank's share of a row-partitioned ADP DGEMM with B distributed by
+    column slabs: exponent stats and B slice planes all-gathered, the ADP
+    decision input max-allreduced, all over NCCL (torch.distributed)."""
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    gen = dgemm_dist_steps(world, transa, m_global, m, n, k, alpha, A, lda, B_slab, beta, C_, ldc, config, handle,
+                           trace)
+    return drive_collectives(gen, world, group)
+
+
+def drive_collectives(gen, world: int, group=None):
+    """Run a dgemm_dist_steps-style generator, serving its collective requests
+    with torch.distributed (NCCL on GPUs, gloo in the CPU tests). Returns the
+    generator's return value."""
+    try:
+        req = next(gen)
+        while True:
+            if req[0] == "all_gather":
+                if world > 1:
+                    dist.all_gather_into_tensor(req[1], req[2].contiguous(), group=group)
+                else:
+                    req[1].copy_(req[2].reshape(req[1].shape))
+            elif req[0] == "all_reduce_max":
+                reduce_xchg(req[1], group)
+            else:
+                raise ValueError(f"unknown collective request {req[0]!r}")
+            req = next(gen)
+    except StopIteration as fin:
+        return fin.value

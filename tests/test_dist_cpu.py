@@ -62,3 +62,76 @@ def test_rows_of_covers_exactly(world, m):
         assert e0 == s1 and s0 <= e0
     for s, e in spans[:-1]:
         assert s % 128 == 0 and e % 128 == 0
+
+
+# ---- B-distributed path: host logic ---------------------------------------------------
+def test_cols_of_and_contract():
+    from paper_2511_13778_b200.dist import cols_of
+
+    assert [cols_of(r, 4, 512) for r in range(4)] == [(0, 128), (128, 256), (256, 384), (384, 512)]
+    with pytest.raises(ValueError):
+        cols_of(0, 3, 512)      # unequal slabs
+    with pytest.raises(ValueError):
+        cols_of(0, 8, 8 * 12)   # slab not a multiple of 8
+
+
+def test_dist_sizes():
+    from paper_2511_13778_b200 import AdpConfig
+    from paper_2511_13778_b200.dist import dist_sizes
+
+    nrec, hdr, plane, cap = dist_sizes(8192, 8192, 8)
+    nr, t = 1024, 32
+    assert nrec == 2 * t * nr + nr and hdr == 4096 and plane == 8192 * nr
+    assert cap == hdr + 18 * plane  # auto mode: max_slices planes
+    assert dist_sizes(8192, 100, 8, AdpConfig(mode=1, forced_slices=7))[3] == 1024 * 4 + 7 * 128 * 1024
+    with pytest.raises(ValueError):
+        dist_sizes(100, 100, 8)
+
+
+def test_dist_decision_matches_decide():
+    from paper_2511_13778_b200 import AdpConfig, PAIRS_TARGET, decide
+    from paper_2511_13778_b200.dist import dist_decision
+
+    for cfg in (AdpConfig(), AdpConfig(pair_limit=PAIRS_TARGET), AdpConfig(mode=1, forced_slices=9)):
+        for exc, esc in [(0, 1), (0, 8), (0, 11), (0, 48), (1, 3), (2, 0), (3, 5)]:
+            path, s, nsl, var = dist_decision([exc, esc], 8192, 8192, 8192, cfg)
+            d = decide(bool(exc & 1), bool(exc & 2), 8192, 8192, 8192, esc, cfg)
+            assert (path == 0) == (d[0] == "emulated")
+            assert s == (d[2] if d[0] == "emulated" else 0)
+            assert (nsl > 0) == (path == 0) and nsl <= max(s, 0)
+    # the fast policy gathers s planes, the variant follows the diagonal count
+    assert dist_decision([0, 1], 8192, 8192, 8192, AdpConfig(pair_limit=PAIRS_TARGET)) == (0, 7, 7, 64)
+    assert dist_decision([0, 8], 8192, 8192, 8192, AdpConfig(pair_limit=PAIRS_TARGET)) == (0, 8, 8, 48)
+
+
+def _collective_worker(rank, world, port, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2511_13778_b200.dist import drive_collectives
+
+    def fake_rank_steps():
+        # the request sequence of dgemm_dist_steps on one rank, CPU tensors
+        bl = torch.arange(6, dtype=torch.int32) + 10 * rank
+        ba = torch.empty(6 * world, dtype=torch.int32)
+        yield ("all_gather", ba, bl)
+        x = torch.tensor([rank & 1, 3 + 4 * rank], dtype=torch.int32)
+        yield ("all_reduce_max", x)
+        slab = torch.full((16,), rank + 1, dtype=torch.int8)
+        g = torch.empty(8 * world, dtype=torch.int8)
+        yield ("all_gather", g, slab[:8])
+        return ba.tolist(), x.tolist(), g.tolist()
+
+    results[rank] = drive_collectives(fake_rank_steps(), world)
+    dist.destroy_process_group()
+
+
+def test_drive_collectives_gloo():
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_collective_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    for r in range(world):
+        ba, x, g = results[r]
+        assert ba == list(range(6)) + [10 + i for i in range(6)]
+        assert x == [1, 7]
+        assert g == [1] * 8 + [2] * 8

@@ -1,0 +1,111 @@
+"""GPU (one device, several virtual ranks): the B-distributed multi-GPU path.
+
+Each virtual rank has its own handle (workspace) and runs the real
+orchestration (dist.dgemm_dist_steps); the collectives it requests are served
+by hand across the ranks (concatenation / elementwise max), exactly what
+NCCL all-gather / all-reduce(MAX) produce. The assembled C must be
+bit-identical to the single-GPU adpb200_dgemm.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import assert_bitwise
+
+pytestmark = pytest.mark.gpu
+
+
+def run_virtual(gens):
+    reqs = [next(g) for g in gens]
+    results = [None] * len(gens)
+    while True:
+        kind = reqs[0][0]
+        assert all(r[0] == kind for r in reqs), "ranks diverged"
+        if kind == "all_gather":
+            cat = torch.cat([r[2].reshape(-1) for r in reqs])
+            for r in reqs:
+                r[1].view(-1).copy_(cat)
+        else:
+            mx = torch.stack([r[1] for r in reqs]).amax(0)
+            for r in reqs:
+                r[1].copy_(mx)
+        nxt = []
+        for i, g in enumerate(gens):
+            try:
+                nxt.append(next(g))
+            except StopIteration as fin:
+                results[i] = fin.value
+        if all(x is not None for x in results):
+            return results
+        assert len(nxt) == len(gens), "ranks finished at different steps"
+        reqs = nxt
+
+
+def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3):
+    from paper_2511_13778_b200 import Handle
+    from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    # column-major storage: A (m x k) -> tensor (k, m); op(A) = A^T for 'T': A stored k x m -> tensor (m, k)
+    Ast = torch.rand((k, m) if transa == "N" else (m, k), generator=g, device="cuda", dtype=torch.float64)
+    Ast = Ast * (1.0 - lo) + lo
+    Bt = torch.rand((n, k), generator=g, device="cuda", dtype=torch.float64) * (1.0 - lo) + lo  # B k x n col-major
+    Ct = torch.rand((n, m), generator=g, device="cuda", dtype=torch.float64)
+    if poison is not None:
+        Bt[poison] = float("nan")
+    ref = Ct.clone()
+    lda = m if transa == "N" else k
+    gpu.dgemm(transa, "N", m, n, k, alpha, Ast, lda, Bt, k, beta, ref, m, cfg)
+    gens, blocks = [], []
+    for r in range(world):
+        r0, r1 = rows_of(r, world, m)
+        c0, c1 = cols_of(r, world, n)
+        mr = r1 - r0
+        Ab = (Ast[:, r0:r1] if transa == "N" else Ast[r0:r1, :]).contiguous()
+        lda_r = max(mr, 1) if transa == "N" else k
+        Bs = Bt[c0:c1].contiguous()
+        Cb = Ct[:, r0:r1].contiguous()
+        blocks.append(Cb)
+        gens.append(dgemm_dist_steps(world, transa, m, mr, n, k, alpha, Ab, lda_r, Bs, beta, Cb, max(mr, 1), cfg,
+                                     Handle(0)))
+    res = run_virtual(gens)
+    torch.cuda.synchronize()
+    assembled = torch.cat(blocks, dim=1)
+    return assembled, ref, res
+
+
+@pytest.mark.parametrize("world,m,n,k,policy", [(2, 640, 384, 512, "full"), (4, 1000, 512, 768, "target"),
+                                                (2, 300, 256, 2048, "target"), (8, 1024, 1024, 1024, "full")])
+def test_dist_bit_identical(gpu, world, m, n, k, policy):
+    cfg = gpu.AdpConfig(pair_limit=gpu.PAIRS_TARGET if policy == "target" else gpu.PAIRS_FULL)
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, alpha=-1.25, beta=0.5)
+    path, s, nsl = res[0]
+    assert all(r == res[0] for r in res)
+    assert path == 0 and s >= 7 and nsl == s
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+
+
+def test_dist_transposed_a_and_wide_span(gpu):
+    cfg = gpu.AdpConfig()
+    got, ref, res = dist_case(gpu, 4, 768, 512, 640, cfg, transa="T", lo=1.0)
+    assert res[0][0] == 0
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+
+
+def test_dist_nan_in_one_slab_falls_back_everywhere(gpu):
+    """A NaN in rank 1's B slab: the max-allreduced exceptional flag sends
+    every rank to the native path, which all-gathers the FP64 B slabs."""
+    cfg = gpu.AdpConfig()
+    n = 512
+    got, ref, res = dist_case(gpu, 4, 700, n, 600, cfg, poison=(n // 4 + 3, 17))
+    assert all(r[0] == 1 and r[2] == 0 for r in res)
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
+
+
+def test_dist_forced_and_native_modes(gpu):
+    for cfg in (gpu.AdpConfig(mode=gpu.AdpMode.ForceEmulate, forced_slices=9, pair_limit=gpu.PAIRS_TARGET),
+                gpu.AdpConfig(mode=gpu.AdpMode.ForceNative)):
+        got, ref, res = dist_case(gpu, 2, 512, 256, 512, cfg)
+        assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+
