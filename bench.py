@@ -41,7 +41,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--n", type=int, default=NOMINAL, help="m_per_gpu = n = k")
+    p.add_argument("--size", type=int, default=NOMINAL, help="m_per_gpu = n = k")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
@@ -132,7 +132,7 @@ def reference_arm(args):
     kind = "reference" if available("reference") else "port"
     orc = Oracle(kind)
     cores = os.cpu_count() or 1
-    rs, cs, k = 256, 2048, args.n  # a 256 x 2048 block of C, full k: same decision path (min dim 256)
+    rs, cs, k = 256, 2048, args.size  # a 256 x 2048 block of C, full k: same decision path (min dim 256)
     rng = np.random.default_rng(1)
     a = rng.uniform(1.0, 2.0, (rs, k))
     b = rng.uniform(1.0, 2.0, (k, cs))
@@ -154,7 +154,7 @@ def reference_arm(args):
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic U(1,2)",
         "config": {"workload": f"reference adp_gemm (CPU, OpenMP) on a {rs}x{cs}x{k} block of the "
-                               f"{args.n}^3 ADP DGEMM", "sample_m": rs, "sample_n": cs, "k": k},
+                               f"{args.size}^3 ADP DGEMM", "sample_m": rs, "sample_n": cs, "k": k},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
                          "sample": f"{rs}x{cs}x{k} block of C per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -194,19 +194,24 @@ def main():
 
     import paper_2511_13778_b200 as adp
     from paper_2511_13778_b200 import _lib
-    from paper_2511_13778_b200.dist import dgemm_rows
+    from paper_2511_13778_b200.dist import cols_of, dgemm_dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    shared = os.environ.get("ADPB200_BENCH_SHARED_GPU") == "1"  # plumbing check only: all ranks on cuda:0, gloo
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
-    n = k = args.n
-    m = args.n                      # rows per GPU (weak scaling)
+    n = k = args.size
+    m = args.size                      # rows per GPU (weak scaling)
     m_global = m * world
     handle = adp.Handle.default(dev.index)
 
@@ -217,13 +222,17 @@ def main():
 
     At = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, 1.0, 2.0, dev.index)   # A: m x k col-major
     Bt = grading.gen_uniform_rect(n, k, 2, 1.0, 2.0, dev.index)                # B: k x n col-major
+    if world > 1:
+        # B distributed by column slabs: this rank keeps columns cols_of(rank) only
+        c0, c1 = cols_of(rank, world, n)
+        Bt = Bt[c0:c1].contiguous()
     Ct = torch.zeros((n, m), device=dev, dtype=torch.float64)                  # C: m x n col-major
     cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET)
     trace_buf = torch.zeros(_lib.TRACE_BYTES, dtype=torch.uint8, device=dev)
 
     def step(config=cfg, A=At, B=Bt, Cm=Ct, trace=None):
         if world > 1:
-            dgemm_rows("N", "N", m_global, m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
+            dgemm_dist("N", m_global, m, n, k, 1.0, A, m, B, 0.0, Cm, m, config, handle, trace=trace)
         else:
             adp.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
 
@@ -261,7 +270,7 @@ def main():
     time.sleep(1.0)
     barrier()
     launches0 = handle.launches()
-    handle.profile_enable(args.steps)
+    handle.profile_enable(args.steps * (4 if world > 1 else 1))  # the dist path is 4 pipeline calls
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
     e0.record()
@@ -339,8 +348,9 @@ def main():
                         "d2h_bytes_per_step": int(Ct.numel() * 8), "ms_per_step": e2e_ms}
         # ---- native FP64 (cuBLAS DGEMM through torch) on the same shapes -------------
         X = At.t()
-        Y = Bt.t()
+        Y = (Bt if world == 1 else grading.gen_uniform_rect(n, k, 2, 1.0, 2.0, dev.index)).t()  # full k x n
         nat_ms = timed(lambda: torch.mm(X, Y), max(3, args.steps // 2), 2)
+        del Y
         extra["native_fp64"] = {"value": 2.0 * m * n * k / (nat_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                                 "impl": "cublasDgemm via torch.mm", "ms_per_step": nat_ms}
         # ---- ADP overhead: guardrails + pinned s=7 vs plain fixed 7-slice emulation ------
@@ -359,6 +369,8 @@ def main():
         # ---- U[-1,1] operands: coarsened ESC picks s = 8 --------------------------------
         Au = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, -1.0, 1.0, dev.index)
         Bu = grading.gen_uniform_rect(n, k, 2, -1.0, 1.0, dev.index)
+        if world > 1:
+            Bu = Bu[c0:c1].contiguous()
         tr2 = torch.zeros_like(trace_buf)
         step(cfg, Au, Bu, Ct, tr2)
         torch.cuda.synchronize()
@@ -375,8 +387,13 @@ def main():
         # the device double-double oracle (Dot2), and the grading ratio
         # |C - AB| / (2^-52 (|A||B|)_ij); cuBLAS DGEMM on the same operands ----------
         step()
+        # (N > 1: this rank's row block against its local B slab, i.e. the C columns of the slab)
+        if world > 1:
+            Ct_acc = Ct[c0:c1].contiguous()
+        else:
+            Ct_acc = Ct
         ref, absab = grading.dd_gemm(Bt, At)          # C^T = B^T A^T in row-major terms
-        rep = grading.error_report(Ct, ref, absab=absab)
+        rep = grading.error_report(Ct_acc, ref, absab=absab)
         nat = torch.mm(At.t(), Bt.t()).t().contiguous()
         rep_n = grading.error_report(nat, ref, absab=absab)
         del ref, absab, nat
@@ -427,8 +444,10 @@ def main():
                                    "guardrails live, ESC-chosen s, pairs d_a+d_b<=s",
                        "m": m_global, "n": n, "k": k, "slices": trace.slices, "esc_bits": trace.esc_bits,
                        "path": trace.path, "pairs": pairs, "gemm_variant": trace.gemm_variant,
-                       "parallelism": f"row-block x{world}, B replicated, ADP decision max-allreduced (NCCL)",
-                       "l2": "inputs larger than L2 (512 MiB per operand)"},
+                       "parallelism": (f"row-block x{world}: A/C rows per rank, B column slabs; B exponent "
+                                       "stats + slice planes all-gathered, ADP decision max-allreduced (NCCL)")
+                       if world > 1 else "single GPU",
+                       "l2": f"inputs larger than L2 ({m * k * 8 >> 20} MiB per operand, L2 126 MB)"},
             "gpu_launches": launches,
             "stage_ms": stage_ms,
             "roofline": roofline,

@@ -165,7 +165,9 @@ def drive_collectives(gen, world: int, group=None):
         req = next(gen)
         while True:
             if req[0] == "all_gather":
-                if world > 1:
+                if world > 1 and dist.get_backend(group) == "gloo":
+                    dist.all_gather(list(req[1].view(-1).chunk(world)), req[2].contiguous().view(-1), group=group)
+                elif world > 1:
                     dist.all_gather_into_tensor(req[1], req[2].contiguous(), group=group)
                 else:
                     req[1].copy_(req[2].reshape(req[1].shape))
