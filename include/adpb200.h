@@ -254,6 +254,26 @@ int adpb200_gen_uniform_rect(adpb200_handle handle, int64_t rows, int64_t cols, 
 int adpb200_gen_test2(adpb200_handle handle, int64_t n, int b, uint64_t seed, double* lhs,
                       double* rhs, double* x, int32_t* j, void* stream);
 
+/* ---- the reference's application caller: blocked Householder QR ----------------
+ * geqrf_blocked (qr.cpp:98-143): A (row-major m x n device, m >= n >= 1) is
+ * overwritten by the factors (R in the upper triangle, unit-diagonal reflector
+ * tails below); t_blocks (device, ceil(n/panel) slots of panel*panel doubles)
+ * receives each panel's upper-triangular T, packed pw x pw at the slot start;
+ * traces (device, 3 per panel) the dispatch of every trailing-update GEMM
+ * (W = Y^T A_s, W = T^T W, A_s -= Y W, all through adpb200_adp_gemm with opt).
+ * Panel factorisation in the reference's operation order on the device:
+ * factors, T and traces are bitwise the reference's. panel <= 1024. */
+int adpb200_geqrf_blocked(adpb200_handle handle, int64_t m, int64_t n, int64_t panel, double* A,
+                          double* t_blocks, adpb200_trace* traces, const adpb200_options* opt,
+                          void* stream);
+/* materialize_q (qr.cpp:145-173): thin Q (m x n, row-major device). */
+int adpb200_qr_materialize_q(adpb200_handle handle, int64_t m, int64_t n, int64_t panel,
+                             const double* factors, const double* t_blocks, double* Q, void* stream);
+/* qr_residual (qr.cpp:183-197): out (device double[2]) = |A0 - QR|_F / |A0|_F,
+ * |I - Q^T Q|_F, with the reference-order native GEMM and sequential norms. */
+int adpb200_qr_residual(adpb200_handle handle, int64_t m, int64_t n, int64_t panel, const double* A0,
+                        const double* factors, const double* t_blocks, double* out, void* stream);
+
 /* Kernel launches issued by this handle since creation (all kernels are ours). */
 uint64_t adpb200_launch_count(adpb200_handle handle);
 

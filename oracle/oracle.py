@@ -371,6 +371,31 @@ class Oracle:
         return dict(max_err=out[0], avg_err=out[1], esc_bits=None if out[2] < 0 else int(out[2]),
                     slices=int(out[3]), fallback=bool(out[4]))
 
+    def qr(self, a, panel, cfg: "Config | None" = None, want_q=True):
+        """geqrf_blocked + materialize_q + qr_residual (qr.cpp) of the reference:
+        (factors, t_packed, traces [3*panels x 7], q or None, (residual, orthogonality))."""
+        self._need_ref("qr")
+        cfg = cfg or Config()
+        a = _f64(a)
+        m, n = a.shape
+        panels = (n + panel - 1) // panel
+        fac = np.empty((m, n), np.float64)
+        t = np.zeros(max(1, panels * panel * panel), np.float64)
+        tr = np.zeros((max(1, 3 * panels), 7), np.int64)
+        q = np.empty((m, n), np.float64) if want_q else None
+        acc = (C.c_double * 2)()
+        cd = (C.c_double * 1)(cfg.cost_ratio)
+        self._check(self.lib.ozref_qr(_p(a), C.c_longlong(m), C.c_longlong(n), C.c_longlong(panel), cfg.ints(), cd,
+                                      _p(fac), _p(t), _p(tr, C.c_longlong), None if q is None else _p(q), acc), "qr")
+        return fac, t, tr[: 3 * panels], q, (acc[0], acc[1])
+
+    def time_qr(self, a, panel, min_dim=256) -> float:
+        self._need_ref("time_qr")
+        a = _f64(a)
+        self.lib.ozref_time_qr.restype = C.c_double
+        return float(self.lib.ozref_time_qr(_p(a), C.c_longlong(a.shape[0]), C.c_longlong(a.shape[1]),
+                                            C.c_longlong(panel), C.c_longlong(min_dim)))
+
 
 def fold_round(acc_row: np.ndarray, exp2: int) -> float:
     """Exact fold of one element's diagonal accumulators + RNE (port only)."""

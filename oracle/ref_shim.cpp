@@ -24,6 +24,7 @@
 #include "ozadp/grading.hpp"
 #include "ozadp/igemm.hpp"
 #include "ozadp/oracle.hpp"
+#include "ozadp/qr.hpp"
 #include "ozadp/slicing.hpp"
 #include "ozadp/threads.hpp"
 
@@ -349,6 +350,65 @@ int ozref_test2_row(long long n, int b, const char* mode, unsigned long long see
         out[3] = r.slices;
         out[4] = r.fallback ? 1.0 : 0.0;
     });
+}
+
+// geqrf_blocked (qr.cpp:98-143) + materialize_q + qr_residual in one call.
+// cfg_i / cfg_d as ozref_adp_gemm. t_out: panels slots of panel*panel
+// doubles, T of panel p packed pw x pw at slot start. traces_i: 3 per panel x
+// {path, reason, esc_bits(-1), slices(-1), m, n, k}. q_out (m x n) and acc[2]
+// (residual, orthogonality) optional.
+int ozref_qr(const double* a, long long m, long long n, long long panel, const long long* cfg_i,
+             const double* cfg_d, double* factors, double* t_out, long long* traces_i, double* q_out,
+             double* acc) {
+    return guarded([&] {
+        AdpConfig cfg;
+        cfg.target_bits = int(cfg_i[0]);
+        cfg.esc_block_len = std::size_t(cfg_i[1]);
+        cfg.max_slices = int(cfg_i[2]);
+        cfg.min_dim = std::size_t(cfg_i[3]);
+        cfg.mode = cfg_i[4] == 1 ? AdpMode::ForceEmulate
+                                 : (cfg_i[4] == 2 ? AdpMode::ForceNative : AdpMode::Auto);
+        cfg.forced_slices = int(cfg_i[5]);
+        cfg.chunk_len = std::size_t(cfg_i[6]);
+        cfg.cost_ratio = cfg_d[0];
+        const MatrixF64 am = wrap(a, m, n);
+        QrResult qr = geqrf_blocked(am, std::size_t(panel), cfg);
+        unwrap(qr.factors, factors);
+        for (std::size_t p = 0; p < qr.t_blocks.size(); ++p)
+            unwrap(qr.t_blocks[p], t_out + p * std::size_t(panel) * std::size_t(panel));
+        for (std::size_t i = 0; i < qr.traces.size(); ++i) {
+            const AdpTrace& tr = qr.traces[i];
+            long long* o = traces_i + 7 * i;
+            o[0] = tr.decision.path == AdpPath::Emulated ? 0 : 1;
+            o[1] = int(tr.decision.reason);
+            o[2] = tr.decision.esc ? tr.decision.esc->esc_bits : -1;
+            o[3] = tr.decision.path == AdpPath::Emulated ? tr.decision.slices : -1;
+            o[4] = (long long)tr.m;
+            o[5] = (long long)tr.n;
+            o[6] = (long long)tr.k;
+        }
+        if (q_out) unwrap(materialize_q(qr), q_out);
+        if (acc) {
+            QrAccuracy r = qr_residual(am, qr);
+            acc[0] = r.residual;
+            acc[1] = r.orthogonality;
+        }
+    });
+}
+
+// Wall-clock seconds of one geqrf_blocked call (bench / CPU baseline).
+double ozref_time_qr(const double* a, long long m, long long n, long long panel, long long min_dim) {
+    const MatrixF64 am = wrap(a, m, n);
+    AdpConfig cfg;
+    cfg.min_dim = std::size_t(min_dim);
+    auto t0 = std::chrono::steady_clock::now();
+    try {
+        QrResult qr = geqrf_blocked(am, std::size_t(panel), cfg);
+        (void)qr;
+    } catch (...) {
+        return -1.0;
+    }
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
 }  // extern "C"

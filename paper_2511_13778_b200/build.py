@@ -20,7 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(ROOT, "build", "adpb200")
 LIB = os.path.join(PKG, "libadpb200.so")
-SOURCES = ["guard.cu", "slice.cu", "igemm.cu", "native.cu", "grade.cu", "api.cu"]
+SOURCES = ["guard.cu", "slice.cu", "igemm.cu", "native.cu", "grade.cu", "qr.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc" if os.path.exists("/usr/local/cuda/bin/nvcc") else "nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -1006,6 +1006,53 @@ int adpb200_gen_test2(adpb200_handle h, int64_t n, int b, uint64_t seed, double*
     return cuda_check(cudaGetLastError(), "gen_test2 launch");
 }
 
+static int qr_check(adpb200_handle h, int64_t m, int64_t n, int64_t panel) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "geqrf_blocked: null handle");
+    if (n < 1) return fail(3, "geqrf_blocked: empty matrix");                 // qr.cpp:100
+    if (m < n) return fail(3, "geqrf_blocked: need m >= n");                  // qr.cpp:101
+    if (panel < 1) return fail(3, "geqrf_blocked: panel width must be positive");  // qr.cpp:102
+    if (panel > 1024) return fail(3, "geqrf_blocked: panel width above 1024 (one-CTA panel kernel)");
+    return ADPB200_OK;
+}
+
+int adpb200_geqrf_blocked(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* A, double* t_blocks,
+                          adpb200_trace* traces, const adpb200_options* opt, void* stream) {
+    int rc = qr_check(h, m, n, panel);
+    if (rc) return rc;
+    adpb200_options o;
+    if (opt) o = *opt;
+    else adpb200_default_options(&o);
+    rc = adpb200_validate_options(&o);  // gemm_config.validate() (qr.cpp:103)
+    if (rc) return rc;
+    if (!A || !t_blocks || !traces) return fail(3, "geqrf_blocked: null buffer");
+    cudaSetDevice(h->device);
+    rc = qr_geqrf(h, m, n, panel, A, t_blocks, traces, &o, static_cast<cudaStream_t>(stream), &h->launches);
+    if (rc == 2) return cuda_check(cudaGetLastError(), "geqrf_blocked");
+    return rc;
+}
+
+int adpb200_qr_materialize_q(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* factors,
+                             const double* t_blocks, double* Q, void* stream) {
+    int rc = qr_check(h, m, n, panel);
+    if (rc) return rc;
+    if (!factors || !t_blocks || !Q) return fail(3, "materialize_q: null buffer");
+    cudaSetDevice(h->device);
+    rc = qr_materialize_q(h, m, n, panel, factors, t_blocks, Q, static_cast<cudaStream_t>(stream), &h->launches);
+    if (rc == 2) return cuda_check(cudaGetLastError(), "materialize_q");
+    return rc;
+}
+
+int adpb200_qr_residual(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* A0,
+                        const double* factors, const double* t_blocks, double* out, void* stream) {
+    int rc = qr_check(h, m, n, panel);
+    if (rc) return rc;
+    if (!A0 || !factors || !t_blocks || !out) return fail(3, "qr_residual: null buffer");
+    cudaSetDevice(h->device);
+    rc = qr_residual(h, m, n, panel, A0, factors, t_blocks, out, static_cast<cudaStream_t>(stream), &h->launches);
+    if (rc == 2) return cuda_check(cudaGetLastError(), "qr_residual");
+    return rc;
+}
+
 int adpb200_scan(adpb200_handle h, const double* A, int64_t count, uint64_t* counts, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "scan: null handle");
     cudaStream_t st = static_cast<cudaStream_t>(stream);

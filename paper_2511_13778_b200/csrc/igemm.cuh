@@ -59,5 +59,12 @@ int gen_uniform_device(int64_t rows, int64_t cols, uint64_t seed, double lo, dou
                        uint64_t* nlaunch);
 int gen_test2_device(int64_t n, int b, uint64_t seed, double* lhs, double* rhs, double* x_out, int32_t* j_out,
                      cudaStream_t st, uint64_t* nlaunch);
+// QR caller (qr.cu): blocked Householder QR with ADP trailing updates, Q and residuals.
+int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, double* t_blocks, adpb200_trace* traces,
+             const adpb200_options* opt, cudaStream_t st, uint64_t* nl);
+int qr_materialize_q(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* fac, const double* t_blocks,
+                     double* q, cudaStream_t st, uint64_t* nl);
+int qr_residual(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* a0, const double* fac,
+                const double* t_blocks, double* out, cudaStream_t st, uint64_t* nl);
 
 }  // namespace adpb200

@@ -1,0 +1,352 @@
+// The reference's application caller: blocked Householder QR whose trailing
+// updates run through the ADP GEMM (proj/src/qr.cpp:98-143, compact WY form,
+// three adp_gemm per panel at :130-132).
+//
+// Device-resident and stream-ordered end to end. The level-2 panel work
+// (make_reflector :26-47, apply_reflector :51-60, build_y :64-71, build_t
+// :75-94) runs in ONE CTA per panel in the reference's exact operation order:
+// every sum that the reference accumulates sequentially is accumulated
+// sequentially by one thread (FP64 adds are not associative), with explicitly
+// rounded intrinsics (the reference is built with -ffp-contract=off); only
+// operations that are independent per element (the tail division, the
+// per-column reflector applications, the z / T entries of one step) run in
+// parallel. The three trailing-update products go through adpb200_adp_gemm
+// (bitwise the reference's adp_gemm), so the factors, T blocks and traces are
+// bitwise the reference's. materialize_q / qr_residual (:145-197) use the
+// reference-order native GEMM and a sequential Frobenius sum.
+#include <algorithm>
+#include <vector>
+
+#include "igemm.cuh"
+
+namespace adpb200 {
+namespace {
+
+constexpr int kPanelThreads = 1024;  // panel width limit of the one-CTA panel kernel
+
+// Panel factorisation of f[p0:m, p0:p0+pw] (row-major f, leading dimension ld).
+// P: column-major scratch (rows x pw). Outputs: the panel written back to f,
+// y (rows x pw) and yT (pw x rows) row-major, t and tT (pw x pw) row-major.
+__global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict__ f, int64_t ld, int64_t m, int64_t p0,
+                                                              int pw, double* __restrict__ P, double* __restrict__ y,
+                                                              double* __restrict__ yT, double* __restrict__ t,
+                                                              double* __restrict__ tT) {
+    const int64_t rows = m - p0;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    __shared__ double tau_s[kPanelThreads];
+    __shared__ double z_s[kPanelThreads];
+    __shared__ double v0_s, beta_s, x0_s;
+    __shared__ int mode_s;
+    for (int64_t e = tid; e < rows * pw; e += nth) {
+        const int64_t r = e / pw, j = e - r * pw;
+        P[j * rows + r] = f[(p0 + r) * ld + p0 + j];
+    }
+    __syncthreads();
+    for (int j = 0; j < pw; ++j) {
+        double* col = P + int64_t(j) * rows;
+        // ---- make_reflector (qr.cpp:26-47): sequential sums on one thread
+        if (tid == 0) {
+            const double x0 = col[j];
+            double tail = 0.0;
+            for (int64_t r = j + 1; r < rows; ++r) tail = __dadd_rn(tail, __dmul_rn(col[r], col[r]));
+            if (tail == 0.0) {
+                mode_s = 0;
+                if (x0 >= 0.0) {
+                    tau_s[j] = 0.0;
+                } else {
+                    col[j] = -x0;
+                    tau_s[j] = 2.0;
+                }
+            } else {
+                // column_norm (qr.cpp:14-22)
+                double amax = 0.0;
+                for (int64_t r = j; r < rows; ++r) {
+                    const double a = fabs(col[r]);
+                    amax = amax < a ? a : amax;  // std::max
+                }
+                double beta = 0.0;
+                if (amax != 0.0) {
+                    double ss = 0.0;
+                    for (int64_t r = j; r < rows; ++r) {
+                        const double q = __ddiv_rn(col[r], amax);
+                        ss = __dadd_rn(ss, __dmul_rn(q, q));
+                    }
+                    beta = __dmul_rn(amax, __dsqrt_rn(ss));
+                }
+                v0_s = x0 > 0.0 ? __ddiv_rn(-tail, __dadd_rn(x0, beta)) : __dsub_rn(x0, beta);
+                beta_s = beta;
+                x0_s = x0;
+                mode_s = 1;
+            }
+        }
+        __syncthreads();
+        if (mode_s == 1) {
+            const double v0 = v0_s;
+            for (int64_t r = j + 1 + tid; r < rows; r += nth) col[r] = __ddiv_rn(col[r], v0);
+            __syncthreads();
+            if (tid == 0) {
+                col[j] = beta_s;
+                tau_s[j] = __ddiv_rn(__dsub_rn(beta_s, x0_s), beta_s);
+            }
+        }
+        __syncthreads();
+        // ---- apply_reflector (qr.cpp:51-60) to the panel's later columns, one thread each
+        const double tau = tau_s[j];
+        if (tau != 0.0) {
+            for (int cc = j + 1 + tid; cc < pw; cc += nth) {
+                double* dst = P + int64_t(cc) * rows;
+                double dot = dst[j];
+                for (int64_t r = j + 1; r < rows; ++r) dot = __dadd_rn(dot, __dmul_rn(col[r], dst[r]));
+                const double w = __dmul_rn(tau, dot);
+                dst[j] = __dsub_rn(dst[j], w);
+                for (int64_t r = j + 1; r < rows; ++r) dst[r] = __dsub_rn(dst[r], __dmul_rn(w, col[r]));
+            }
+        }
+        __syncthreads();
+    }
+    // write the panel back; build_y (qr.cpp:64-71)
+    for (int64_t e = tid; e < rows * pw; e += nth) {
+        const int64_t r = e / pw, j = e - r * pw;
+        const double v = P[j * rows + r];
+        f[(p0 + r) * ld + p0 + j] = v;
+        const double yv = r == j ? 1.0 : (r > j ? v : 0.0);
+        y[r * pw + j] = yv;
+        yT[j * rows + r] = yv;
+    }
+    // build_t (qr.cpp:75-94), T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) (Y^T y_j)
+    for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) t[e] = 0.0;
+    __syncthreads();
+    for (int j = 0; j < pw; ++j) {
+        if (tid == 0) t[j * pw + j] = tau_s[j];
+        if (j > 0) {
+            // z_i = sum_{r >= j} y(r, i) y(r, j), i < j (y read from the column-major scratch)
+            for (int i = tid; i < j; i += nth) {
+                const double* ci = P + int64_t(i) * rows;
+                const double* cj = P + int64_t(j) * rows;
+                double dot = 0.0;
+                for (int64_t r = j; r < rows; ++r) {
+                    const double yi = ci[r];                  // r >= j > i: tail of column i
+                    const double yj = r == j ? 1.0 : cj[r];  // unit diagonal of column j
+                    dot = __dadd_rn(dot, __dmul_rn(yi, yj));
+                }
+                z_s[i] = dot;
+            }
+            __syncthreads();
+            for (int i = tid; i < j; i += nth) {
+                double dot = 0.0;
+                for (int l = i; l < j; ++l) dot = __dadd_rn(dot, __dmul_rn(t[i * pw + l], z_s[l]));
+                t[i * pw + j] = __dmul_rn(-tau_s[j], dot);
+            }
+        }
+        __syncthreads();
+    }
+    for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) {
+        const int64_t i = e / pw, j = e - i * pw;
+        tT[j * pw + i] = t[e];
+    }
+}
+
+// dst (rows x cols, leading dimension ldd) = src (leading dimension lds)
+__global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
+                                  int64_t rows, int64_t cols) {
+    const int64_t total = rows * cols;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols, c = e - r * cols;
+        dst[r * ldd + c] = src[r * lds + c];
+    }
+}
+
+// dst (cols x rows) = transpose of src (rows x cols), both row-major compact
+__global__ void transpose_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t rows, int64_t cols) {
+    const int64_t total = rows * cols;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols, c = e - r * cols;
+        dst[c * rows + r] = src[e];
+    }
+}
+
+// build_y from the factors (materialize_q): y (rows x pw) unit lower trapezoid
+__global__ void build_y_kernel(const double* __restrict__ fac, int64_t ld, int64_t m, int64_t p0, int pw,
+                               double* __restrict__ y, double* __restrict__ yT) {
+    const int64_t rows = m - p0;
+    const int64_t total = rows * pw;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / pw, j = e - r * pw;
+        const double v = r == j ? 1.0 : (r > j ? fac[(p0 + r) * ld + p0 + j] : 0.0);
+        y[e] = v;
+        yT[j * rows + r] = v;
+    }
+}
+
+__global__ void eye_kernel(double* __restrict__ q, int64_t m, int64_t n) {
+    const int64_t total = m * n;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        q[e] = i == j ? 1.0 : 0.0;
+    }
+}
+
+// upper_r (qr.cpp:175-181)
+__global__ void upper_r_kernel(const double* __restrict__ fac, int64_t ld, int64_t n, double* __restrict__ r) {
+    const int64_t total = n * n;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        r[e] = j >= i ? fac[i * ld + j] : 0.0;
+    }
+}
+
+// diff = a - b (elementwise); with b == nullptr, gram(i,i) -= 1 on a square matrix in place
+__global__ void sub_kernel(double* __restrict__ a, const double* __restrict__ b, int64_t total, int64_t n_diag) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        if (b) a[e] = __dsub_rn(a[e], b[e]);
+        else if (e / n_diag == e % n_diag) a[e] = __dsub_rn(a[e], 1.0);
+    }
+}
+
+// frobenius_norm (matrix.hpp:65-69): ONE sequential sum, like the reference.
+// out[0] = ||d|| / ||a|| (||d|| when ||a|| == 0), out[1] = ||g||
+__global__ void qr_norms_kernel(const double* __restrict__ d, const double* __restrict__ a, const double* __restrict__ g,
+                                int64_t nda, int64_t ng, double* __restrict__ out) {
+    auto frob = [](const double* x, int64_t cnt) {
+        double s = 0.0;
+        for (int64_t i = 0; i < cnt; ++i) s = __dadd_rn(s, __dmul_rn(x[i], x[i]));
+        return __dsqrt_rn(s);
+    };
+    if (threadIdx.x == 0) {
+        const double dn = frob(d, nda), an = frob(a, nda);
+        out[0] = an == 0.0 ? dn : __ddiv_rn(dn, an);
+    } else if (threadIdx.x == 32) {
+        out[1] = frob(g, ng);
+    }
+}
+
+unsigned grid_for(int64_t total) {
+    int64_t b = (total + 255) / 256;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(b, int64_t(num_sms()) * 16));
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t st;
+    explicit DevBuf(cudaStream_t s) : st(s) {}
+    double* alloc(size_t count) {
+        if (cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(double), st) != cudaSuccess) p = nullptr;
+        return static_cast<double*>(p);
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+}  // namespace
+
+// ---- host orchestration (called from api.cu's C ABI) ------------------------------
+int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, double* t_blocks, adpb200_trace* traces,
+             const adpb200_options* opt, cudaStream_t st, uint64_t* nl) {
+    const int64_t pwmax = std::min(panel, n);
+    DevBuf bP(st), by(st), byT(st), bt(st), btT(st), bas(st), bw1(st), bw2(st), bup(st);
+    double* P = bP.alloc(size_t(m) * pwmax);
+    double* y = by.alloc(size_t(m) * pwmax);
+    double* yT = byT.alloc(size_t(m) * pwmax);
+    double* t = bt.alloc(size_t(pwmax) * pwmax);
+    double* tT = btT.alloc(size_t(pwmax) * pwmax);
+    double* as = bas.alloc(size_t(m) * (n - pwmax));
+    double* w1 = bw1.alloc(size_t(pwmax) * (n - pwmax));
+    double* w2 = bw2.alloc(size_t(pwmax) * (n - pwmax));
+    double* up = bup.alloc(size_t(m) * (n - pwmax));
+    if (!P || !y || !yT || !t || !tT || !as || !w1 || !w2 || !up) return 2;
+    int64_t p = 0;
+    for (int64_t p0 = 0; p0 < n; p0 += panel, ++p) {
+        const int pw = (int)std::min(panel, n - p0);
+        const int64_t rows = m - p0, nt = n - p0 - pw;
+        const int threads = std::min(kPanelThreads, std::max(32, (pw + 31) / 32 * 32));
+        panel_kernel<<<1, threads, 0, st>>>(f, n, m, p0, pw, P, y, yT, t, tT);
+        ++*nl;
+        copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
+        ++*nl;
+        if (nt > 0) {
+            copy_block_kernel<<<grid_for(rows * nt), 256, 0, st>>>(f + p0 * n + p0 + pw, n, as, nt, rows, nt);
+            ++*nl;
+        }
+        // A_s -= Y T^T Y^T A_s, all three products dispatched (qr.cpp:127-132)
+        int rc = adpb200_adp_gemm(h, pw, nt, rows, 1.0, yT, as, 0.0, nullptr, w1, opt, traces + 3 * p, st);
+        if (!rc) rc = adpb200_adp_gemm(h, pw, nt, pw, 1.0, tT, w1, 0.0, nullptr, w2, opt, traces + 3 * p + 1, st);
+        if (!rc) rc = adpb200_adp_gemm(h, rows, nt, pw, -1.0, y, w2, 1.0, as, up, opt, traces + 3 * p + 2, st);
+        if (rc) return rc;
+        if (nt > 0) {
+            copy_block_kernel<<<grid_for(rows * nt), 256, 0, st>>>(up, nt, f + p0 * n + p0 + pw, n, rows, nt);
+            ++*nl;
+        }
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+int qr_materialize_q(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* fac, const double* t_blocks,
+                     double* q, cudaStream_t st, uint64_t* nl) {
+    const int64_t pwmax = std::min(panel, n);
+    DevBuf by(st), byT(st), bqs(st), bx1(st), bx2(st), bup(st);
+    double* y = by.alloc(size_t(m) * pwmax);
+    double* yT = byT.alloc(size_t(m) * pwmax);
+    double* qs = bqs.alloc(size_t(m) * n);
+    double* x1 = bx1.alloc(size_t(pwmax) * n);
+    double* x2 = bx2.alloc(size_t(pwmax) * n);
+    double* up = bup.alloc(size_t(m) * n);
+    if (!y || !yT || !qs || !x1 || !x2 || !up) return 2;
+    eye_kernel<<<grid_for(m * n), 256, 0, st>>>(q, m, n);
+    ++*nl;
+    const int64_t panels = (n + panel - 1) / panel;
+    // Q = (I - Y_1 T_1 Y_1^T) ... (I - Y_K T_K Y_K^T) applied to thin I, rightmost first (qr.cpp:145-173)
+    for (int64_t p = panels - 1; p >= 0; --p) {
+        const int64_t p0 = p * panel;
+        const int pw = (int)std::min(panel, n - p0);
+        const int64_t rows = m - p0;
+        build_y_kernel<<<grid_for(rows * pw), 256, 0, st>>>(fac, n, m, p0, pw, y, yT);
+        copy_block_kernel<<<grid_for(rows * n), 256, 0, st>>>(q + p0 * n, n, qs, n, rows, n);
+        *nl += 2;
+        int rc = adpb200_native_gemm(h, yT, qs, pw, n, rows, 1.0, 0.0, nullptr, x1, st);
+        if (!rc) {
+            copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t_blocks + p * panel * panel, pw, up, pw, pw,
+                                                                         pw);
+            ++*nl;
+            rc = adpb200_native_gemm(h, up, x1, pw, n, pw, 1.0, 0.0, nullptr, x2, st);
+        }
+        if (!rc) rc = adpb200_native_gemm(h, y, x2, rows, n, pw, -1.0, 1.0, qs, up, st);
+        if (rc) return rc;
+        copy_block_kernel<<<grid_for(rows * n), 256, 0, st>>>(up, n, q + p0 * n, n, rows, n);
+        ++*nl;
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+int qr_residual(adpb200_handle h, int64_t m, int64_t n, int64_t panel, const double* a0, const double* fac,
+                const double* t_blocks, double* out, cudaStream_t st, uint64_t* nl) {
+    DevBuf bq(st), bqT(st), br(st), bd(st), bg(st);
+    double* q = bq.alloc(size_t(m) * n);
+    double* qT = bqT.alloc(size_t(m) * n);
+    double* r = br.alloc(size_t(n) * n);
+    double* d = bd.alloc(size_t(m) * n);
+    double* g = bg.alloc(size_t(n) * n);
+    if (!q || !qT || !r || !d || !g) return 2;
+    int rc = qr_materialize_q(h, m, n, panel, fac, t_blocks, q, st, nl);
+    if (rc) return rc;
+    upper_r_kernel<<<grid_for(n * n), 256, 0, st>>>(fac, n, n, r);
+    ++*nl;
+    rc = adpb200_native_gemm(h, q, r, m, n, n, 1.0, 0.0, nullptr, d, st);  // prod = Q R
+    if (rc) return rc;
+    // diff = a0 - prod: d := a0 - d, computed as a copy of a0 minus prod
+    copy_block_kernel<<<grid_for(m * n), 256, 0, st>>>(a0, n, qT, n, m, n);
+    sub_kernel<<<grid_for(m * n), 256, 0, st>>>(qT, d, m * n, 0);
+    *nl += 2;
+    double* diff = qT;
+    // gram = Q^T Q - I (the transpose goes into d, no longer needed)
+    transpose_kernel<<<grid_for(m * n), 256, 0, st>>>(q, d, m, n);
+    ++*nl;
+    rc = adpb200_native_gemm(h, d, q, n, n, m, 1.0, 0.0, nullptr, g, st);
+    if (rc) return rc;
+    sub_kernel<<<grid_for(n * n), 256, 0, st>>>(g, nullptr, n * n, n);
+    qr_norms_kernel<<<1, 64, 0, st>>>(diff, a0, g, m * n, n * n, out);
+    *nl += 2;
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
+}  // namespace adpb200

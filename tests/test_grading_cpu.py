@@ -65,3 +65,12 @@ def test_csv_format():
     assert grading._num(1.2345678901234568e20) == "123456789012345680000"
     assert grading._num(1e22) == "1e+22"
     assert grading._num(-0.0) == "-0"
+
+
+def test_qr_histogram_csv():
+    from paper_2511_13778_b200 import AdpTrace
+    from paper_2511_13778_b200.qr import histogram_csv
+
+    tr = [AdpTrace(path="emulated", slices=8), AdpTrace(path="emulated", slices=7),
+          AdpTrace(path="emulated", slices=8), AdpTrace(path="native_fallback")]
+    assert histogram_csv(tr) == "slices,count\n7,1\n8,2\nnative_fallback,1\n"
