@@ -396,6 +396,20 @@ class Oracle:
         return float(self.lib.ozref_time_qr(_p(a), C.c_longlong(a.shape[0]), C.c_longlong(a.shape[1]),
                                             C.c_longlong(panel), C.c_longlong(min_dim)))
 
+    def write_matrix(self, path, a):
+        self._need_ref("write_matrix")
+        a = _f64(a)
+        self._check(self.lib.ozref_write_matrix(path.encode(), _p(a), C.c_longlong(a.shape[0]),
+                                                C.c_longlong(a.shape[1])), "write_matrix")
+
+    def read_matrix(self, path):
+        self._need_ref("read_matrix")
+        dims = (C.c_longlong * 2)()
+        self._check(self.lib.ozref_read_matrix(path.encode(), None, C.c_longlong(0), dims), "read_matrix")
+        out = np.empty((dims[0], dims[1]), np.float64)
+        self._check(self.lib.ozref_read_matrix(path.encode(), _p(out), C.c_longlong(out.size), dims), "read_matrix")
+        return out
+
 
 def fold_round(acc_row: np.ndarray, exp2: int) -> float:
     """Exact fold of one element's diagonal accumulators + RNE (port only)."""

@@ -25,6 +25,7 @@
 #include "ozadp/igemm.hpp"
 #include "ozadp/oracle.hpp"
 #include "ozadp/qr.hpp"
+#include "ozadp/matrix_io.hpp"
 #include "ozadp/slicing.hpp"
 #include "ozadp/threads.hpp"
 
@@ -409,6 +410,20 @@ double ozref_time_qr(const double* a, long long m, long long n, long long panel,
         return -1.0;
     }
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// matrix_io (matrix_io.cpp): write_matrix by extension / read_matrix by sniffing.
+int ozref_write_matrix(const char* path, const double* a, long long rows, long long cols) {
+    return guarded([&] { write_matrix(path, wrap(a, rows, cols)); });
+}
+// dims[2] out; out may be NULL to query the shape (cap elements max).
+int ozref_read_matrix(const char* path, double* out, long long cap, long long* dims) {
+    return guarded([&] {
+        MatrixF64 m = read_matrix(path);
+        dims[0] = (long long)m.rows();
+        dims[1] = (long long)m.cols();
+        if (out && (long long)m.size() <= cap) unwrap(m, out);
+    });
 }
 
 }  // extern "C"

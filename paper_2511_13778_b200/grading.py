@@ -314,7 +314,9 @@ def _num(v: float) -> str:
     if point <= 0:
         fixed = "0." + "0" * (-point) + digits
     elif point >= len(digits):
-        fixed = digits + "0" * (point - len(digits))
+        # an integer: the fixed form prints its exact digits (123456789012345683968,
+        # not the shortest digits padded with zeros), like printf("%f")
+        fixed = str(int(v))
     else:
         fixed = digits[:point] + "." + digits[point:]
     return sign + (fixed if len(fixed) <= len(sci) else sci)

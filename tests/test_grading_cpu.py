@@ -62,7 +62,7 @@ def test_csv_format():
     assert grading.to_csv(row) == "test2,256,4,auto,53,9,8,0,1e-16,1e-04,42"
     row2 = grading.SweepRow(test="uniform", n=512, mode="native", max_err=123.0, avg_err=1.5, seed=7)
     assert grading.to_csv(row2) == "uniform,512,,native,53,,0,0,123,1.5,7"
-    assert grading._num(1.2345678901234568e20) == "123456789012345680000"
+    assert grading._num(1.2345678901234568e20) == "123456789012345683968"
     assert grading._num(1e22) == "1e+22"
     assert grading._num(-0.0) == "-0"
 
