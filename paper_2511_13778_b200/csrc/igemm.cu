@@ -25,6 +25,7 @@
 // k longer than the int32-safe chunk (see int32_kchunk) is split into chunks;
 // each chunk's exact partial sum is kept in a limb workspace in HBM.
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "igemm.cuh"
@@ -34,10 +35,6 @@ namespace adpb200 {
 
 namespace {
 
-constexpr int kFirstEpiWarp = 4;                  // warps 0-3: TMA, MMA, TMEM alloc, spare
-constexpr int kEpiWarps = 8;                      // 2 per TMEM lane quadrant
-constexpr int kEpiThreads = kEpiWarps * 32;
-constexpr int kThreads = kFirstEpiWarp * 32 + kEpiThreads;
 constexpr int kBM = 128;      // rows of a tile (UMMA M)
 constexpr int kKB = 32;       // bytes of k per stage (one UMMA K step for int8)
 constexpr int kMaxStages = 8;
@@ -45,6 +42,16 @@ constexpr int kGroupM = 16;   // raster: 16 m-tiles per group
 
 template <int NB>
 struct Cfg {
+    // warp roles: warps 0-3 = TMA producer, MMA issuer, TMEM allocator, spare; then
+    // 8 epilogue warps, 2 per TMEM lane quadrant (warp id % 4), NB/2 columns each.
+    // (Measured alternatives: one epilogue warp per quadrant (256 threads, 255
+    // registers) drains TMEM 2x slower; 16 epilogue warps cap registers at 96.)
+    static constexpr int kFirstEpiWarp = 4;
+    static constexpr int kAllocWarp = 2;
+    static constexpr int kEpiWarps = 8;
+    static constexpr int kEpiThreads = kEpiWarps * 32;
+    static constexpr int kThreads = kFirstEpiWarp * 32 + kEpiThreads;
+    static constexpr int kColGroups = kEpiWarps / 4;
     static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
     // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
     static constexpr int kNL = NB >= 48 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
@@ -305,6 +312,11 @@ struct Loop {
     uint32_t a_bytes, stage_bytes;
 };
 
+// Timing diagnostics (ADPB200_DEBUG & 4): per CTA, clock64 cycles of the MMA
+// warp in total / waiting for TMEM to drain / waiting for a full stage, and of
+// the first epilogue warp holding TMEM (tmem_full seen -> tmem_empty arrive).
+__device__ unsigned long long g_dbg[1024 * 4];
+
 // The MMA role, converged warp; SCHED = compile-time (S, L) or runtime smem.
 template <int NB, int S, int L>
 __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const SmemSched* sched, uint32_t stage0,
@@ -312,14 +324,20 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
     constexpr bool kStatic = S > 0;
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
+    const bool timing = (debug & 4) != 0;
+    unsigned long long t_start = timing ? clock64() : 0ull, w_tmem = 0, w_full = 0;
     for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
         for (int c = 0; c < lp.nchunks; ++c) {
+            unsigned long long t0 = timing ? clock64() : 0ull;
             tc::mbar_wait(&hdr->tmem_empty, acc_phase ^ 1);
+            if (timing) w_tmem += clock64() - t0;
             tc::fence_after();
             const int64_t kb0 = int64_t(c) * lp.kb_per_chunk;
             const int64_t kb1 = kb0 + lp.kb_per_chunk < lp.nkb ? kb0 + lp.kb_per_chunk : lp.nkb;
             for (int64_t kb = kb0; kb < kb1; ++kb) {
+                if (timing) t0 = clock64();
                 tc::mbar_wait(&hdr->full[stage], phase);
+                if (timing) w_full += clock64() - t0;
                 tc::fence_after();
                 const uint32_t sa = stage0 + uint32_t(stage) * lp.stage_bytes;
                 const uint32_t sb = sa + lp.a_bytes;
@@ -364,6 +382,11 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
             acc_phase ^= 1;
         }
     }
+    if (timing && (threadIdx.x & 31) == 0 && blockIdx.x < 1024) {
+        g_dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
+        g_dbg[blockIdx.x * 4 + 1] = w_tmem;
+        g_dbg[blockIdx.x * 4 + 2] = w_full;
+    }
 }
 
 // (S, L) pairs with a compile-time schedule: the ADPB200_PAIRS_TARGET
@@ -396,7 +419,7 @@ __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemH
 }
 
 template <int NB>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
     igemm_kernel(const __grid_constant__ PlaneMaps maps, GemmArgs g) {
     using C = Cfg<NB>;
     const Plan* plan = g.plan;
@@ -433,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc::mbar_init(&hdr->empty[i], 1);
         }
         tc::mbar_init(&hdr->tmem_full, 1);
-        tc::mbar_init(&hdr->tmem_empty, kEpiThreads);
+        tc::mbar_init(&hdr->tmem_empty, C::kEpiThreads);
         tc::fence_barrier_init();
     }
     if (threadIdx.x == 32) {
@@ -447,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::tma_prefetch(map_a);
         tc::tma_prefetch(map_b);
     }
-    if (warp == 2) tc::tmem_alloc(&hdr->tmem_slot, 512);
+    if (warp == C::kAllocWarp) tc::tmem_alloc(&hdr->tmem_slot, 512);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
@@ -491,14 +514,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ===== MMA issuer (converged warp, one elected lane issues) =====
         mma_dispatch<NB>(s, L, lp, hdr, sched, tc::smem_u32(stages), tmem_base, g.debug);
-    } else if (warp >= kFirstEpiWarp) {
-        // ===== epilogue: 8 warps, (lane quadrant, column half) each =====
-        const int ew = warp - kFirstEpiWarp;
-        const int q = warp & 3;        // TMEM lane quadrant (warp id % 4)
-        const int jh = ew / 4;         // column half
-        constexpr int kCols = NB / 2;  // columns per epilogue warp
+    } else if (warp >= C::kFirstEpiWarp) {
+        // ===== epilogue: (lane quadrant, column group) per warp =====
+        const int ew = warp - C::kFirstEpiWarp;
+        const int q = warp & 3;                        // TMEM lane quadrant (warp id % 4)
+        const int jh = ew / 4;                         // column group
+        constexpr int kCols = NB / C::kColGroups;      // columns per epilogue warp
         uint32_t acc_phase = 0;
         const int exp_base = -14 - 8 * L;
+        const bool timing = (g.debug & 4) != 0 && ew == 0;
+        unsigned long long hold = 0, th = 0;
         for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
             int64_t mt, nt;
             tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
@@ -513,8 +538,92 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < lp.nchunks; ++c) {
                 tc::mbar_wait(&hdr->tmem_full, acc_phase);
                 tc::fence_after();
+                if (timing) th = clock64();
                 const bool last = c == lp.nchunks - 1;
                 const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
+                if constexpr (C::kNL == 2) {
+                    if (!g.dump) {
+                        // phase A (holding TMEM): fold every column of the warp exactly and
+                        // park it in kW 32-bit registers, so the tile's whole accumulator set
+                        // leaves TMEM before any rounding math. Missing diagonals (D >= L+1)
+                        // count as zeros at the low end: S' = sum_{D < kNDMax} acc_D
+                        // 256^(kNDMax-1-D) = S * 256^(kNDMax-1-L), so every shift is static
+                        // and the exponent below absorbs the factor (|S'| < 2^88 for NB 64,
+                        // < 2^104 for NB 48).
+                        constexpr int kW = NB == 64 ? 3 : 4;
+                        constexpr int kB = 2;  // columns per TMEM load batch
+                        uint32_t w[kCols][kW];
+#pragma unroll
+                        for (int b = 0; b < kCols / kB; ++b) {
+                            const int j0 = jh * kCols + b * kB;
+                            uint32_t v[C::kNDMax][kB];
+#pragma unroll
+                            for (int D = 0; D < C::kNDMax; ++D) {
+                                if (D < ndiag) {
+                                    tc::tmem_ld<kB>(trow + uint32_t(D * NB + j0), v[D]);
+                                } else {
+#pragma unroll
+                                    for (int cc = 0; cc < kB; ++cc) v[D][cc] = 0u;
+                                }
+                            }
+                            tc::tmem_wait_ld();
+                            if (g.debug & 8) continue;  // diagnostics: TMEM drain without the fold
+#pragma unroll
+                            for (int cc = 0; cc < kB; ++cc) {
+                                __int128 S128 = 0;
+#pragma unroll
+                                for (int g0 = 0; g0 < C::kNDMax; g0 += 4) {
+                                    int64_t h = 0;
+                                    constexpr int kLast = C::kNDMax;
+                                    const int len = kLast - g0 < 4 ? kLast - g0 : 4;
+#pragma unroll
+                                    for (int D = g0; D < g0 + len; ++D) h = h * 256 + int32_t(v[D][cc]);
+                                    S128 = g0 == 0 ? __int128(h) : (S128 << (8 * len)) + h;
+                                }
+                                const unsigned __int128 U = (unsigned __int128)S128;
+#pragma unroll
+                                for (int i = 0; i < kW; ++i) w[b * kB + cc][i] = uint32_t(U >> (32 * i));
+                            }
+                        }
+                        tc::fence_before();
+                        tc::mbar_arrive(&hdr->tmem_empty);
+                        if (timing) hold += clock64() - th;
+                        // phase B (TMEM already back with the MMA warp): round, scale, store
+#pragma unroll
+                        for (int jl = 0; jl < kCols; ++jl) {
+                            const int ebj = __shfl_sync(0xffffffffu, eb_lane, jl);
+                            const int64_t col = nt * NB + jh * kCols + jl;
+                            if (!row_ok || col >= g.N || (g.debug & 2)) continue;
+                            uint64_t S[2];
+                            S[0] = uint64_t(w[jl][0]) | (uint64_t(w[jl][1]) << 32);
+                            if constexpr (kW == 3)
+                                S[1] = uint64_t(int64_t(int32_t(w[jl][2])));  // sign-extend bit 95
+                            else
+                                S[1] = uint64_t(w[jl][2]) | (uint64_t(w[jl][3]) << 32);
+                            if (lp.nchunks > 1) {
+                                uint64_t* P = g.partial + size_t(blockIdx.x) * (2 * NB * kBM) +
+                                              size_t(jh * kCols + jl) * kBM + (q * 32 + lane);
+                                const int64_t lstride = int64_t(NB) * kBM;
+                                if (c > 0) {
+                                    const uint64_t prev[2] = {P[0], P[lstride]};
+                                    limbs_add<2>(S, prev);
+                                }
+                                if (!last) {
+                                    P[0] = S[0];
+                                    P[lstride] = S[1];
+                                    continue;
+                                }
+                            }
+                            const double vv = round_i128(__int128((unsigned __int128)S[1] << 64 | S[0]),
+                                                         ea + ebj - 14 - 8 * (C::kNDMax - 1));
+                            double r = __dmul_rn(g.alpha, vv);
+                            if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
+                            g.c_out[row + col * g.ldc] = r;
+                        }
+                        acc_phase ^= 1;
+                        continue;
+                    }
+                }
 #pragma unroll 1
                 for (int j0 = jh * kCols; j0 < (jh + 1) * kCols; j0 += C::kCW) {
                     int eb[C::kCW];
@@ -530,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         // to the MMA warp now, the last batch's math overlaps its next tile
                         tc::fence_before();
                         tc::mbar_arrive(&hdr->tmem_empty);
+                        if (timing) hold += clock64() - th;
                     }
 #pragma unroll
                     for (int cc = 0; cc < C::kCW; ++cc) {
@@ -605,9 +715,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc_phase ^= 1;
             }
         }
+        if (timing && lane == 0 && blockIdx.x < 1024) g_dbg[blockIdx.x * 4 + 3] = hold;
     }
     __syncthreads();
-    if (warp == 2) {
+    if (warp == C::kAllocWarp) {
         tc::fence_after();
         tc::tmem_dealloc(tmem_base, 512);
     }
@@ -709,28 +820,45 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     switch (nb) {
         case 64:
             set_attr_once<64>();
-            igemm_kernel<64><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            igemm_kernel<64><<<grid, Cfg<64>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 48:
             set_attr_once<48>();
-            igemm_kernel<48><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            igemm_kernel<48><<<grid, Cfg<48>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 32:
             set_attr_once<32>();
-            igemm_kernel<32><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            igemm_kernel<32><<<grid, Cfg<32>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 16:
             set_attr_once<16>();
-            igemm_kernel<16><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            igemm_kernel<16><<<grid, Cfg<16>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 8:
             set_attr_once<8>();
-            igemm_kernel<8><<<grid, kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            igemm_kernel<8><<<grid, Cfg<8>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         default:
             return -2;
     }
     ++*nlaunch;
+    if (debug & 4) {
+        // diagnostics only: synchronise and summarise the per-CTA cycle counters
+        unsigned long long h[1024 * 4];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_dbg, sizeof(unsigned long long) * 4 * size_t(grid));
+        double t = 0, wt = 0, wf = 0, ho = 0;
+        for (int b = 0; b < grid; ++b) {
+            t += double(h[b * 4]);
+            wt += double(h[b * 4 + 1]);
+            wf += double(h[b * 4 + 2]);
+            ho += double(h[b * 4 + 3]);
+        }
+        fprintf(stderr,
+                "igemm<%d> debug: mma warp %.0f cycles/CTA, waiting tmem %.1f%%, waiting full stage %.1f%%, "
+                "epilogue holds tmem %.1f%%\n",
+                nb, t / grid, 100.0 * wt / t, 100.0 * wf / t, 100.0 * ho / t);
+    }
     return 0;
 }
 

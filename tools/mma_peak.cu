@@ -75,19 +75,34 @@ struct Ops<3> {
     }
 };
 
+// Shared-memory write pressure next to the MMAs (tma_chunk > 0): warp 2 streams
+// a global buffer into a separate smem ring with cp.async.bulk (the TMA's
+// async-proxy write path, like the GEMM's producer) while warp 0 issues MMAs;
+// the bytes it moved are reported through wbytes.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
 template <int CASE>
 __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int runtime_ops, const Op* rt,
-                                                   unsigned long long* cycles) {
+                                                   unsigned long long* cycles, int tma_chunk = 0,
+                                                   const uint8_t* gsrc = nullptr, unsigned long long* wbytes = nullptr) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint32_t tmem_slot;
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t wbar[3];
+    __shared__ volatile int stop_flag;
     __shared__ Op sops[16];
     for (int i = threadIdx.x; i < 144 * 1024 / 4; i += blockDim.x)
         reinterpret_cast<uint32_t*>(smem)[i] = 0x01010101u * (i & 7);
     if (threadIdx.x < Ops<CASE>::n) sops[threadIdx.x] = rt[threadIdx.x];
     if (threadIdx.x == 0) {
         tc::mbar_init(&bar, 1);
+        for (int i = 0; i < 3; ++i) tc::mbar_init(&wbar[i], 1);
+        stop_flag = 0;
         tc::fence_barrier_init();
     }
     if (threadIdx.x / 32 == 1) tc::tmem_alloc(&tmem_slot, 512);
@@ -122,7 +137,30 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int runtime_ops, c
         __syncwarp();
         tc::mbar_wait(&bar, 0);
         unsigned long long t1 = clock64();
-        if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+        if (threadIdx.x == 0) {
+            cycles[blockIdx.x] = t1 - t0;
+            stop_flag = 1;
+        }
+    } else if (threadIdx.x == 64 && tma_chunk > 0) {
+        // three chunks in flight into [144 KiB, 144 KiB + 3 * tma_chunk)
+        const uint32_t ring = tc::smem_u32(smem) + 144u * 1024u;
+        unsigned long long moved = 0;
+        uint32_t phase[3] = {0, 0, 0};
+        const uint8_t* src = gsrc + size_t(blockIdx.x % 8) * (1u << 20);
+        for (int i = 0; i < 3; ++i) {
+            tc::mbar_expect_tx(&wbar[i], tma_chunk);
+            bulk_g2s(ring + i * tma_chunk, src + i * tma_chunk, tma_chunk, tc::smem_u32(&wbar[i]));
+        }
+        for (int it = 0; !stop_flag; ++it) {
+            const int i = it % 3;
+            tc::mbar_wait(&wbar[i], phase[i]);
+            phase[i] ^= 1;
+            moved += tma_chunk;
+            tc::mbar_expect_tx(&wbar[i], tma_chunk);
+            bulk_g2s(ring + i * tma_chunk, src + ((it + 3) % 48) * tma_chunk, tma_chunk, tc::smem_u32(&wbar[i]));
+        }
+        for (int i = 0; i < 3; ++i) tc::mbar_wait(&wbar[i], phase[i]);
+        wbytes[blockIdx.x] = moved;
     }
     __syncthreads();
     if (threadIdx.x / 32 == 1) {
@@ -132,20 +170,27 @@ __global__ void __launch_bounds__(128, 1) mma_loop(int iters, int runtime_ops, c
 }
 
 template <int CASE>
-static void run(const char* name, int iters, int runtime_ops) {
+static void run(const char* name, int iters, int runtime_ops, int tma_chunk = 0) {
+    static uint8_t* gsrc = nullptr;
+    static unsigned long long* wb = nullptr;
+    if (!gsrc) {
+        cudaMalloc(&gsrc, 8u << 20);
+        cudaMemset(gsrc, 1, 8u << 20);
+        cudaMalloc(&wb, 148 * 8);
+    }
     Op* d;
     cudaMalloc(&d, sizeof(Op) * Ops<CASE>::n);
     cudaMemcpy(d, Ops<CASE>::opv, sizeof(Op) * Ops<CASE>::n, cudaMemcpyHostToDevice);
     unsigned long long* dcyc;
     cudaMalloc(&dcyc, 148 * 8);
-    const int smem = 144 * 1024 + 1024;
+    const int smem = 144 * 1024 + 3 * 16384 + 1024;
     cudaFuncSetAttribute(mma_loop<CASE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    mma_loop<CASE><<<148, 128, smem>>>(100, runtime_ops, d, dcyc);
+    mma_loop<CASE><<<148, 128, smem>>>(100, runtime_ops, d, dcyc, tma_chunk, gsrc, wb);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    mma_loop<CASE><<<148, 128, smem>>>(iters, runtime_ops, d, dcyc);
+    mma_loop<CASE><<<148, 128, smem>>>(iters, runtime_ops, d, dcyc, tma_chunk, gsrc, wb);
     cudaEventRecord(e1);
     cudaError_t err = cudaEventSynchronize(e1);
     float ms = 0;
@@ -159,9 +204,13 @@ static void run(const char* name, int iters, int runtime_ops) {
     }
     const double tops = 2.0 * macs * double(iters) * 148 / (ms * 1e-3) / 1e12;
     const double cpi = double(cyc[0]) / iters;
+    unsigned long long wbh[148] = {};
+    if (tma_chunk) cudaMemcpy(wbh, wb, sizeof(wbh), cudaMemcpyDeviceToHost);
     printf("{\"case\": \"%s\", \"err\": \"%s\", \"ms\": %.3f, \"int8_tops\": %.1f, \"cycles_per_iter\": %.1f, "
-           "\"ideal_cycles_per_iter\": %.1f, \"efficiency\": %.3f, \"sm_clock_ghz\": %.3f}\n",
-           name, cudaGetErrorString(err), ms, tops, cpi, ideal, ideal / cpi, double(cyc[0]) / (ms * 1e6));
+           "\"ideal_cycles_per_iter\": %.1f, \"efficiency\": %.3f, \"sm_clock_ghz\": %.3f, "
+           "\"smem_write_B_per_clk\": %.1f}\n",
+           name, cudaGetErrorString(err), ms, tops, cpi, ideal, ideal / cpi, double(cyc[0]) / (ms * 1e6),
+           double(wbh[0]) / double(cyc[0]));
     cudaFree(d);
     cudaFree(dcyc);
 }
@@ -176,5 +225,9 @@ int main(int argc, char** argv) {
     run<2>("n64_static", 400000, 0);
     run<3>("schedule_s7_L7_nb64_static", 60000, 0);
     run<3>("schedule_s7_L7_nb64_runtime", 60000, 1);
+    // the same schedule while a bulk-copy (TMA path) stream writes shared memory
+    run<3>("schedule_s7_L7_nb64_with_bulk_writes_16k", 60000, 0, 16384);
+    run<3>("schedule_s7_L7_nb64_with_bulk_writes_4k", 60000, 0, 4096);
+    run<0>("n256_with_bulk_writes_16k", 400000, 0, 16384);
     return 0;
 }
