@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libadpb200.so")
+# ADPB200_LIB: an alternative build of the same library (tuning experiments only)
+LIB_PATH = os.environ.get("ADPB200_LIB") or os.path.join(PKG, "libadpb200.so")
 
 OK, ERR_RUNTIME, ERR_CONTRACT = 0, 2, 3
 MODE_AUTO, MODE_EMULATE, MODE_NATIVE = 0, 1, 2
