@@ -22,20 +22,66 @@
 namespace adpb200 {
 namespace {
 
-constexpr int kPanelThreads = 1024;  // panel width limit of the one-CTA panel kernel
+constexpr int kPanelThreads = 256;   // one CTA per panel; columns beyond 256 loop
+constexpr size_t kPanelSmemMax = 192 * 1024;  // reflector column + squares in shared memory up to 12288 rows
+
+// Sequential sums in the reference's order, with the loads software-pipelined
+// (independent of the running sum) so one thread runs at FP64-add latency.
+// sum_{r in [r0, r1)} x[r] * y[r] added onto `init` left to right.
+__device__ __forceinline__ double seq_dot(double init, const double* __restrict__ x, const double* __restrict__ y,
+                                          int64_t r0, int64_t r1) {
+    // 16 products per chunk, the next chunk's loads issued before this chunk's adds:
+    // ~32 loads in flight per thread hide the L2 latency of the column walk
+    constexpr int kU = 16;
+    double acc = init;
+    int64_t r = r0;
+    if (r + kU <= r1) {
+        double xa[kU], ya[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            xa[u] = x[r + u];
+            ya[u] = y[r + u];
+        }
+        for (; r + 2 * kU <= r1; r += kU) {
+            double xb[kU], yb[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                xb[u] = x[r + kU + u];
+                yb[u] = y[r + kU + u];
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) acc = __dadd_rn(acc, __dmul_rn(xa[u], ya[u]));
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                xa[u] = xb[u];
+                ya[u] = yb[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) acc = __dadd_rn(acc, __dmul_rn(xa[u], ya[u]));
+        r += kU;
+    }
+    for (; r < r1; ++r) acc = __dadd_rn(acc, __dmul_rn(x[r], y[r]));
+    return acc;
+}
 
 // Panel factorisation of f[p0:m, p0:p0+pw] (row-major f, leading dimension ld).
-// P: column-major scratch (rows x pw). Outputs: the panel written back to f,
-// y (rows x pw) and yT (pw x rows) row-major, t and tT (pw x pw) row-major.
+// P: column-major scratch (rows x pw). v: the current reflector column (shared
+// memory when it fits, else global scratch). Outputs: the panel written back to
+// f, y (rows x pw) and yT (pw x rows) row-major, t and tT (pw x pw) row-major.
 __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict__ f, int64_t ld, int64_t m, int64_t p0,
                                                               int pw, double* __restrict__ P, double* __restrict__ y,
                                                               double* __restrict__ yT, double* __restrict__ t,
-                                                              double* __restrict__ tT) {
+                                                              double* __restrict__ tT, double* __restrict__ vglob) {
+    extern __shared__ double vsh[];
     const int64_t rows = m - p0;
+    double* v = vglob ? vglob : vsh;
+    double* q2 = v + rows;  // (v[r] / amax)^2, computed in parallel, summed in order by one thread
     const int tid = threadIdx.x, nth = blockDim.x;
-    __shared__ double tau_s[kPanelThreads];
-    __shared__ double z_s[kPanelThreads];
-    __shared__ double v0_s, beta_s, x0_s;
+    __shared__ double tau_s[1024];
+    __shared__ double z_s[1024];
+    __shared__ double red_s[32];
+    __shared__ double v0_s, beta_s, x0_s, tail_s;
     __shared__ int mode_s;
     for (int64_t e = tid; e < rows * pw; e += nth) {
         const int64_t r = e / pw, j = e - r * pw;
@@ -44,37 +90,64 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
     __syncthreads();
     for (int j = 0; j < pw; ++j) {
         double* col = P + int64_t(j) * rows;
-        // ---- make_reflector (qr.cpp:26-47): sequential sums on one thread
+        for (int64_t r = j + tid; r < rows; r += nth) v[r] = col[r];
+        __syncthreads();
+        // ---- make_reflector (qr.cpp:26-47)
+        // column_norm's max (qr.cpp:15): exact and order-free, reduced in parallel
+        double amax = 0.0;
+        for (int64_t r = j + tid; r < rows; r += nth) {
+            const double a = fabs(v[r]);
+            amax = amax < a ? a : amax;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double b = __shfl_xor_sync(0xffffffffu, amax, o);
+            amax = amax < b ? b : amax;
+        }
+        if ((tid & 31) == 0) red_s[tid >> 5] = amax;
+        __syncthreads();
+        amax = red_s[0];
+        for (int w = 1; w < (nth + 31) / 32; ++w) amax = amax < red_s[w] ? red_s[w] : amax;
+        // the squares (f/amax)^2 of column_norm (qr.cpp:17-19) are element-independent:
+        // divide in parallel (a division costs ~100 cycles on one thread), sum in order below
+        if (amax != 0.0)
+            for (int64_t r = j + tid; r < rows; r += nth) {
+                const double q = __ddiv_rn(v[r], amax);
+                q2[r] = __dmul_rn(q, q);
+            }
+        __syncthreads();
+        // the two sequential sums run concurrently on two warps, each in reference order
+        if (tid == 0) tail_s = seq_dot(0.0, v, v, j + 1, rows);  // tail_ss (qr.cpp:29)
+        if (tid == 32 % nth) {
+            double ss = 0.0;
+            if (amax != 0.0) {
+                int64_t r = j;
+                for (; r + 16 <= rows; r += 16) {
+                    double b[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) b[u] = q2[r + u];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) ss = __dadd_rn(ss, b[u]);
+                }
+                for (; r < rows; ++r) ss = __dadd_rn(ss, q2[r]);
+            }
+            beta_s = amax != 0.0 ? __dmul_rn(amax, __dsqrt_rn(ss)) : 0.0;
+        }
+        __syncthreads();
         if (tid == 0) {
-            const double x0 = col[j];
-            double tail = 0.0;
-            for (int64_t r = j + 1; r < rows; ++r) tail = __dadd_rn(tail, __dmul_rn(col[r], col[r]));
+            const double x0 = v[j], tail = tail_s;
             if (tail == 0.0) {
                 mode_s = 0;
                 if (x0 >= 0.0) {
                     tau_s[j] = 0.0;
                 } else {
                     col[j] = -x0;
+                    v[j] = -x0;
                     tau_s[j] = 2.0;
                 }
             } else {
-                // column_norm (qr.cpp:14-22)
-                double amax = 0.0;
-                for (int64_t r = j; r < rows; ++r) {
-                    const double a = fabs(col[r]);
-                    amax = amax < a ? a : amax;  // std::max
-                }
-                double beta = 0.0;
-                if (amax != 0.0) {
-                    double ss = 0.0;
-                    for (int64_t r = j; r < rows; ++r) {
-                        const double q = __ddiv_rn(col[r], amax);
-                        ss = __dadd_rn(ss, __dmul_rn(q, q));
-                    }
-                    beta = __dmul_rn(amax, __dsqrt_rn(ss));
-                }
+                const double beta = beta_s;
                 v0_s = x0 > 0.0 ? __ddiv_rn(-tail, __dadd_rn(x0, beta)) : __dsub_rn(x0, beta);
-                beta_s = beta;
                 x0_s = x0;
                 mode_s = 1;
             }
@@ -82,10 +155,15 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
         __syncthreads();
         if (mode_s == 1) {
             const double v0 = v0_s;
-            for (int64_t r = j + 1 + tid; r < rows; r += nth) col[r] = __ddiv_rn(col[r], v0);
+            for (int64_t r = j + 1 + tid; r < rows; r += nth) {
+                const double q = __ddiv_rn(v[r], v0);
+                v[r] = q;
+                col[r] = q;
+            }
             __syncthreads();
             if (tid == 0) {
                 col[j] = beta_s;
+                v[j] = beta_s;
                 tau_s[j] = __ddiv_rn(__dsub_rn(beta_s, x0_s), beta_s);
             }
         }
@@ -95,11 +173,23 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
         if (tau != 0.0) {
             for (int cc = j + 1 + tid; cc < pw; cc += nth) {
                 double* dst = P + int64_t(cc) * rows;
-                double dot = dst[j];
-                for (int64_t r = j + 1; r < rows; ++r) dot = __dadd_rn(dot, __dmul_rn(col[r], dst[r]));
+                const double dot = seq_dot(dst[j], v, dst, j + 1, rows);
                 const double w = __dmul_rn(tau, dot);
                 dst[j] = __dsub_rn(dst[j], w);
-                for (int64_t r = j + 1; r < rows; ++r) dst[r] = __dsub_rn(dst[r], __dmul_rn(w, col[r]));
+                // the update is element-independent: load a chunk, then store it (the
+                // stores would otherwise serialise every load behind them: v may alias)
+                int64_t r = j + 1;
+                for (; r + 16 <= rows; r += 16) {
+                    double d[16], vv[16];
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        d[u] = dst[r + u];
+                        vv[u] = v[r + u];
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) dst[r + u] = __dsub_rn(d[u], __dmul_rn(w, vv[u]));
+                }
+                for (; r < rows; ++r) dst[r] = __dsub_rn(dst[r], __dmul_rn(w, v[r]));
             }
         }
         __syncthreads();
@@ -107,9 +197,9 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
     // write the panel back; build_y (qr.cpp:64-71)
     for (int64_t e = tid; e < rows * pw; e += nth) {
         const int64_t r = e / pw, j = e - r * pw;
-        const double v = P[j * rows + r];
-        f[(p0 + r) * ld + p0 + j] = v;
-        const double yv = r == j ? 1.0 : (r > j ? v : 0.0);
+        const double val = P[j * rows + r];
+        f[(p0 + r) * ld + p0 + j] = val;
+        const double yv = r == j ? 1.0 : (r > j ? val : 0.0);
         y[r * pw + j] = yv;
         yT[j * rows + r] = yv;
     }
@@ -119,17 +209,12 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
     for (int j = 0; j < pw; ++j) {
         if (tid == 0) t[j * pw + j] = tau_s[j];
         if (j > 0) {
-            // z_i = sum_{r >= j} y(r, i) y(r, j), i < j (y read from the column-major scratch)
+            // z_i = sum_{r >= j} y(r, i) y(r, j), i < j: y(j, j) = 1 first, then the tails
+            const double* cj = P + int64_t(j) * rows;
             for (int i = tid; i < j; i += nth) {
                 const double* ci = P + int64_t(i) * rows;
-                const double* cj = P + int64_t(j) * rows;
-                double dot = 0.0;
-                for (int64_t r = j; r < rows; ++r) {
-                    const double yi = ci[r];                  // r >= j > i: tail of column i
-                    const double yj = r == j ? 1.0 : cj[r];  // unit diagonal of column j
-                    dot = __dadd_rn(dot, __dmul_rn(yi, yj));
-                }
-                z_s[i] = dot;
+                const double first = __dmul_rn(ci[j], 1.0);
+                z_s[i] = seq_dot(__dadd_rn(0.0, first), ci, cj, j + 1, rows);
             }
             __syncthreads();
             for (int i = tid; i < j; i += nth) {
@@ -255,12 +340,26 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
     double* w2 = bw2.alloc(size_t(pwmax) * (n - pwmax));
     double* up = bup.alloc(size_t(m) * (n - pwmax));
     if (!P || !y || !yT || !t || !tT || !as || !w1 || !w2 || !up) return 2;
+    DevBuf bvg(st);
+    double* vg = nullptr;
+    if (2 * size_t(m) * sizeof(double) > kPanelSmemMax) {
+        vg = bvg.alloc(2 * size_t(m));
+        if (!vg) return 2;
+    }
+    static bool attr = [] {
+        cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        return true;
+    }();
+    (void)attr;
     int64_t p = 0;
     for (int64_t p0 = 0; p0 < n; p0 += panel, ++p) {
         const int pw = (int)std::min(panel, n - p0);
         const int64_t rows = m - p0, nt = n - p0 - pw;
-        const int threads = std::min(kPanelThreads, std::max(32, (pw + 31) / 32 * 32));
-        panel_kernel<<<1, threads, 0, st>>>(f, n, m, p0, pw, P, y, yT, t, tT);
+        const int threads = kPanelThreads;
+        // the reflector column in shared memory when it fits (sequential sums at smem latency)
+        const size_t vbytes = 2 * size_t(rows) * sizeof(double);
+        const bool vsmem = vbytes <= kPanelSmemMax;
+        panel_kernel<<<1, threads, vsmem ? vbytes : 0, st>>>(f, n, m, p0, pw, P, y, yT, t, tT, vsmem ? nullptr : vg);
         ++*nl;
         copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
         ++*nl;
