@@ -166,7 +166,7 @@ int plane_cap(const adpb200_options& o, int fixed_slices, int fixed_limit) {
     return cap;
 }
 
-constexpr int kHostChunks = 4;  // row chunks of the host-buffer path (GEMM chunk i || D2H chunk i-1)
+constexpr int kHostChunks = 4;  // row chunks of the host-buffer path (GEMM chunk i || D2H chunk i-1); 8 measured slower
 
 // Destination of C on the host for the host-buffer entry points.
 struct HostOut {
