@@ -240,12 +240,21 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
     __shared__ __align__(16) uint32_t sBmn[kEscTB][kEscBJ / 2];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
     const int64_t i0 = int64_t(blockIdx.y) * kEscBI, j0 = int64_t(blockIdx.x) * kEscBJ;
+    // B stats of column slabs of nr lines, one record of `rec` int32 per slab (the
+    // all-gathered layout of the B-distributed path; nr = n: one slab): the offset of
+    // column j0 + jj minus gt * nr, computed once per CTA (no division in the loops)
+    __shared__ int64_t sBoff[kEscBJ];
+    if (threadIdx.x < kEscBJ) {
+        const int64_t gj = j0 + threadIdx.x;
+        const int64_t r = gj / nr;
+        sBoff[threadIdx.x] = r * rec + (gj - r * nr);
+    }
+    __syncthreads();
     uint32_t z[4][4];  // [i][j pair]
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
-
     for (int64_t tb = 0; tb < t; tb += kEscTB) {
         __syncthreads();
         for (int idx = threadIdx.x; idx < kEscTB * kEscBI; idx += 256) {
@@ -261,19 +270,12 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
             const int jp = idx % (kEscBJ / 2), tt = idx / (kEscBJ / 2);
             const int64_t gj = j0 + 2 * jp, gt = tb + tt;
             const bool ok0 = gj < n && gt < t, ok1 = gj + 1 < n && gt < t;
-            // B stats of column slabs of nr lines, one record of `rec` int32 per slab
-            // (the all-gathered layout of the B-distributed path; nr = n: one slab)
-            const int64_t r0 = gj / nr, r1 = (gj + 1) / nr;
-            const int64_t o0 = r0 * rec + gt * nr + (gj - r0 * nr), o1 = r1 * rec + gt * nr + (gj + 1 - r1 * nr);
+            const int64_t o0 = sBoff[2 * jp] + gt * nr, o1 = sBoff[2 * jp + 1] + gt * nr;
             sBmx[tt][jp] = pack2(ok0 ? to16(bmaxT[o0]) : kS16, ok1 ? to16(bmaxT[o1]) : kS16);
             sBmn[tt][jp] = pack2(ok0 ? to16(bminT[o0]) : kS16, ok1 ? to16(bminT[o1]) : kS16);
         }
         __syncthreads();
-        // only the staged blocks (short k, e.g. 4 blocks at k = 1024, would
-        // otherwise spend 7/8 of the max-plus on sentinel padding)
-        const int tcount = t - tb < kEscTB ? int(t - tb) : kEscTB;
-#pragma unroll 4
-        for (int tt = 0; tt < tcount; ++tt) {
+        auto step = [&](int tt) {
             const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
             const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
             const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
@@ -289,6 +291,16 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
                     z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
                     z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
                 }
+        };
+        if (t - tb >= kEscTB) {
+#pragma unroll 4
+            for (int tt = 0; tt < kEscTB; ++tt) step(tt);
+        } else {
+            // only the staged blocks (short k, e.g. 4 blocks at k = 1024, would
+            // otherwise spend 7/8 of the max-plus on sentinel padding)
+            const int tcount = int(t - tb);
+#pragma unroll 4
+            for (int tt = 0; tt < tcount; ++tt) step(tt);
         }
     }
     int esc = 0;
@@ -305,8 +317,7 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
                 if (gj >= n) continue;
                 const int zz = int(int16_t(z[a][b] >> (16 * h)));
                 if (zz <= -8000) continue;  // structurally zero dot product
-                const int64_t rj = gj / nr;
-                esc = max(esc, la + bline[rj * rec + (gj - rj * nr)] - zz + 1);
+                esc = max(esc, la + bline[sBoff[2 * (tx * 4 + b) + h]] - zz + 1);
             }
     }
     esc = warp_max(esc);

@@ -318,7 +318,7 @@ struct Loop {
 // Timing diagnostics (ADPB200_DEBUG & 4): per CTA, clock64 cycles of the MMA
 // warp in total / waiting for TMEM to drain / waiting for a full stage, and of
 // the first epilogue warp holding TMEM (tmem_full seen -> tmem_empty arrive).
-__device__ unsigned long long g_dbg[1024 * 4];
+__device__ unsigned long long g_dbg[1024 * 5];
 
 // The MMA role, converged warp; SCHED = compile-time (S, L) or runtime smem.
 template <int NB, int S, int L>
@@ -328,7 +328,7 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
     int stage = 0;
     uint32_t phase = 0, acc_phase = 0;
     const bool timing = (debug & 4) != 0;
-    unsigned long long t_start = timing ? clock64() : 0ull, w_tmem = 0, w_full = 0;
+    unsigned long long t_start = timing ? clock64() : 0ull, w_tmem = 0, w_full = 0, w_head = 0;
     for (int64_t tile = blockIdx.x; tile < lp.ntiles; tile += gridDim.x) {
         for (int c = 0; c < lp.nchunks; ++c) {
             unsigned long long t0 = timing ? clock64() : 0ull;
@@ -340,7 +340,11 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
             for (int64_t kb = kb0; kb < kb1; ++kb) {
                 if (timing) t0 = clock64();
                 tc::mbar_wait(&hdr->full[stage], phase);
-                if (timing) w_full += clock64() - t0;
+                if (timing) {
+                    const unsigned long long dt = clock64() - t0;
+                    w_full += dt;
+                    if (kb - kb0 < 8) w_head += dt;  // the first 8 k-blocks after a TMEM wait
+                }
                 tc::fence_after();
                 const uint32_t sa = stage0 + uint32_t(stage) * lp.stage_bytes;
                 const uint32_t sb = sa + lp.a_bytes;
@@ -389,6 +393,7 @@ __device__ __forceinline__ void mma_role(const Loop& lp, SmemHeader* hdr, const 
         g_dbg[blockIdx.x * 4 + 0] = clock64() - t_start;
         g_dbg[blockIdx.x * 4 + 1] = w_tmem;
         g_dbg[blockIdx.x * 4 + 2] = w_full;
+        g_dbg[4096 + blockIdx.x] = w_head;
     }
 }
 
@@ -847,20 +852,21 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     ++*nlaunch;
     if (debug & 4) {
         // diagnostics only: synchronise and summarise the per-CTA cycle counters
-        unsigned long long h[1024 * 4];
+        static unsigned long long h[1024 * 5];
         cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(h, g_dbg, sizeof(unsigned long long) * 4 * size_t(grid));
-        double t = 0, wt = 0, wf = 0, ho = 0;
+        cudaMemcpyFromSymbol(h, g_dbg, sizeof(h));
+        double t = 0, wt = 0, wf = 0, ho = 0, wh = 0;
         for (int b = 0; b < grid; ++b) {
             t += double(h[b * 4]);
             wt += double(h[b * 4 + 1]);
             wf += double(h[b * 4 + 2]);
             ho += double(h[b * 4 + 3]);
+            wh += double(h[4096 + b]);
         }
         fprintf(stderr,
-                "igemm<%d> debug: mma warp %.0f cycles/CTA, waiting tmem %.1f%%, waiting full stage %.1f%%, "
-                "epilogue holds tmem %.1f%%\n",
-                nb, t / grid, 100.0 * wt / t, 100.0 * wf / t, 100.0 * ho / t);
+                "igemm<%d> debug: mma warp %.0f cycles/CTA, waiting tmem %.1f%%, waiting full stage %.1f%% "
+                "(%.1f%% in the first 8 k-blocks of a tile/chunk), epilogue holds tmem %.1f%%\n",
+                nb, t / grid, 100.0 * wt / t, 100.0 * wf / t, 100.0 * wh / t, 100.0 * ho / t);
     }
     return 0;
 }

@@ -27,4 +27,6 @@ for _ in range(10):
 st = h.profile_read()
 print(json.dumps({"debug": os.environ.get("ADPB200_DEBUG", "0"), "n": n,
                   "gemm_ms": sorted(c["gemm"] for c in st)[len(st) // 2],
-                  "slice_ms": sorted(c["slice"] for c in st)[len(st) // 2]}))
+                  "slice_ms": sorted(c["slice"] for c in st)[len(st) // 2],
+                  "esc_ms": sorted(c["esc"] for c in st)[len(st) // 2],
+                  "stats_ms": sorted(c["stats"] for c in st)[len(st) // 2]}))
