@@ -133,9 +133,9 @@ def reference_arm(args):
     orc = Oracle(kind)
     cores = os.cpu_count() or 1
     rs, cs, k = 256, 2048, args.size  # a 256 x 2048 block of C, full k: same decision path (min dim 256)
-    rng = np.random.default_rng(1)
-    a = rng.uniform(1.0, 2.0, (rs, k))
-    b = rng.uniform(1.0, 2.0, (k, cs))
+    # the reference's own generator (gen_uniform_rect, xoshiro256++), U(1,2), seeds 1 and 2
+    a = orc.gen_uniform_rect(rs, k, 1, 1.0, 2.0)
+    b = orc.gen_uniform_rect(k, cs, 2, 1.0, 2.0)
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -152,7 +152,7 @@ def reference_arm(args):
         "impl": "reference", "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, 8192^3",
         "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic U(1,2)",
+        "dtype": "f64", "data": "synthetic U(1,2): the reference's gen_uniform_rect (xoshiro256++) seeds 1, 2",
         "config": {"workload": f"reference adp_gemm (CPU, OpenMP) on a {rs}x{cs}x{k} block of the "
                                f"{args.size}^3 ADP DGEMM", "sample_m": rs, "sample_n": cs, "k": k},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
