@@ -124,9 +124,15 @@ int adpb200_adp_gemm(adpb200_handle handle, int64_t m, int64_t n, int64_t k, dou
                      void* stream);
 
 /* Host-buffer variants (A, B, C, trace in HOST memory; page-locked buffers
- * recommended): copy the operands in, run the pipeline, copy C out while the
- * slice GEMM still computes (row chunks), return when C is on the host. The
- * end-to-end path the reference's value-returning adp_gemm corresponds to. */
+ * recommended): the end-to-end path the reference's value-returning adp_gemm
+ * corresponds to; returns when C is on the host. The PCIe transfer overlaps
+ * the computation: op(A) goes first, op(B) follows in column chunks on a
+ * second stream, and each chunk's exponent stats, ESC contribution, slicing
+ * and GEMM columns run as soon as it lands with a speculated slice count (the
+ * handle's last decision), its C columns going straight back. The real ADP
+ * decision is still made on the device from all the data; when it differs
+ * from the speculation the predicated stages recompute C. Results are bitwise
+ * those of adpb200_dgemm / adpb200_adp_gemm on device copies. */
 int adpb200_dgemm_host(adpb200_handle handle, char transa, char transb, int64_t m, int64_t n, int64_t k,
                        double alpha, const double* A, int64_t lda, const double* B, int64_t ldb,
                        double beta, double* C, int64_t ldc, const adpb200_options* opt,

@@ -23,6 +23,7 @@ using namespace adpb200;
 // Stage timing (adpb200_profile_*): CUDA events recorded on the caller's
 // stream around each pipeline stage, read back on request.
 constexpr int kStages = ADPB200_PROFILE_STAGES;
+constexpr int kMaxStreamChunks = 8;  // column chunks of B streamed over PCIe while the GEMM runs
 
 struct adpb200_context {
     int device = 0;
@@ -38,6 +39,12 @@ struct adpb200_context {
     cudaStream_t d2h = nullptr;
     cudaEvent_t chunk_ev[16] = {};
     int chunk_next = 0;
+    // streamed host path: H2D stream, per-chunk events, pinned plan read-back and
+    // the slice count speculated for the next call (the last decided one)
+    cudaStream_t h2d = nullptr;
+    cudaEvent_t h2d_ev[kMaxStreamChunks + 2] = {};
+    Plan* host_plan = nullptr;
+    int spec_s = 7;
 };
 
 namespace {
@@ -439,6 +446,144 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     return cuda_check(cudaGetLastError(), "dist phase 4");
 }
 
+__global__ void spec_fixup_kernel(Plan* plan, const Plan* spec) {
+    // the decided plan matches the speculation: every predicated stage after this
+    // point has nothing to do (slicing, GEMM and fallback all check the path)
+    if (plan->path == ADPB200_PATH_EMULATED && plan->slices == spec->slices && plan->L == spec->L &&
+        plan->variant == spec->variant)
+        plan->path = kPathDone;
+}
+
+// Host-buffer path with the PCIe transfer overlapped: the internal A (all of
+// it: ESC needs every row) goes first, then B in column chunks on a second
+// stream; each chunk's stats, ESC contribution, slicing and GEMM n-tiles run
+// as soon as it lands, with a SPECULATED slice count (the handle's last
+// decision, or the forced one), and its C columns go back over PCIe at once.
+// When every chunk is done the real decision is made on the device exactly as
+// in run_pipeline; if it differs from the speculation (other s, exceptional
+// values, size/cost gates) the predicated slicing / GEMM / fallback recompute C
+// with the real plan and C is copied again. One host read of the decided plan
+// per call (the call returns with C on the host anyway). Results are those of
+// run_pipeline bit for bit: the speculation only decides what runs early.
+// copy_b(c0, c1, stream) copies internal B lines [c0, c1) to the device;
+// copy_c(c0, c1) enqueues the D2H of internal C columns [c0, c1) on h->d2h.
+template <class CopyB, class CopyC>
+int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* tdev, cudaStream_t st,
+                 cudaEvent_t a_ready, CopyB copy_b, CopyC copy_c, bool* streamed) {
+    *streamed = false;
+    if (o.mode == ADPB200_MODE_NATIVE || P.M == 0 || P.K == 0) return ADPB200_OK;
+    const int cap = plane_cap(o, 0, 0);
+    const int s_spec = o.mode == ADPB200_MODE_EMULATE ? o.forced_slices : std::min(h->spec_s, o.max_slices);
+    Plan hp{};
+    fill_emulation_plan(hp, s_spec, o.pair_limit, P.K);
+    const int nb = hp.variant;
+    if (hp.nsl > cap || nb == 0 || P.N < 2 * int64_t(nb) * 4) return ADPB200_OK;
+    int64_t chunk = (P.N + kMaxStreamChunks - 1) / kMaxStreamChunks;
+    chunk = (chunk + nb - 1) / nb * nb;
+    const int nchunks = int((P.N + chunk - 1) / chunk);
+    *streamed = true;
+
+    const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
+    int rc = ensure_ws(h, Lw.total, st);
+    if (rc) return rc;
+    uint64_t* nl = &h->launches;
+    Plan* plan = at<Plan>(h, Lw.plan);
+    Plan* spec = at<Plan>(h, Lw.scratch);
+    int32_t* amax = at<int32_t>(h, Lw.stats_a_max);
+    int32_t* amin = at<int32_t>(h, Lw.stats_a_min);
+    int32_t* aline = at<int32_t>(h, Lw.line_a);
+    int32_t* bmax = at<int32_t>(h, Lw.stats_b_max);
+    int32_t* bmin = at<int32_t>(h, Lw.stats_b_min);
+    int32_t* bline = at<int32_t>(h, Lw.line_b);
+    int8_t* pa = at<int8_t>(h, Lw.planes_a);
+    int8_t* pb = at<int8_t>(h, Lw.planes_b);
+    int32_t* sa = at<int32_t>(h, Lw.scale_a);
+    int32_t* sb = at<int32_t>(h, Lw.scale_b);
+    const int64_t t = Lw.blocks;
+    const int64_t mn = std::min(std::min(P.tm, P.tn), P.tk);
+    const bool esc_expected = (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
+                              mn >= o.min_dim;
+    // B chunks on the H2D stream, after A (a_ready) and after everything earlier on st
+    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1];
+    rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
+    if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent");
+    if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->h2d, a_ready, 0), "cudaStreamWaitEvent");
+    for (int c = 0; c < nchunks && !rc; ++c) {
+        const int64_t c0 = c * chunk, c1 = std::min(P.N, c0 + chunk);
+        rc = copy_b(c0, c1, h->h2d);
+        if (!rc) rc = cuda_check(cudaEventRecord(h->h2d_ev[c], h->h2d), "cudaEventRecord(h2d)");
+    }
+    if (rc) return rc;
+    // A: stats, speculative plan, slicing
+    rc = cuda_check(cudaMemsetAsync(plan, 0, sizeof(Plan), st), "cudaMemsetAsync(plan)");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(spec, 0, sizeof(Plan), st), "cudaMemsetAsync(spec)");
+    if (!rc) rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent(A)");
+    if (rc) return rc;
+    launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
+    launch_set_plan(spec, s_spec, o.pair_limit, P.K, st, nl);
+    launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, spec, 0, cap, st, nl);
+    GemmArgs g{};
+    g.plan = spec;
+    g.M = P.M;
+    g.N = P.N;
+    g.K = P.K;
+    g.scale_a = sa;
+    g.scale_b = sb;
+    g.alpha = P.alpha;
+    g.beta = P.beta;
+    g.c_out = P.c_out;
+    g.ldc = P.ldc;
+    g.c_in = P.c_in;
+    g.ldc_in = P.ldc_in;
+    g.partial = at<uint64_t>(h, Lw.partial);
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t c0 = c * chunk, c1 = std::min(P.N, c0 + chunk), lines = c1 - c0;
+        rc = cuda_check(cudaStreamWaitEvent(st, h->h2d_ev[c], 0), "cudaStreamWaitEvent(B chunk)");
+        if (rc) return rc;
+        const LineView bv{P.b.ptr + c0 * P.b.ls, lines, P.K, P.b.ls, P.b.ps};
+        // chunk stats: block-major records of `lines` lines at offset c0 (line maxima stay contiguous)
+        launch_stats(bv, o.esc_block_len, bmax + c0 * t, bmin + c0 * t, bline + c0, plan->counts + 3, &plan->exc, 2, 1,
+                     st, nl);
+        if (esc_expected)
+            launch_esc(amax, amin, aline, bmax + c0 * t, bmin + c0 * t, bline + c0, P.M, lines, t, plan, &plan->esc_raw,
+                       &plan->esc_ran, st, nl);
+        launch_slice(bv, bline + c0, pb + c0 * 32, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb + c0, spec, 0, cap, st, nl);
+        g.nt_begin = c0 / nb;
+        g.nt_end = (c1 + nb - 1) / nb;
+        if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
+            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+        cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
+        rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
+        if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
+        if (!rc) rc = copy_c(c0, c1);
+        if (rc) return rc;
+    }
+    // the real decision (the trace is written here), then compare with the speculation
+    launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, P.swap_ab, tdev, st, nl);
+    spec_fixup_kernel<<<1, 1, 0, st>>>(plan, spec);
+    ++*nl;
+    rc = cuda_check(cudaMemcpyAsync(h->host_plan, plan, sizeof(Plan), cudaMemcpyDeviceToHost, st), "D2H plan");
+    if (!rc) rc = cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (rc) return rc;
+    const Plan hp2 = *h->host_plan;
+    if (hp2.path == kPathDone || hp2.path == ADPB200_PATH_EMULATED) h->spec_s = hp2.slices;
+    if (hp2.path == kPathDone) return ADPB200_OK;
+    // speculation missed: recompute with the decided plan (predicated kernels)
+    g.plan = plan;
+    g.nt_begin = g.nt_end = 0;
+    launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, plan, 0, cap, st, nl);
+    launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, 0, cap, st, nl);
+    for (int v : {64, 48, 32, 16, 8})
+        if (launch_igemm(v, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
+            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+    launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+    cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
+    rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
+    if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
+    if (!rc) rc = copy_c(0, P.N);
+    return rc ? rc : cuda_check(cudaGetLastError(), "kernel launch");
+}
+
 // Row-major product out = alpha*A*B + beta*c_in (MatrixF64 layout) expressed
 // in the internal orientation by the exact operand swap C^T = B^T A^T:
 // internal A-lines = columns of B, B-lines = rows of A, out(i,j) = C[j][i].
@@ -533,6 +678,13 @@ int adpb200_destroy(adpb200_handle h) {
             if (e) cudaEventDestroy(e);
         cudaStreamDestroy(h->d2h);
     }
+    if (h->h2d) {
+        cudaStreamSynchronize(h->h2d);
+        for (auto& e : h->h2d_ev)
+            if (e) cudaEventDestroy(e);
+        cudaStreamDestroy(h->h2d);
+    }
+    if (h->host_plan) cudaFreeHost(h->host_plan);
     if (h->io) {
         cudaDeviceSynchronize();
         cudaFree(h->io);
@@ -793,6 +945,11 @@ int prepare_io(adpb200_context* h, size_t bytes, cudaStream_t st) {
             rc = cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
             if (rc) return rc;
         }
+        rc = cuda_check(cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking), "cudaStreamCreate(h2d)");
+        for (auto& e : h->h2d_ev)
+            if (!rc) rc = cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        if (!rc) rc = cuda_check(cudaMallocHost(&h->host_plan, sizeof(Plan)), "cudaMallocHost(plan)");
+        if (rc) return rc;
     }
     if (h->io_bytes >= bytes) return ADPB200_OK;
     if (h->io) cudaFreeAsync(h->io, st);
@@ -836,17 +993,22 @@ int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, in
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t ta = align_up(sizeof(adpb200_trace), 256), sa = align_up(size_t(arows) * acols * 8, 256),
                  sb = align_up(size_t(brows) * bcols * 8, 256), sc = align_up(size_t(m) * n * 8, 256);
-    rc = prepare_io(h, ta + sa + sb + sc, st);
+    const size_t sc2 = beta != 0.0 ? sc : 0;  // C input kept apart: a missed speculation recomputes from it
+    rc = prepare_io(h, ta + sa + sb + sc + sc2, st);
     if (rc) return rc;
     char* io = static_cast<char*>(h->io);
     adpb200_trace* tdev = reinterpret_cast<adpb200_trace*>(io);
     double* dA = reinterpret_cast<double*>(io + ta);
     double* dB = reinterpret_cast<double*>(io + ta + sa);
     double* dC = reinterpret_cast<double*>(io + ta + sa + sb);
-    // B first: its statistics do not wait for A
-    if ((rc = h2d_block(dB, B, brows, bcols, ldb, st))) return rc;
-    if ((rc = h2d_block(dA, A, arows, acols, lda, st))) return rc;
-    if (beta != 0.0 && (rc = h2d_block(dC, C, m, n, ldc, st))) return rc;
+    double* dCin = beta != 0.0 ? reinterpret_cast<double*>(io + ta + sa + sb + sc) : dC;
+    // A (and C when beta != 0) on the H2D stream, after the work already queued on st
+    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1], a_ready = h->h2d_ev[kMaxStreamChunks];
+    if ((rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord"))) return rc;
+    if ((rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent"))) return rc;
+    if ((rc = h2d_block(dA, A, arows, acols, lda, h->h2d))) return rc;
+    if (beta != 0.0 && (rc = h2d_block(dCin, C, m, n, ldc, h->h2d))) return rc;
+    if ((rc = cuda_check(cudaEventRecord(a_ready, h->h2d), "cudaEventRecord"))) return rc;
     Problem P{};
     P.M = m;
     P.N = n;
@@ -855,16 +1017,40 @@ int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, in
     P.b = is_n(transb) ? LineView{dB, n, k, brows, 1} : LineView{dB, n, k, 1, brows};
     P.alpha = alpha;
     P.beta = beta;
-    P.c_in = dC;
+    P.c_in = dCin;
     P.ldc_in = m;
     P.c_out = dC;
     P.ldc = m;
     P.tm = m;
     P.tn = n;
     P.tk = k;
-    HostOut out{C, ldc};
-    rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &out);
+    // internal B lines [c0, c1) = columns (op N) or rows (op T) of the stored B
+    auto copy_b = [&](int64_t c0, int64_t c1, cudaStream_t s) {
+        if (c1 <= c0) return int(ADPB200_OK);
+        if (is_n(transb))
+            return cuda_check(cudaMemcpy2DAsync(dB + c0 * brows, size_t(brows) * 8, B + c0 * ldb, size_t(ldb) * 8,
+                                                size_t(brows) * 8, size_t(c1 - c0), cudaMemcpyHostToDevice, s),
+                              "cudaMemcpy2DAsync(H2D B chunk)");
+        return cuda_check(cudaMemcpy2DAsync(dB + c0, size_t(brows) * 8, B + c0, size_t(ldb) * 8, size_t(c1 - c0) * 8,
+                                            size_t(bcols), cudaMemcpyHostToDevice, s),
+                          "cudaMemcpy2DAsync(H2D B chunk)");
+    };
+    auto copy_c = [&](int64_t c0, int64_t c1) {
+        if (c1 <= c0 || m == 0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpy2DAsync(C + c0 * ldc, size_t(ldc) * 8, dC + c0 * m, size_t(m) * 8, size_t(m) * 8,
+                                            size_t(c1 - c0), cudaMemcpyDeviceToHost, h->d2h),
+                          "cudaMemcpy2DAsync(D2H C chunk)");
+    };
+    bool streamed = false;
+    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_b, copy_c, &streamed);
     if (rc) return rc;
+    if (!streamed) {
+        if ((rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent"))) return rc;
+        if ((rc = h2d_block(dB, B, brows, bcols, ldb, st))) return rc;
+        HostOut out{C, ldc};
+        rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &out);
+        if (rc) return rc;
+    }
     return finish_host(h, trace, tdev, st);
 }
 
@@ -884,21 +1070,45 @@ int adpb200_adp_gemm_host(adpb200_handle h, int64_t m, int64_t n, int64_t k, dou
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t ta = align_up(sizeof(adpb200_trace), 256), sa = align_up(size_t(m) * k * 8, 256),
                  sb = align_up(size_t(k) * n * 8, 256), sc = align_up(size_t(m) * n * 8, 256);
-    rc = prepare_io(h, ta + sa + sb + sc, st);
+    const size_t sc2 = beta != 0.0 ? sc : 0;
+    rc = prepare_io(h, ta + sa + sb + sc + sc2, st);
     if (rc) return rc;
     char* io = static_cast<char*>(h->io);
     adpb200_trace* tdev = reinterpret_cast<adpb200_trace*>(io);
     double* dA = reinterpret_cast<double*>(io + ta);
     double* dB = reinterpret_cast<double*>(io + ta + sa);
     double* dC = reinterpret_cast<double*>(io + ta + sa + sb);
-    // row-major buffers are column-major transposes: copy them as such
-    if ((rc = h2d_block(dB, B, n, k, n, st))) return rc;
-    if ((rc = h2d_block(dA, A, k, m, k, st))) return rc;
-    if (beta != 0.0 && (rc = h2d_block(dC, c_in, n, m, n, st))) return rc;
-    Problem P = rowmajor_problem(m, n, k, alpha, dA, dB, beta, dC, dC);
-    HostOut hout{out, n};
-    rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &hout);
+    double* dCin = beta != 0.0 ? reinterpret_cast<double*>(io + ta + sa + sb + sc) : dC;
+    // internally C^T = B^T A^T: the internal A is the user's B (all of it first),
+    // the internal B-lines are the user's rows of A (streamed in row chunks)
+    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1], a_ready = h->h2d_ev[kMaxStreamChunks];
+    if ((rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord"))) return rc;
+    if ((rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent"))) return rc;
+    if ((rc = h2d_block(dB, B, n, k, n, h->h2d))) return rc;
+    if (beta != 0.0 && (rc = h2d_block(dCin, c_in, n, m, n, h->h2d))) return rc;
+    if ((rc = cuda_check(cudaEventRecord(a_ready, h->h2d), "cudaEventRecord"))) return rc;
+    Problem P = rowmajor_problem(m, n, k, alpha, dA, dB, beta, dCin, dC);
+    auto copy_b = [&](int64_t c0, int64_t c1, cudaStream_t s) {
+        if (c1 <= c0 || k == 0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpyAsync(dA + c0 * k, A + c0 * k, size_t(c1 - c0) * k * 8, cudaMemcpyHostToDevice, s),
+                          "cudaMemcpyAsync(H2D A rows)");
+    };
+    auto copy_c = [&](int64_t c0, int64_t c1) {
+        if (c1 <= c0 || n == 0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpyAsync(out + c0 * n, dC + c0 * n, size_t(c1 - c0) * n * 8, cudaMemcpyDeviceToHost,
+                                          h->d2h),
+                          "cudaMemcpyAsync(D2H C rows)");
+    };
+    bool streamed = false;
+    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_b, copy_c, &streamed);
     if (rc) return rc;
+    if (!streamed) {
+        if ((rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent"))) return rc;
+        if ((rc = h2d_block(dA, A, k, m, k, st))) return rc;
+        HostOut hout{out, n};
+        rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &hout);
+        if (rc) return rc;
+    }
     return finish_host(h, trace, tdev, st);
 }
 

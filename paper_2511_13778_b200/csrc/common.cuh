@@ -21,6 +21,10 @@ struct LineView {
     int64_t ls, ps;
 };
 
+// Internal path value (never reported): the work of the plan is already done
+// (the streamed host path's speculation matched the decision).
+constexpr int32_t kPathDone = 7;
+
 // Device-resident plan: filled by the guardrail kernels and the decision
 // kernel, read by every later kernel (no host round trip).
 struct Plan {

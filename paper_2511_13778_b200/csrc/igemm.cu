@@ -443,7 +443,11 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
     const int64_t mt_end = g.mt_end > 0 && g.mt_end < mt_total ? g.mt_end : mt_total;
     const int64_t mt_off = g.mt_begin;
     lp.tiles_m = mt_end > mt_off ? mt_end - mt_off : 0;
-    lp.tiles_n = (g.N + NB - 1) / NB;
+    // n-tile range [nt_begin, nt_end) (column chunks of the streamed host path; nt_end 0 = all)
+    const int64_t nt_total = (g.N + NB - 1) / NB;
+    const int64_t nt_end = g.nt_end > 0 && g.nt_end < nt_total ? g.nt_end : nt_total;
+    const int64_t nt_off = g.nt_begin;
+    lp.tiles_n = nt_end > nt_off ? nt_end - nt_off : 0;
     lp.ntiles = lp.tiles_m * lp.tiles_n;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -492,6 +496,7 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
             int64_t mt, nt;
             tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
             mt += mt_off;
+            nt += nt_off;
             for (int64_t kb = 0; kb < lp.nkb; ++kb) {
                 tc::mbar_wait(&hdr->empty[stage], phase ^ 1);
                 if (elect_one()) {
@@ -536,6 +541,7 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
             int64_t mt, nt;
             tile_coords(tile, lp.tiles_m, lp.tiles_n, mt, nt);
             mt += mt_off;
+            nt += nt_off;
             const int64_t row = mt * kBM + q * 32 + lane;
             const bool row_ok = row < g.M;
             const int ea = row_ok ? g.scale_a[row] : 0;
@@ -815,7 +821,9 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     }
     const int64_t mt_total = (g.M + kBM - 1) / kBM;
     const int64_t mt_end = g.mt_end > 0 && g.mt_end < mt_total ? g.mt_end : mt_total;
-    const int64_t tiles = (mt_end - g.mt_begin) * ((g.N + nb - 1) / nb);
+    const int64_t nt_total = (g.N + nb - 1) / nb;
+    const int64_t nt_end = g.nt_end > 0 && g.nt_end < nt_total ? g.nt_end : nt_total;
+    const int64_t tiles = (mt_end - g.mt_begin) * (nt_end - g.nt_begin);
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
     GemmArgs a = g;

@@ -28,6 +28,7 @@ struct GemmArgs {
     int smem_bytes;
     int debug;  // timing diagnostics only (ADPB200_DEBUG): 1 skip MMAs, 2 skip epilogue math
     int64_t mt_begin, mt_end;  // 128-row m-tile range to compute (mt_end 0 = all)
+    int64_t nt_begin, nt_end;  // NB-column n-tile range to compute (nt_end 0 = all)
 };
 
 // nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.
