@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmax_out,
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit, int transposed) {
+                                                         int exc_bit, int transposed, int64_t tstride) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
         bmin = warp_min(bmin);
         if (lane == 0) {
             bool any = bmax != kNegSentinel;
-            const int64_t o = transposed ? blk * v.lines + line : task;
+            const int64_t o = transposed ? blk * tstride + line : task;
             bmax_out[o] = any ? bmax : kNegSentinel;
             bmin_out[o] = any ? bmin : kNegSentinel;
         }
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmax_out,
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit, int transposed) {
+                                                         int exc_bit, int transposed, int64_t tstride) {
     int nan = 0, inf = 0, negz = 0;
     const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     for (int64_t blk = blockIdx.y; blk < blocks; blk += gridDim.y) {
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                 }
             }
             bool any = bmax != kNegSentinel;
-            const int64_t o = transposed ? blk * v.lines + line : line * blocks + blk;
+            const int64_t o = transposed ? blk * tstride + line : line * blocks + blk;
             bmax_out[o] = any ? bmax : kNegSentinel;
             bmin_out[o] = any ? bmin : kNegSentinel;
         }
@@ -171,12 +171,12 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
 
 // line_max[line] = max over the line's block maxima (sentinel is the minimum,
 // so all-zero blocks drop out and all-zero lines stay sentinel).
-__global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lines, int64_t blocks,
+__global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lines, int64_t blocks, int64_t stride,
                                   int32_t* __restrict__ line_max) {
     const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (line >= lines) return;
     int mx = kNegSentinel;
-    for (int64_t b = 0; b < blocks; ++b) mx = max(mx, bmaxT[b * lines + line]);
+    for (int64_t b = 0; b < blocks; ++b) mx = max(mx, bmaxT[b * stride + line]);
     line_max[line] = mx;
 }
 
@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
                                                   const int32_t* __restrict__ bmaxT,
                                                   const int32_t* __restrict__ bminT,
                                                   const int32_t* __restrict__ bline, int64_t m, int64_t n,
-                                                  int64_t t, int64_t nr, int64_t rec, const Plan* plan,
-                                                  int32_t* esc_out, int32_t* ran_flag) {
+                                                  int64_t t, int64_t nr, int64_t rec, int64_t astride,
+                                                  const Plan* plan, int32_t* esc_out, int32_t* ran_flag) {
     if (plan && plan->exc) return;  // exceptional inputs never reach the ESC (adp.cpp:58-62)
     // A words hold (a, a); B words hold (b_j, b_j+1) for the thread's j pairs
     __shared__ __align__(16) uint32_t sAmx[kEscTB][kEscBI];
@@ -261,8 +261,8 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
             const int ii = idx % kEscBI, tt = idx / kEscBI;
             const int64_t gi = i0 + ii, gt = tb + tt;
             const bool ok = gi < m && gt < t;
-            const int vx = ok ? to16(amaxT[gt * m + gi]) : kS16;
-            const int vn = ok ? to16(aminT[gt * m + gi]) : kS16;
+            const int vx = ok ? to16(amaxT[gt * astride + gi]) : kS16;
+            const int vn = ok ? to16(aminT[gt * astride + gi]) : kS16;
             sAmx[tt][ii] = pack2(vx, vx);
             sAmn[tt][ii] = pack2(vn, vn);
         }
@@ -412,8 +412,9 @@ int num_sms() {
 
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
-                  uint64_t* nlaunch) {
+                  uint64_t* nlaunch, int64_t tstride) {
     const int64_t blocks = v.len == 0 ? 0 : (v.len + block_len - 1) / block_len;
+    if (tstride <= 0) tstride = v.lines;
     if (v.lines == 0) return;
     if (blocks > 0) {
         if (v.ps == 1 || v.lines == 1) {
@@ -425,16 +426,17 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
             if (grid < 1) grid = 1;
             // lines of a single row-major line: ps may be anything when len == 1
             stats_rows_kernel<<<grid, 256, 0, st>>>(w, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit, transposed);
+                                                    exc_bit, transposed, tstride);
         } else {
             dim3 grid((unsigned)((v.lines + 255) / 256), (unsigned)(blocks < 65535 ? blocks : 65535));
             stats_cols_kernel<<<grid, 256, 0, st>>>(v, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit, transposed);
+                                                    exc_bit, transposed, tstride);
         }
         ++*nlaunch;
     }
     if (transposed) {
-        line_max_t_kernel<<<(unsigned)((v.lines + 255) / 256), 256, 0, st>>>(bmax, v.lines, blocks, line_max);
+        line_max_t_kernel<<<(unsigned)((v.lines + 255) / 256), 256, 0, st>>>(bmax, v.lines, blocks, tstride,
+                                                                               line_max);
     } else {
         int lgrid = (int)((v.lines * 32 + 255) / 256);
         line_max_kernel<<<lgrid, 256, 0, st>>>(bmax, v.lines, blocks, line_max);
@@ -454,12 +456,13 @@ void launch_scan(const double* a, int64_t count, unsigned long long* counts, int
 void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
                 const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
                 int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch, int64_t b_nr,
-                int64_t b_rec) {
+                int64_t b_rec, int64_t a_stride) {
     if (m == 0 || n == 0) return;
     if (b_nr <= 0) b_nr = n;
+    if (a_stride <= 0) a_stride = m;
     dim3 grid((unsigned)((n + kEscBJ - 1) / kEscBJ), (unsigned)((m + kEscBI - 1) / kEscBI));
-    esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, plan, esc_out,
-                                     ran_flag);
+    esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, a_stride, plan,
+                                     esc_out, ran_flag);
     ++*nlaunch;
 }
 

@@ -8,19 +8,22 @@ int num_sms();
 // K1: fused Inf/NaN/-0 counts + per-(line, block) exponent max/min + line max.
 // transposed = 1 stores the block stats block-major ([block][line], what the
 // ESC kernel consumes); 0 the reference's line-major [line][block].
+// tstride: line stride of the transposed layout (0 = v.lines), so a range of lines
+// can write into a larger block-major array.
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
-                  uint64_t* nlaunch);
+                  uint64_t* nlaunch, int64_t tstride = 0);
 void launch_scan(const double* a, int64_t count, unsigned long long* counts, int32_t* exc, cudaStream_t st,
                  uint64_t* nlaunch);
 // K2: coarsened ESC over block-major stats (atomicMax into esc_out, which must start at 0).
 // B stats may come as column slabs of b_nr lines, slab r's record starting at
 // r * b_rec int32 (bmax/bmin/bline pointers at their offsets inside record 0);
-// b_nr = 0: one slab of all n lines.
+// b_nr = 0: one slab of all n lines. a_stride: line stride of the A stats (0 = m),
+// so a range of A-lines of a larger block-major array can be passed.
 void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, const int32_t* bmax,
                 const int32_t* bmin, const int32_t* bline, int64_t m, int64_t n, int64_t t, const Plan* plan,
                 int32_t* esc_out, int32_t* ran_flag, cudaStream_t st, uint64_t* nlaunch, int64_t b_nr = 0,
-                int64_t b_rec = 0);
+                int64_t b_rec = 0, int64_t a_stride = 0);
 
 // Multi-GPU B-distributed path: copy all-gathered slab records
 // ([scale int32 x nr | pad to hdr][nsl planes of nkb x nr x 32 B]) into the
