@@ -173,6 +173,13 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
  *              nsl = 0 (native fallback): all-gather the FP64 B slabs (= B)
  *   phase 4  gathered records -> the GEMM's plane layout, tcgen05 GEMM of the
  *            local rows (or the native GEMM against the gathered B).
+ * Overlapped alternative to phase 4 (the plane all-gather runs while the GEMM
+ * tiles that need only this rank's own B columns compute):
+ *   phase 5  gathered = this rank's own slab record (`slab`): place it and run
+ *            the GEMM n-tiles inside columns [rank*n/world, (rank+1)*n/world)
+ *            (no-op when nsl = 0) — issue it, then wait for the all-gather;
+ *   phase 6  gathered = all records: place them and run every other n-tile
+ *            (or, when nsl = 0, the native GEMM against the gathered B).
  * Same decision and slice count on every rank: the assembled C is
  * bit-identical to the single-GPU adpb200_dgemm('N'/transa, 'N'). */
 int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]);
@@ -180,7 +187,7 @@ int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* o
  * gather; 0 on the native path), GEMM variant. */
 int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global,
                           int64_t n, int64_t k, int32_t out[4]);
-int adpb200_dgemm_dist(adpb200_handle handle, int phase, int64_t m_global, int world, char transa,
+int adpb200_dgemm_dist(adpb200_handle handle, int phase, int64_t m_global, int world, int rank, char transa,
                        int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                        const double* B_slab, double beta, double* C, int64_t ldc,
                        const adpb200_options* opt, adpb200_trace* trace, int32_t* bstats_local,

@@ -105,8 +105,8 @@ def lib() -> C.CDLL:
         "adpb200_native_gemm": (C.c_int, [vp, vp, vp, i64, i64, i64, f64, f64, vp, vp, vp]),
         "adpb200_dist_sizes": (C.c_int, [i64, i64, C.c_int, popt, C.POINTER(i64)]),
         "adpb200_dist_decision": (C.c_int, [popt, C.POINTER(i32), i64, i64, i64, C.POINTER(i32)]),
-        "adpb200_dgemm_dist": (C.c_int, [vp, C.c_int, i64, C.c_int, C.c_char, i64, i64, i64, f64, vp, i64, vp, f64,
-                                         vp, i64, popt, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
+        "adpb200_dgemm_dist": (C.c_int, [vp, C.c_int, i64, C.c_int, C.c_int, C.c_char, i64, i64, i64, f64, vp, i64,
+                                         vp, f64, vp, i64, popt, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
         "adpb200_geqrf_blocked": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, popt, vp]),
         "adpb200_qr_materialize_q": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "adpb200_qr_residual": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),

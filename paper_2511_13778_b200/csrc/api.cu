@@ -339,7 +339,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
 //                                                                       (or B itself on fallback)
 //   4  gathered records -> global B planes + scales ; tcgen05 GEMM   (or native GEMM)
 struct DistIO {
-    int world;
+    int world, rank;
     int64_t nr;              // B columns per rank
     int32_t* bstats_local;   // [bmax t x nr][bmin t x nr][bline nr]
     const int32_t* bstats_all;
@@ -407,7 +407,66 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
         }
         return cuda_check(cudaGetLastError(), "dist phase 3");
     }
-    // phase 4
+    // phases 5 / 6: phase 4 split so the plane all-gather overlaps the GEMM of the
+    // tiles that only need this rank's own B columns (phase 5, `gathered` = own slab
+    // record), the other tiles follow once the records are in (phase 6)
+    if (phase >= 4 && P.M == 0) return ADPB200_OK;  // no rows on this rank: nothing to compute
+    if ((phase == 5 || phase == 6) && io.nsl > 0) {
+        int8_t* pa = at<int8_t>(h, Lw.planes_a);
+        int8_t* pb = at<int8_t>(h, Lw.planes_b);
+        int32_t* sb = at<int32_t>(h, Lw.scale_b);
+        const int64_t nkb = Lw.pitch / 32;
+        const int64_t rec_bytes = slab_hdr(nr) + int64_t(io.nsl) * nkb * nr * 32;
+        tm.begin(3);
+        if (phase == 5)
+            launch_gather_planes(static_cast<const int8_t*>(io.gathered), rec_bytes, slab_hdr(nr), 1, nr, nkb, io.nsl,
+                                 pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb, st, nl, io.rank);
+        else
+            launch_gather_planes(static_cast<const int8_t*>(io.gathered), rec_bytes, slab_hdr(nr), io.world, nr, nkb,
+                                 io.nsl, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb, st, nl);
+        tm.end(3);
+        GemmArgs g{};
+        g.plan = plan;
+        g.M = P.M;
+        g.N = P.N;
+        g.K = P.K;
+        g.scale_a = at<int32_t>(h, Lw.scale_a);
+        g.scale_b = sb;
+        g.alpha = P.alpha;
+        g.beta = P.beta;
+        g.c_out = P.c_out;
+        g.ldc = P.ldc;
+        g.c_in = P.c_in;
+        g.ldc_in = P.ldc_in;
+        g.partial = at<uint64_t>(h, Lw.partial);
+        tm.begin(4);
+        for (int nb : {64, 48, 32, 16, 8}) {
+            // n-tiles entirely inside this rank's columns [rank*nr, (rank+1)*nr)
+            const int64_t own_b = (int64_t(io.rank) * nr + nb - 1) / nb;
+            const int64_t own_e = std::max(own_b, (int64_t(io.rank) + 1) * nr / nb);
+            const int64_t nt_total = (P.N + nb - 1) / nb;
+            int64_t ranges[2][2] = {{own_b, own_e}, {0, 0}};
+            int nrange = 1;
+            if (phase == 6) {  // everything phase 5 did not compute
+                ranges[0][0] = 0;
+                ranges[0][1] = own_b;
+                ranges[1][0] = own_e;
+                ranges[1][1] = nt_total;
+                nrange = 2;
+            }
+            for (int q = 0; q < nrange; ++q) {
+                if (ranges[q][1] <= ranges[q][0]) continue;
+                g.nt_begin = ranges[q][0];
+                g.nt_end = ranges[q][1];
+                if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, nkb, cap, g, st, nl))
+                    return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+            }
+        }
+        tm.end(4);
+        return cuda_check(cudaGetLastError(), "dist phase 5/6");
+    }
+    if (phase == 5) return ADPB200_OK;  // native fallback: nothing local to do
+    // phase 4 (or 6 on the native fallback)
     if (io.nsl > 0) {
         int8_t* pa = at<int8_t>(h, Lw.planes_a);
         int8_t* pb = at<int8_t>(h, Lw.planes_b);
@@ -868,13 +927,15 @@ int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int
     return ADPB200_OK;
 }
 
-int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world, char transa, int64_t m, int64_t n,
+int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world, int rank, char transa, int64_t m,
+                       int64_t n,
                        int64_t k, double alpha, const double* A, int64_t lda, const double* B_slab, double beta,
                        double* C, int64_t ldc, const adpb200_options* opt, adpb200_trace* trace,
                        int32_t* bstats_local, const int32_t* bstats_all, int32_t* xchg, int8_t* slab,
                        const void* gathered, int nsl, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_dist: null handle");
-    if (phase < 1 || phase > 4) return fail(3, "dgemm_dist: phase must be 1..4");
+    if (phase < 1 || phase > 6) return fail(3, "dgemm_dist: phase must be 1..6");
+    if (rank < 0 || rank >= world) return fail(3, "dgemm_dist: rank out of range");
     adpb200_options o;
     if (opt) o = *opt;
     else adpb200_default_options(&o);
@@ -888,9 +949,9 @@ int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world,
     if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
     if (beta != 0.0 && !C) return fail(3, "dgemm_dist: beta != 0 needs C");
     if ((phase == 1 && !bstats_local) || (phase == 2 && (!bstats_all || !xchg)) ||
-        (phase == 3 && (!xchg || !slab || !bstats_local)) || (phase == 4 && !gathered))
+        (phase == 3 && (!xchg || !slab || !bstats_local)) || (phase >= 4 && !gathered))
         return fail(3, "dgemm_dist: missing exchange buffer for this phase");
-    if (phase == 4 && (nsl < 0 || nsl > plane_cap(o, 0, 0))) return fail(3, "dgemm_dist: bad nsl");
+    if (phase >= 4 && (nsl < 0 || nsl > plane_cap(o, 0, 0))) return fail(3, "dgemm_dist: bad nsl");
     Problem P{};
     P.M = m;
     P.N = n;
@@ -906,7 +967,7 @@ int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world,
     P.tm = m_global;
     P.tn = n;
     P.tk = k;
-    DistIO io{world, n / world, bstats_local, bstats_all, xchg, slab, gathered, nsl};
+    DistIO io{world, rank, n / world, bstats_local, bstats_all, xchg, slab, gathered, nsl};
     cudaSetDevice(h->device);
     return run_dist(h, P, o, trace, static_cast<cudaStream_t>(stream), phase, io);
 }

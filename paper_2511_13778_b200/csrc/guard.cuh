@@ -28,9 +28,10 @@ void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, 
 // Multi-GPU B-distributed path: copy all-gathered slab records
 // ([scale int32 x nr | pad to hdr][nsl planes of nkb x nr x 32 B]) into the
 // GEMM's blocked plane layout (global line = r * nr + local) and scale_b.
+// (`world` records starting with rank r_first.)
 void launch_gather_planes(const int8_t* recs, int64_t rec_bytes, int64_t hdr, int world, int64_t nr, int64_t nkb,
                           int nsl, int8_t* planes, int64_t slots, int64_t plane_stride, int32_t* scale,
-                          cudaStream_t st, uint64_t* nlaunch);
+                          cudaStream_t st, uint64_t* nlaunch, int r_first = 0);
 void launch_esc_finish(int32_t* out, int target_bits, cudaStream_t st, uint64_t* nlaunch);
 void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int32_t* dst, cudaStream_t st,
                           uint64_t* nlaunch);

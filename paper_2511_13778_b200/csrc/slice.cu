@@ -381,8 +381,8 @@ namespace {
 
 // One 16-byte chunk per thread: (rank, plane, k-block, local line, half).
 __global__ void gather_planes_kernel(const int8_t* __restrict__ recs, int64_t rec_bytes, int64_t hdr, int world,
-                                     int64_t nr, int64_t nkb, int nsl, int8_t* __restrict__ planes, int64_t slots,
-                                     int64_t plane_stride, int32_t* __restrict__ scale) {
+                                     int r_first, int64_t nr, int64_t nkb, int nsl, int8_t* __restrict__ planes,
+                                     int64_t slots, int64_t plane_stride, int32_t* __restrict__ scale) {
     const int64_t per_rank = int64_t(nsl) * nkb * nr * 2;
     const int64_t total = per_rank * world;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
@@ -396,12 +396,13 @@ __global__ void gather_planes_kernel(const int8_t* __restrict__ recs, int64_t re
         const int64_t d = x / nkb;
         const uint4 v = *reinterpret_cast<const uint4*>(recs + r * rec_bytes + hdr + ((d * nkb + kb) * nr + jl) * 32 +
                                                         half * 16);
-        *reinterpret_cast<uint4*>(planes + d * plane_stride + (kb * slots + r * nr + jl) * 32 + half * 16) = v;
+        *reinterpret_cast<uint4*>(planes + d * plane_stride + (kb * slots + (r_first + r) * nr + jl) * 32 + half * 16) =
+            v;
     }
     const int64_t ns = int64_t(world) * nr;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < ns; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / nr;
-        scale[e] = reinterpret_cast<const int32_t*>(recs + r * rec_bytes)[e - r * nr];
+        scale[r_first * nr + e] = reinterpret_cast<const int32_t*>(recs + r * rec_bytes)[e - r * nr];
     }
 }
 
@@ -409,10 +410,10 @@ __global__ void gather_planes_kernel(const int8_t* __restrict__ recs, int64_t re
 
 void launch_gather_planes(const int8_t* recs, int64_t rec_bytes, int64_t hdr, int world, int64_t nr, int64_t nkb,
                           int nsl, int8_t* planes, int64_t slots, int64_t plane_stride, int32_t* scale,
-                          cudaStream_t st, uint64_t* nlaunch) {
+                          cudaStream_t st, uint64_t* nlaunch, int r_first) {
     if (world <= 0 || nr <= 0) return;
-    gather_planes_kernel<<<num_sms() * 8, 256, 0, st>>>(recs, rec_bytes, hdr, world, nr, nkb, nsl, planes, slots,
-                                                        plane_stride, scale);
+    gather_planes_kernel<<<num_sms() * 8, 256, 0, st>>>(recs, rec_bytes, hdr, world, r_first, nr, nkb, nsl, planes,
+                                                        slots, plane_stride, scale);
     ++*nlaunch;
 }
 

@@ -99,13 +99,18 @@ def dist_decision(xchg_host, m_global: int, n: int, k: int, config: Optional[Adp
 def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
                      A: torch.Tensor, lda: int, B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int,
                      config: Optional[AdpConfig] = None, handle: Optional[Handle] = None,
-                     trace: Optional[torch.Tensor] = None):
+                     trace: Optional[torch.Tensor] = None, rank: int = 0, overlap: bool = True):
     """The B-distributed ADP DGEMM of one rank as a generator of collective
     requests, so that the same orchestration runs under torch.distributed
     (dgemm_dist) and under a single-process multi-rank driver (the tests):
 
         ("all_gather", out, inp)   out = concatenation over ranks of inp
+        ("all_gather_async", out, inp)  the same, started without waiting
+        ("wait",)                  wait for the pending asynchronous all-gather
         ("all_reduce_max", t)      t = elementwise max over ranks (in place)
+
+    With overlap (default) the B-plane all-gather runs while the GEMM tiles that
+    need only this rank's own B columns compute (phases 5 and 6).
 
     Rank owns rows of op(A) / C (column-major local block, ldc) and the B
     column slab B_slab (k x n/world column-major, compact: a (n/world, k)
@@ -124,7 +129,7 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     tr = None if trace is None else C.c_void_p(trace.data_ptr())
 
     def phase(p, gathered=None, nsl=0):
-        check(lib().adpb200_dgemm_dist(handle.h, p, m_global, world, transa.encode()[:1], m, n, k, float(alpha),
+        check(lib().adpb200_dgemm_dist(handle.h, p, m_global, world, rank, transa.encode()[:1], m, n, k, float(alpha),
                                        _ptr(A), lda, _ptr(B_slab), float(beta), _ptr(C_), ldc, C.byref(o), tr,
                                        _ptr(bl), _ptr(ba), _ptr(xchg), _ptr(slab), gathered, int(nsl), st))
 
@@ -137,6 +142,12 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     if nsl > 0:
         rec = hdr + nsl * plane_bytes
         gathered = torch.empty(rec * world, dtype=torch.int8, device=dev)
+        if overlap:
+            yield ("all_gather_async", gathered, slab[:rec])
+            phase(5, C.c_void_p(slab.data_ptr()), nsl)     # own columns while the planes travel
+            yield ("wait",)
+            phase(6, C.c_void_p(gathered.data_ptr()), nsl)
+            return (path, s, nsl)
         yield ("all_gather", gathered, slab[:rec])
     else:
         gathered = torch.empty((n, k), dtype=torch.float64, device=dev)  # column-major B, ldb = k
@@ -152,8 +163,9 @@ def dgemm_dist(transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
     column slabs: exponent stats and B slice planes all-gathered, the ADP
     decision input max-allreduced, all over NCCL (torch.distributed)."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
     gen = dgemm_dist_steps(world, transa, m_global, m, n, k, alpha, A, lda, B_slab, beta, C_, ldc, config, handle,
-                           trace)
+                           trace, rank=rank)
     return drive_collectives(gen, world, group)
 
 
@@ -161,16 +173,25 @@ def drive_collectives(gen, world: int, group=None):
     """Run a dgemm_dist_steps-style generator, serving its collective requests
     with torch.distributed (NCCL on GPUs, gloo in the CPU tests). Returns the
     generator's return value."""
+    pending = None
     try:
         req = next(gen)
         while True:
-            if req[0] == "all_gather":
+            if req[0] in ("all_gather", "all_gather_async"):
+                asy = req[0] == "all_gather_async"
                 if world > 1 and dist.get_backend(group) == "gloo":
                     dist.all_gather(list(req[1].view(-1).chunk(world)), req[2].contiguous().view(-1), group=group)
                 elif world > 1:
-                    dist.all_gather_into_tensor(req[1], req[2].contiguous(), group=group)
+                    # async: NCCL's stream waits for the inputs; the caller's stream only waits at "wait"
+                    work = dist.all_gather_into_tensor(req[1], req[2].contiguous(), group=group, async_op=asy)
+                    if asy:
+                        pending = work
                 else:
                     req[1].copy_(req[2].reshape(req[1].shape))
+            elif req[0] == "wait":
+                if pending is not None:
+                    pending.wait()
+                    pending = None
             elif req[0] == "all_reduce_max":
                 reduce_xchg(req[1], group)
             else:

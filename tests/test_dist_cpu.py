@@ -118,7 +118,8 @@ def _collective_worker(rank, world, port, results):
         yield ("all_reduce_max", x)
         slab = torch.full((16,), rank + 1, dtype=torch.int8)
         g = torch.empty(8 * world, dtype=torch.int8)
-        yield ("all_gather", g, slab[:8])
+        yield ("all_gather_async", g, slab[:8])
+        yield ("wait",)
         return ba.tolist(), x.tolist(), g.tolist()
 
     results[rank] = drive_collectives(fake_rank_steps(), world)

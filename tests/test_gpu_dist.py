@@ -21,7 +21,9 @@ def run_virtual(gens):
     while True:
         kind = reqs[0][0]
         assert all(r[0] == kind for r in reqs), "ranks diverged"
-        if kind == "all_gather":
+        if kind == "wait":
+            pass
+        elif kind in ("all_gather", "all_gather_async"):
             cat = torch.cat([r[2].reshape(-1) for r in reqs])
             for r in reqs:
                 r[1].view(-1).copy_(cat)
@@ -41,7 +43,8 @@ def run_virtual(gens):
         reqs = nxt
 
 
-def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3):
+def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3,
+              overlap=True):
     from paper_2511_13778_b200 import Handle
     from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
 
@@ -68,7 +71,7 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
         Cb = Ct[:, r0:r1].contiguous()
         blocks.append(Cb)
         gens.append(dgemm_dist_steps(world, transa, m, mr, n, k, alpha, Ab, lda_r, Bs, beta, Cb, max(mr, 1), cfg,
-                                     Handle(0)))
+                                     Handle(0), rank=r, overlap=overlap))
     res = run_virtual(gens)
     torch.cuda.synchronize()
     assembled = torch.cat(blocks, dim=1)
@@ -84,6 +87,17 @@ def test_dist_bit_identical(gpu, world, m, n, k, policy):
     assert all(r == res[0] for r in res)
     assert path == 0 and s >= 7 and nsl == s
     assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+
+
+@pytest.mark.parametrize("world,n", [(4, 4 * 40), (8, 8 * 24), (2, 2 * 200)])
+def test_dist_overlap_ragged_slabs(gpu, world, n):
+    """Slabs that are not multiples of the GEMM's NB: tiles straddling two ranks'
+    columns are left to phase 6; C still bit-identical, with and without overlap."""
+    for cfg in (gpu.AdpConfig(min_dim=8), gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET)):
+        for overlap in (True, False):
+            got, ref, res = dist_case(gpu, world, 512, n, 640, cfg, overlap=overlap)
+            assert res[0][0] == 0
+            assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
 
 
 def test_dist_transposed_a_and_wide_span(gpu):
