@@ -195,15 +195,12 @@ __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
 template <int S, bool kVec>
 __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t groups, int64_t span) {
     const int64_t tasks = a.v.lines * groups;
-    for (int64_t task = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; task < tasks;
-         task += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t line = task / groups, g = task - line * groups;
-        const int lm = a.line_max[line];
-        const int E = lm == kNegSentinel ? 0 : lm + 2;
-        if (g == 0 && a.scale) a.scale[line] = E;
-        const int64_t p0 = g * 8;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    // the next task's 64 bytes are requested before this task is sliced and
+    // stored: two loads in flight per thread keep HBM busier
+    auto load = [&](int64_t task, uint64_t (&bits)[8]) {
+        const int64_t line = task / groups, p0 = (task - line * groups) * 8;
         const double* lp = a.v.ptr + line * a.v.ls;
-        uint64_t bits[8];
         if (kVec && p0 + 8 <= a.v.len) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -216,11 +213,23 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
             for (int q = 0; q < 8; ++q)
                 bits[q] = p0 + q < a.v.len ? __double_as_longlong(__ldg(lp + p0 + q)) : 0ull;
         }
+    };
+    int64_t task = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    uint64_t cur[8];
+    if (task < tasks) load(task, cur);
+    for (; task < tasks; task += stride) {
+        uint64_t nxt[8];
+        if (task + stride < tasks) load(task + stride, nxt);
+        const int64_t line = task / groups, g = task - line * groups;
+        const int lm = a.line_max[line];
+        const int E = lm == kNegSentinel ? 0 : lm + 2;
+        if (g == 0 && a.scale) a.scale[line] = E;
+        const int64_t p0 = g * 8;
         const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
         if constexpr (S <= 16) {
             typename Word<S>::T X[8];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[q], E);
+            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(cur[q], E);
 #pragma unroll
             for (int d = 0; d < S; ++d) {
                 if (d >= nsl) break;
@@ -238,15 +247,17 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
             int8_t dig[kMaxSlices];
             const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
             for (int q = 0; q < nvalid; ++q) {
-                slice_digits_slow(bits[q], E, s, dig);
+                slice_digits_slow(cur[q], E, s, dig);
                 for (int d = 0; d < nsl; ++d) a.planes[plane_off(a, d, line, p0 + q)] = dig[d];
             }
         }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
     }
 }
 
 template <bool kVec>
-__global__ void __launch_bounds__(256) slice_rows_kernel(SliceArgs a) {
+__global__ void __launch_bounds__(256, 3) slice_rows_kernel(SliceArgs a) {
     int s, nsl;
     if (!resolve(a, s, nsl)) return;
     // blocked planes are zero-filled up to the 32-byte k-block
