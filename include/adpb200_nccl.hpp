@@ -1,0 +1,104 @@
+// adpb200_nccl.hpp — the B-distributed multi-GPU ADP DGEMM driven from C++ with
+// NCCL (one process or thread per GPU, one ncclComm_t per rank), the native
+// counterpart of paper_2511_13778_b200/dist.py. Header-only; link libadpb200.so,
+// the CUDA runtime and libnccl.
+//
+// Rank r owns rows [r0, r0+m) of op(A) and C (column-major, ld lda / ldc) and
+// the B column slab r: k x (n/world), column-major, leading dimension k
+// (n/world a multiple of 8). The collectives run on the caller's stream
+// (statistics all-gather, decision max-allreduce) and on a second stream for
+// the B-plane all-gather, which overlaps the GEMM of the rank's own columns
+// (phases 5/6 of adpb200_dgemm_dist). One 8-byte host read of the reduced
+// decision input sizes that all-gather. Every rank takes the same decision:
+// the assembled C is bit-identical to one GPU's adpb200_dgemm.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdint>
+
+#include "adpb200.h"
+
+namespace adpb200 {
+
+namespace nccl_detail {
+inline int cu(cudaError_t e) { return e == cudaSuccess ? ADPB200_OK : ADPB200_ERR_RUNTIME; }
+inline int nc(ncclResult_t r) { return r == ncclSuccess ? ADPB200_OK : ADPB200_ERR_RUNTIME; }
+}  // namespace nccl_detail
+
+// Returns an adpb200 status (0 ok, 2 runtime incl. CUDA/NCCL failures, 3 contract).
+inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int world, char transa, int64_t m_global,
+                           int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
+                           const double* B_slab, double beta, double* C, int64_t ldc, const adpb200_options* opt,
+                           adpb200_trace* trace_dev, cudaStream_t st) {
+    using namespace nccl_detail;
+    int64_t sz[4];
+    int rc = adpb200_dist_sizes(n, k, world, opt, sz);
+    if (rc) return rc;
+    const int64_t nrec = sz[0], hdr = sz[1], plane_bytes = sz[2], cap_bytes = sz[3];
+    int32_t *bl = nullptr, *ba = nullptr, *xchg = nullptr;
+    int8_t *slab = nullptr, *gathered = nullptr;
+    double* bfull = nullptr;
+    cudaStream_t comm_st = nullptr;
+    cudaEvent_t ev_slab = nullptr, ev_gather = nullptr;
+    int32_t xh[2] = {0, 0};
+    int32_t dec[4] = {0, 0, 0, 0};
+    auto phase = [&](int p, const void* g, int nsl) {
+        return adpb200_dgemm_dist(h, p, m_global, world, rank, transa, m, n, k, alpha, A, lda, B_slab, beta, C, ldc,
+                                  opt, trace_dev, bl, ba, xchg, slab, g, nsl, st);
+    };
+    rc = cu(cudaMallocAsync(&bl, size_t(nrec) * 4, st));
+    if (!rc) rc = cu(cudaMallocAsync(&ba, size_t(nrec) * 4 * world, st));
+    if (!rc) rc = cu(cudaMallocAsync(&xchg, 8, st));
+    if (!rc) rc = cu(cudaMallocAsync(&slab, size_t(cap_bytes), st));
+    if (!rc) rc = cu(cudaMemsetAsync(xchg, 0, 8, st));
+    // 1: exponent statistics of the A rows and the B slab; all-gather the slab records
+    if (!rc) rc = phase(1, nullptr, 0);
+    if (!rc) rc = nc(ncclAllGather(bl, ba, size_t(nrec), ncclInt32, comm, st));
+    // 2: ESC of the local rows against every column; max-allreduce {exceptional, esc}
+    if (!rc) rc = phase(2, nullptr, 0);
+    if (!rc) rc = nc(ncclAllReduce(xchg, xchg, 2, ncclInt32, ncclMax, comm, st));
+    // 3: decision, slicing; the host learns how many planes travel
+    if (!rc) rc = phase(3, nullptr, 0);
+    if (!rc) rc = cu(cudaMemcpyAsync(xh, xchg, 8, cudaMemcpyDeviceToHost, st));
+    if (!rc) rc = cu(cudaStreamSynchronize(st));
+    if (!rc) rc = adpb200_dist_decision(opt, xh, m_global, n, k, dec);
+    const int nsl = dec[2];
+    if (!rc && nsl > 0) {
+        // B planes all-gathered on a second stream while this rank's own columns compute
+        const int64_t rec = hdr + int64_t(nsl) * plane_bytes;
+        rc = cu(cudaMallocAsync(&gathered, size_t(rec) * world, st));
+        if (!rc) rc = cu(cudaStreamCreateWithFlags(&comm_st, cudaStreamNonBlocking));
+        if (!rc) rc = cu(cudaEventCreateWithFlags(&ev_slab, cudaEventDisableTiming));
+        if (!rc) rc = cu(cudaEventCreateWithFlags(&ev_gather, cudaEventDisableTiming));
+        if (!rc) rc = cu(cudaEventRecord(ev_slab, st));
+        if (!rc) rc = cu(cudaStreamWaitEvent(comm_st, ev_slab, 0));
+        if (!rc) rc = nc(ncclAllGather(slab, gathered, size_t(rec), ncclInt8, comm, comm_st));
+        if (!rc) rc = cu(cudaEventRecord(ev_gather, comm_st));
+        if (!rc) rc = phase(5, slab, nsl);
+        if (!rc) rc = cu(cudaStreamWaitEvent(st, ev_gather, 0));
+        if (!rc) rc = phase(6, gathered, nsl);
+    } else if (!rc) {
+        // native fallback: every rank needs all of B in FP64 (the slabs concatenate to B, ld = k)
+        rc = cu(cudaMallocAsync(&bfull, size_t(k) * size_t(n) * 8, st));
+        if (!rc) rc = nc(ncclAllGather(B_slab, bfull, size_t(k) * size_t(n / world), ncclFloat64, comm, st));
+        if (!rc) rc = phase(6, bfull, 0);
+    }
+    // stream-ordered frees; the events / side stream are released once their work is done
+    if (bl) cudaFreeAsync(bl, st);
+    if (ba) cudaFreeAsync(ba, st);
+    if (xchg) cudaFreeAsync(xchg, st);
+    if (slab) cudaFreeAsync(slab, st);
+    if (gathered) cudaFreeAsync(gathered, st);
+    if (bfull) cudaFreeAsync(bfull, st);
+    if (comm_st) {
+        cudaStreamSynchronize(comm_st);
+        cudaStreamDestroy(comm_st);
+    }
+    if (ev_slab) cudaEventDestroy(ev_slab);
+    if (ev_gather) cudaEventDestroy(ev_gather);
+    return rc;
+}
+
+}  // namespace adpb200

@@ -138,3 +138,15 @@ def test_cpp_facade_compiles_and_checks_contracts(tmp_path):
     exe = _build_facade(tmp_path)
     r = subprocess.run([exe, "cpu"], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr + r.stdout
+
+
+def test_nccl_cpp_driver_compiles(tmp_path):
+    """include/adpb200_nccl.hpp (C++ multi-GPU driver over NCCL) compiles and links
+    against libadpb200.so and libnccl (the run is a GPU test)."""
+    exe = os.path.join(str(tmp_path), "dist_nccl_check")
+    cmd = ["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "tests", "cpp", "dist_nccl_check.cpp"), "-o", exe,
+           "-L", os.path.join(ROOT, "paper_2511_13778_b200"), "-ladpb200",
+           "-L/usr/local/cuda/lib64", "-lcudart", "-lnccl"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
