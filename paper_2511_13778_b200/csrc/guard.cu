@@ -250,6 +250,14 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
         sBoff[threadIdx.x] = r * rec + (gj - r * nr);
     }
     __syncthreads();
+    // staging roles, fixed per thread: one A line (or one B column pair), every 4th block
+    const int sl = threadIdx.x % 64, st0 = threadIdx.x / 64;
+    const int64_t ga = i0 + sl;
+    const bool a_ok = ga < m;
+    const int32_t* pamx = amaxT + ga;
+    const int32_t* pamn = aminT + ga;
+    const bool b_ok0 = j0 + 2 * sl < n, b_ok1 = j0 + 2 * sl + 1 < n;
+    const int64_t bo0 = sBoff[2 * sl], bo1 = sBoff[2 * sl + 1];
     uint32_t z[4][4];  // [i][j pair]
 #pragma unroll
     for (int a = 0; a < 4; ++a)
@@ -257,22 +265,17 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
         for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
     for (int64_t tb = 0; tb < t; tb += kEscTB) {
         __syncthreads();
-        for (int idx = threadIdx.x; idx < kEscTB * kEscBI; idx += 256) {
-            const int ii = idx % kEscBI, tt = idx / kEscBI;
-            const int64_t gi = i0 + ii, gt = tb + tt;
-            const bool ok = gi < m && gt < t;
-            const int vx = ok ? to16(amaxT[gt * astride + gi]) : kS16;
-            const int vn = ok ? to16(aminT[gt * astride + gi]) : kS16;
-            sAmx[tt][ii] = pack2(vx, vx);
-            sAmn[tt][ii] = pack2(vn, vn);
-        }
-        for (int idx = threadIdx.x; idx < kEscTB * kEscBJ / 2; idx += 256) {
-            const int jp = idx % (kEscBJ / 2), tt = idx / (kEscBJ / 2);
-            const int64_t gj = j0 + 2 * jp, gt = tb + tt;
-            const bool ok0 = gj < n && gt < t, ok1 = gj + 1 < n && gt < t;
-            const int64_t o0 = sBoff[2 * jp] + gt * nr, o1 = sBoff[2 * jp + 1] + gt * nr;
-            sBmx[tt][jp] = pack2(ok0 ? to16(bmaxT[o0]) : kS16, ok1 ? to16(bmaxT[o1]) : kS16);
-            sBmn[tt][jp] = pack2(ok0 ? to16(bminT[o0]) : kS16, ok1 ? to16(bminT[o1]) : kS16);
+#pragma unroll 1
+        for (int tt = st0; tt < kEscTB; tt += 4) {
+            const int64_t gt = tb + tt;
+            const bool tok = gt < t;
+            const int vx = a_ok && tok ? to16(pamx[gt * astride]) : kS16;
+            const int vn = a_ok && tok ? to16(pamn[gt * astride]) : kS16;
+            sAmx[tt][sl] = pack2(vx, vx);
+            sAmn[tt][sl] = pack2(vn, vn);
+            const int64_t go = gt * nr;
+            sBmx[tt][sl] = pack2(b_ok0 && tok ? to16(bmaxT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bmaxT[bo1 + go]) : kS16);
+            sBmn[tt][sl] = pack2(b_ok0 && tok ? to16(bminT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bminT[bo1 + go]) : kS16);
         }
         __syncthreads();
         auto step = [&](int tt) {
@@ -303,24 +306,32 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
             for (int tt = 0; tt < tcount; ++tt) step(tt);
         }
     }
-    int esc = 0;
+    // spans, two j per int16x2 word: la + lb + 1 - z in [-4193, 4195] for real
+    // exponents; z <= -8000 (structurally zero dot product, or a padded row /
+    // column) is masked to -32768 so it never wins the max.
+    uint32_t lbp[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const int jj = 2 * (tx * 4 + b);
+        const int l0 = j0 + jj < n ? bline[sBoff[jj]] : 0, l1 = j0 + jj + 1 < n ? bline[sBoff[jj + 1]] : 0;
+        lbp[b] = pack2(l0 + 1, l1 + 1);
+    }
+    const uint32_t lim = pack2(-8000, -8000);
+    uint32_t best = pack2(-32768, -32768);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int64_t gi = i0 + ty * 4 + a;
-        if (gi >= m) continue;
-        const int la = aline[gi];
+        const int la = gi < m ? aline[gi] : 0;
+        const uint32_t lap = pack2(la, la);
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t gj = j0 + 2 * (tx * 4 + b) + h;
-                if (gj >= n) continue;
-                const int zz = int(int16_t(z[a][b] >> (16 * h)));
-                if (zz <= -8000) continue;  // structurally zero dot product
-                esc = max(esc, la + bline[sBoff[2 * (tx * 4 + b) + h]] - zz + 1);
-            }
+        for (int b = 0; b < 4; ++b) {
+            const uint32_t span = __vsub2(__vadd2(lap, lbp[b]), z[a][b]);
+            const uint32_t dead = __vcmples2(z[a][b], lim);  // 0xffff per half where z <= -8000
+            best = __vmaxs2(best, (span & ~dead) | (0x80008000u & dead));
+        }
     }
-    esc = warp_max(esc);
+    int esc = max(int(int16_t(best & 0xffffu)), int(int16_t(best >> 16)));
+    esc = warp_max(max(esc, 0));
     if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(esc_out, esc);
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && ran_flag) *ran_flag = 1;
 }
