@@ -42,6 +42,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--size", type=int, default=NOMINAL, help="m_per_gpu = n = k")
+    p.add_argument("--config", choices=["c2", "c4"], default="c2",
+                   help="c2: the headline (8192^3 per GPU, weak scaling); c4: BASELINE config 4, 32768^3 U[-1,1] "
+                        "row-partitioned over the GPUs (strong scaling; side measurements skipped)")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
@@ -210,9 +213,20 @@ def main():
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
-    n = k = args.size
-    m = args.size                      # rows per GPU (weak scaling)
-    m_global = m * world
+    c4 = args.config == "c4"
+    if c4:
+        from paper_2511_13778_b200.dist import rows_of
+
+        n = k = m_global = 32768       # BASELINE config 4 (strong scaling: rows partitioned)
+        r0, r1 = rows_of(rank, world, m_global)
+        m = r1 - r0
+        lo = -1.0
+        args.quick = True
+    else:
+        n = k = args.size
+        m = args.size                  # rows per GPU (weak scaling)
+        m_global = m * world
+        lo = 1.0
     handle = adp.Handle.default(dev.index)
 
     # synthetic operands, column-major storage (torch row-major of the transpose),
@@ -220,8 +234,8 @@ def main():
     # xoshiro256++, grading.cpp:56-63) drawn on the device
     from paper_2511_13778_b200 import grading
 
-    At = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, 1.0, 2.0, dev.index)   # A: m x k col-major
-    Bt = grading.gen_uniform_rect(n, k, 2, 1.0, 2.0, dev.index)                # B: k x n col-major
+    At = grading.gen_uniform_rect(k, m, 1 + 1000 * rank, lo, 2.0 if lo > 0 else 1.0, dev.index)  # A: m x k col-major
+    Bt = grading.gen_uniform_rect(n, k, 2, lo, 2.0 if lo > 0 else 1.0, dev.index)               # B: k x n col-major
     if world > 1:
         # B distributed by column slabs: this rank keeps columns cols_of(rank) only
         c0, c1 = cols_of(rank, world, n)
@@ -311,8 +325,10 @@ def main():
         pass
     pairs = trace.pairs or 0
     achieved = 2.0 * m * n * k * pairs / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    traffic = None
+    traffic = None  # the ncu capture is of the 8192^3 headline kernel
     try:
+        if c4:
+            raise OSError
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             traffic = json.load(f).get("igemm_dram_bytes_per_launch")
     except OSError:
@@ -435,13 +451,16 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, 8192^3",
+            "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, "
+                      + ("32768^3 (BASELINE config 4)" if c4 else "8192^3"),
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if c4 else "weak", "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic U(1,2): the reference's gen_uniform_rect (xoshiro256++) seeds 1, 2, on the device",
-            "config": {"workload": f"ADP DGEMM {m_global}x{n}x{k} column-major NN (8192 rows per GPU), "
-                                   "guardrails live, ESC-chosen s, pairs d_a+d_b<=s",
+            "data": ("synthetic U[-1,1]" if c4 else "synthetic U(1,2)")
+                    + ": the reference's gen_uniform_rect (xoshiro256++) seeds 1, 2, on the device",
+            "config": {"workload": f"ADP DGEMM {m_global}x{n}x{k} column-major NN ("
+                                   + ("rows partitioned over the GPUs" if c4 else "8192 rows per GPU")
+                                   + "), guardrails live, ESC-chosen s, pairs d_a+d_b<=s",
                        "m": m_global, "n": n, "k": k, "slices": trace.slices, "esc_bits": trace.esc_bits,
                        "path": trace.path, "pairs": pairs, "gemm_variant": trace.gemm_variant,
                        "parallelism": (f"row-block x{world}: A/C rows per rank, B column slabs; B exponent "
