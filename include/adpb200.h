@@ -71,8 +71,21 @@ typedef struct adpb200_options {
                                   PAPER.md:734-757); the slice count stays pinned to
                                   forced_slices, exceptional inputs still fall back */
     int32_t fallback;          /* ADPB200_FALLBACK_* */
-    int32_t reserved[5];
+    int32_t esc_method;        /* ADPB200_ESC_COARSENED (default: the reference's esc_coarsened)
+                                  or ADPB200_ESC_CERTIFIED: when the coarsened ESC asks for more
+                                  than the minimum slice count s0 = ceil((target_bits+2)/8), an
+                                  INT8 tensor-core GEMM of exponent indicator planes checks
+                                  whether every (i,j) has, among the first min(k, 512)
+                                  positions, a product within 2*delta bits of
+                                  rowmax_i + colmax_j (delta the largest with 2*delta+1 <= the
+                                  ESC s0 tolerates); if so esc_bits = 2*delta+1 (an upper bound
+                                  of esc_exact, esc.cpp:61-87), else the coarsened value stays.
+                                  Single-GPU entry points; the multi-GPU phases ignore it. */
+    int32_t reserved[4];
 } adpb200_options;
+
+#define ADPB200_ESC_COARSENED 0
+#define ADPB200_ESC_CERTIFIED 1
 
 /* AdpTrace (adp.hpp:57-67) + decision details; written to DEVICE memory by
  * the pipeline (stream-ordered). -1 encodes JSON null. */

@@ -411,6 +411,40 @@ class Oracle:
         return out
 
 
+def exponent_field(a: np.ndarray) -> np.ndarray:
+    """Effective exponents floor(log2|v|) with NEG_SENTINEL at zeros and non-finite
+    values (esc.cpp:26-56 exponent_field; subnormals included via frexp)."""
+    a = np.abs(_f64(a))
+    _, e = np.frexp(a)
+    ok = (a != 0) & np.isfinite(a)
+    return np.where(ok, e.astype(np.int64) - 1, NEG_SENTINEL)
+
+
+def esc_certified(a, b, coarse_esc: int, target_bits: int = 53, window: int = 512) -> int:
+    """Numpy restatement of the certified ESC (adpb200_options.esc_method = 1,
+    guard.cu certify_prep_kernel): with s0 = required_slices(target_bits, 0)
+    (esc.cpp:8-12), e0 = 8 s0 - target_bits - 2 and delta = (e0 - 1) // 2, the
+    result is 2 delta + 1 when every (i, j) has some l with
+    e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta (then the exact
+    z_ij of esc_exact, esc.cpp:61-87, is >= rowmax_i + colmax_j - 2 delta and
+    span_ij <= 2 delta + 1), and coarse_esc otherwise or when coarse_esc is
+    already <= 2 delta + 1. Only the first `window` positions l are inspected
+    (row / column maxima over the whole line), like api.cu's kCertifyWindow."""
+    s0 = (target_bits + 2 + 7) // 8
+    e0 = 8 * s0 - target_bits - 2
+    delta = (e0 - 1) // 2 if e0 >= 1 else -1
+    if delta < 0 or coarse_esc <= 2 * delta + 1:
+        return coarse_esc
+    ea, eb = exponent_field(a), exponent_field(b)
+    rmax = ea.max(axis=1, initial=NEG_SENTINEL)
+    cmax = eb.max(axis=0, initial=NEG_SENTINEL)
+    ea, eb = ea[:, :window], eb[:window, :]
+    p = ((ea != NEG_SENTINEL) & (ea >= rmax[:, None] - delta)).astype(np.float64)
+    q = ((eb != NEG_SENTINEL) & (eb >= cmax[None, :] - delta)).astype(np.float64)
+    counts = p @ q  # exact: 0/1 products, sums <= k < 2^53
+    return 2 * delta + 1 if bool((counts > 0).all()) else coarse_esc
+
+
 def fold_round(acc_row: np.ndarray, exp2: int) -> float:
     """Exact fold of one element's diagonal accumulators + RNE (port only)."""
     lib = _load("port")

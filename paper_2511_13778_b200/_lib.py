@@ -33,7 +33,8 @@ class Options(C.Structure):
         ("pair_limit", C.c_int32),
         ("guardrails_forced", C.c_int32),
         ("fallback", C.c_int32),
-        ("reserved", C.c_int32 * 5),
+        ("esc_method", C.c_int32),
+        ("reserved", C.c_int32 * 4),
     ]
 
 

@@ -41,6 +41,9 @@ class AdpMode(enum.IntEnum):
     ForceNative = 2
 
 
+ESC_METHODS = {"coarsened": 0, "certified": 1}
+
+
 @dataclass
 class AdpConfig:
     """ozadp::AdpConfig (adp.hpp:18-33) + the B200 extensions."""
@@ -55,6 +58,9 @@ class AdpConfig:
     chunk_len: int = 65536
     pair_limit: int = PAIRS_FULL      # PAIRS_FULL (reference), PAIRS_TARGET (d_a+d_b <= s) or a limit
     guardrails_forced: bool = False   # ForceEmulate still runs scan + ESC + decide
+    # "coarsened" (the reference's esc_coarsened) or "certified": the coarsened ESC
+    # lowered to the s0 bound when an INT8 indicator GEMM certifies it (adpb200.h)
+    esc_method: str = "coarsened"
 
     def to_c(self) -> _lib.Options:
         o = _lib.default_options()
@@ -68,6 +74,7 @@ class AdpConfig:
         o.chunk_len = int(self.chunk_len)
         o.pair_limit = int(self.pair_limit)
         o.guardrails_forced = 1 if self.guardrails_forced else 0
+        o.esc_method = ESC_METHODS.get(self.esc_method, -1)
         return o
 
     def validate(self) -> None:

@@ -84,7 +84,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // Carve-up of the workspace for one call.
 struct Layout {
     size_t plan, stats_a_max, stats_a_min, line_a, stats_b_max, stats_b_min, line_b, scale_a, scale_b, planes_a,
-        planes_b, partial, scratch, total;
+        planes_b, partial, scratch, rplan, total;
     int64_t blocks, pitch, slots_a, slots_b;
     int cap;
 };
@@ -116,6 +116,7 @@ Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) 
     L.planes_b = take(cap ? size_t(cap) * L.slots_b * L.pitch : 0);
     L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
     L.scratch = take(4096);
+    L.rplan = take(sizeof(Plan));
     L.total = off;
     return L;
 }
@@ -193,6 +194,50 @@ struct HostOut {
     }
 };
 
+constexpr int64_t kCertifyWindow = 512;  // k positions the certificate inspects
+
+// Certified ESC (adpb200_options.esc_method): exponent indicator planes of A
+// and B go to plane 0 of the slice buffers (free until slicing), one INT8 GEMM
+// counts per (i, j) the positions where both are on, and no zero count lowers
+// plan->esc_raw to 2 delta + 1 (guard.cu: certify_prep_kernel). Stream-ordered,
+// predicated on the coarsened result: nothing runs when it already gives s0.
+int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, const Layout& Lw, Plan* plan,
+                cudaStream_t st) {
+    uint64_t* nl = &h->launches;
+    Plan* rplan = at<Plan>(h, Lw.rplan);
+    int8_t* pa = at<int8_t>(h, Lw.planes_a);
+    int8_t* pb = at<int8_t>(h, Lw.planes_b);
+    // the first kCertifyWindow positions only: a nonzero count there already
+    // certifies (i, j), and U[-1,1]-like data misses with probability ~(3/4)^512
+    const int64_t kw = std::min<int64_t>(P.K, kCertifyWindow);
+    LineView va = P.a, vb = P.b;
+    va.len = kw;
+    vb.len = kw;
+    launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl);
+    launch_slice(va, at<int32_t>(h, Lw.line_a), pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st,
+                 nl, 1);
+    launch_slice(vb, at<int32_t>(h, Lw.line_b), pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, nullptr, rplan, 0, 1, st,
+                 nl, 1);
+    GemmArgs g{};
+    g.plan = rplan;
+    g.M = P.M;
+    g.N = P.N;
+    g.K = kw;
+    g.scale_a = at<int32_t>(h, Lw.scale_a);
+    g.scale_b = at<int32_t>(h, Lw.scale_b);
+    g.alpha = 1.0;
+    g.partial = at<uint64_t>(h, Lw.partial);
+    g.zero_flag = &rplan->exc;
+    if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, Lw.cap, g, st, nl))
+        return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
+    launch_certify_finish(plan, rplan, st, nl);
+    return ADPB200_OK;
+}
+
+bool certify_wanted(const Problem& P, const adpb200_options& o, bool esc_expected, int cap) {
+    return o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected && cap >= 1 && P.M > 0 && P.N > 0 && P.K > 0;
+}
+
 // phase 0: the whole pipeline. Multi-GPU row partition: phase 1 runs the
 // guardrails (K1, K2) on this rank's rows and exports {exc, esc_raw} to xchg
 // (device int32[2]) for a max-allreduce across ranks; phase 2 imports the
@@ -242,6 +287,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     if (esc_expected && phase != 2)
         launch_esc(amax, amin, aline, bmax, bmin, bline, P.M, P.N, Lw.blocks, plan, &plan->esc_raw, &plan->esc_ran,
                    st, nl);
+    if (phase == 0 && certify_wanted(P, o, esc_expected, cap) && (rc = run_certify(h, P, o, Lw, plan, st))) return rc;
     tm.end(1);
     static_assert(offsetof(Plan, esc_raw) == offsetof(Plan, exc) + 4, "xchg layout");
     if (phase == 1) {
@@ -618,6 +664,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
         if (rc) return rc;
     }
     // the real decision (the trace is written here), then compare with the speculation
+    if (certify_wanted(P, o, esc_expected, cap) && (rc = run_certify(h, P, o, Lw, plan, st))) return rc;
     launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, P.swap_ab, tdev, st, nl);
     spec_fixup_kernel<<<1, 1, 0, st>>>(plan, spec);
     ++*nl;
@@ -715,6 +762,8 @@ int adpb200_validate_options(const adpb200_options* o) {
         return fail(3, "GemmParams: chunk_len * 16384 must stay below 2^31");
     if (o->pair_limit < ADPB200_PAIRS_TARGET) return fail(3, "options: bad pair_limit");
     if (o->fallback != ADPB200_FALLBACK_REFERENCE) return fail(3, "options: bad fallback");
+    if (o->esc_method != ADPB200_ESC_COARSENED && o->esc_method != ADPB200_ESC_CERTIFIED)
+        return fail(3, "options: bad esc_method");
     return ADPB200_OK;
 }
 

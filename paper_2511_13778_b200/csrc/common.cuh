@@ -45,7 +45,8 @@ struct Plan {
     int32_t kchunk;    // k elements per int32 accumulation chunk
     int32_t nchunks;
     double cost;
-    int32_t pad[4];
+    int32_t aux;  // certified-ESC plan: the indicator threshold delta
+    int32_t pad[3];
 };
 
 struct DecideInput {

@@ -502,6 +502,50 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
     ++*nlaunch;
 }
 
+// ---- certified ESC ----------------------------------------------------------------
+// s0 = required_slices(target_bits, 0) is the fewest slices any input can get;
+// it tolerates esc <= e0 = 8 s0 - target_bits - 2. If some l has
+// e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta, the exact
+// largest product exponent z_ij (esc.cpp:61-87) is >= rowmax_i + colmax_j -
+// 2 delta, so span_ij <= 2 delta + 1. delta = (e0 - 1) / 2 makes that span
+// fit s0. The "some l" test for every (i, j) is one INT8 GEMM of 0/1 planes.
+__global__ void certify_prep_kernel(const Plan* plan, Plan* rplan, int target_bits, int64_t k) {
+    Plan r{};
+    r.path = kPathDone;
+    const int s0 = (target_bits + 2 + 7) / 8;
+    const int e0 = 8 * s0 - target_bits - 2;
+    const int delta = e0 >= 1 ? (e0 - 1) / 2 : -1;
+    if (plan->esc_ran && plan->exc == 0 && delta >= 0 && plan->esc_raw > 2 * delta + 1 && k > 0 &&
+        k <= (int64_t(1) << 30)) {
+        r.path = ADPB200_PATH_EMULATED;
+        r.slices = 1;
+        r.L = 0;
+        r.nsl = 1;
+        r.pairs = 1;
+        r.variant = 64;
+        r.kchunk = int32_t((k + 31) / 32 * 32);  // counts <= k: one int32 chunk
+        r.nchunks = 1;
+        r.aux = delta;
+        r.exc = 0;  // the GEMM's zero-count flag
+    }
+    *rplan = r;
+}
+
+__global__ void certify_finish_kernel(Plan* plan, const Plan* rplan) {
+    if (rplan->path == ADPB200_PATH_EMULATED && rplan->exc == 0) plan->esc_raw = 2 * rplan->aux + 1;
+}
+
+void launch_certify_prep(const Plan* plan, Plan* rplan, int target_bits, int64_t k, cudaStream_t st,
+                         uint64_t* nlaunch) {
+    certify_prep_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits, k);
+    ++*nlaunch;
+}
+
+void launch_certify_finish(Plan* plan, const Plan* rplan, cudaStream_t st, uint64_t* nlaunch) {
+    certify_finish_kernel<<<1, 1, 0, st>>>(plan, rplan);
+    ++*nlaunch;
+}
+
 void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
                    int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch) {
     decide_kernel<<<1, 1, 0, st>>>(plan, opt, m, n, k, esc_expected, swap_ab, trace);

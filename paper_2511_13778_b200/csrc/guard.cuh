@@ -50,6 +50,14 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
 // zero-filled up to the next multiple of 32 positions; 0: [line][pitch].
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
                   int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
-                  uint64_t* nlaunch);
+                  uint64_t* nlaunch, int indicator = 0);
+
+// Certified ESC (adpb200_options.esc_method): prep turns the coarsened result in
+// `plan` into the indicator-GEMM plan `rplan` (path kPathDone when there is
+// nothing to certify); finish lowers plan->esc_raw to 2*delta+1 when no
+// (i, j) count came out zero.
+void launch_certify_prep(const Plan* plan, Plan* rplan, int target_bits, int64_t k, cudaStream_t st,
+                         uint64_t* nlaunch);
+void launch_certify_finish(Plan* plan, const Plan* rplan, cudaStream_t st, uint64_t* nlaunch);
 
 }  // namespace adpb200

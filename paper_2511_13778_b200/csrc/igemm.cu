@@ -555,6 +555,29 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                 if (timing) th = clock64();
                 const bool last = c == lp.nchunks - 1;
                 const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
+                if constexpr (NB == 64) {
+                    if (g.zero_flag) {
+                        // certified ESC: diagonal 0 holds the indicator-product counts;
+                        // one zero count among the valid (i, j) voids the certificate
+                        bool zero = false;
+#pragma unroll
+                        for (int b = 0; b < kCols / 8; ++b) {
+                            uint32_t v[8];
+                            tc::tmem_ld<8>(trow + uint32_t(jh * kCols + b * 8), v);
+                            tc::tmem_wait_ld();
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc) {
+                                const int64_t col = nt * NB + jh * kCols + b * 8 + cc;
+                                if (row_ok && col < g.N && v[cc] == 0u) zero = true;
+                            }
+                        }
+                        tc::fence_before();
+                        tc::mbar_arrive(&hdr->tmem_empty);
+                        if (__any_sync(0xffffffffu, zero) && lane == 0) atomicOr(g.zero_flag, 1);
+                        acc_phase ^= 1;
+                        continue;
+                    }
+                }
                 if constexpr (C::kNL == 2) {
                     if (!g.dump) {
                         // phase A (holding TMEM): fold every column of the warp exactly and

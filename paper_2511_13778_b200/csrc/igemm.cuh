@@ -29,6 +29,7 @@ struct GemmArgs {
     int debug;  // timing diagnostics only (ADPB200_DEBUG): 1 skip MMAs, 2 skip epilogue math
     int64_t mt_begin, mt_end;  // 128-row m-tile range to compute (mt_end 0 = all)
     int64_t nt_begin, nt_end;  // NB-column n-tile range to compute (nt_end 0 = all)
+    int32_t* zero_flag;        // certified ESC: no C; set to 1 if any (i, j) has a zero diagonal-0 count
 };
 
 // nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.

@@ -170,7 +170,22 @@ struct SliceArgs {
     int32_t* scale;
     const Plan* plan;
     int slices_fixed;
+    int indicator;         // certified ESC: one plane of (e >= line_max - plan->aux) bytes
 };
+
+// Certified-ESC indicator bytes of 8 elements: 1 where the element is finite,
+// nonzero and its effective exponent is within delta of the line maximum.
+__device__ __forceinline__ void indicator_bytes(const uint64_t (&bits)[8], int lm, int delta, uint32_t& lo,
+                                                uint32_t& hi) {
+    lo = hi = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const uint64_t b = bits[q];
+        const bool on = (b << 1) != 0 && ((b >> 52) & 0x7ff) != 0x7ff && eff_exp(b) >= lm - delta;
+        if (q < 4) lo |= uint32_t(on) << (8 * q);
+        else hi |= uint32_t(on) << (8 * (q - 4));
+    }
+}
 
 // byte offset of (d, line, pos) inside the planes
 __device__ __forceinline__ int64_t plane_off(const SliceArgs& a, int d, int64_t line, int64_t pos) {
@@ -226,7 +241,17 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
         if (g == 0 && a.scale) a.scale[line] = E;
         const int64_t p0 = g * 8;
         const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
-        if constexpr (S <= 16) {
+        if constexpr (S == 0) {
+            uint32_t lo, hi;
+            indicator_bytes(cur, lm, a.plan->aux, lo, hi);
+            int8_t* out = a.planes + plane_off(a, 0, line, p0);
+            if (kVec && nvalid == 8) {
+                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+            } else {
+                const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+                for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
+            }
+        } else if constexpr (S <= 16) {
             typename Word<S>::T X[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(cur[q], E);
@@ -263,6 +288,10 @@ __global__ void __launch_bounds__(256, 3) slice_rows_kernel(SliceArgs a) {
     // blocked planes are zero-filled up to the 32-byte k-block
     const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
     const int64_t groups = (span + 7) / 8;
+    if (a.indicator) {
+        rows_body<0, kVec>(a, nsl, groups, span);
+        return;
+    }
     switch (s) {
 #define ADPB200_ROWS_CASE(S) \
     case S: rows_body<S, kVec>(a, nsl, groups, span); break;
@@ -346,6 +375,16 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
     uint64_t bits[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) bits[q] = tile[og * 8 + q][ol];
+    if (a.indicator) {
+        uint32_t lo, hi;
+        indicator_bytes(bits, lm, a.plan->aux, lo, hi);
+        const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+        int8_t* out = a.planes + plane_off(a, 0, line, p0);
+        if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+        else
+            for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, 0, line, p0 + q)] = int8_t(w >> (8 * q));
+        return;
+    }
     switch (s) {
 #define ADPB200_COLS_CASE(S) \
     case S: cols_body<S>(a, nsl, bits, E, line, p0, nvalid); break;
@@ -362,9 +401,9 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
 
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
                   int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
-                  uint64_t* nlaunch) {
+                  uint64_t* nlaunch, int indicator) {
     if (v.lines == 0) return;
-    SliceArgs a{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed};
+    SliceArgs a{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed, indicator};
     const bool rows = v.ps == 1 || v.lines == 1 || v.len == 0;
     if (rows) {
         if (a.v.lines == 1) a.v.ls = 0;

@@ -1,0 +1,91 @@
+"""Certified ESC on the GPU (adpb200_options.esc_method = ADPB200_ESC_CERTIFIED):
+the indicator planes + INT8 count GEMM must reproduce the numpy restatement
+(oracle.esc_certified) exactly, the decision must follow the reference's
+decide() on that ESC, and C must equal the reference-order emulated_gemm at
+the decided s bitwise — on the device path, the streamed host path and at
+4096^3, where U[-1,1] drops from the coarsened s = 8 to s = 7 with the
+accuracy of a double-double oracle kept."""
+import numpy as np
+import pytest
+
+from conftest import assert_bitwise
+from oracle.oracle import Config, esc_certified
+
+pytestmark = pytest.mark.gpu
+
+PATHS = ("emulated", "native_fallback")
+
+
+def _make(name, m, k, n, seed):
+    rng = np.random.default_rng(seed)
+    if name == "u12":
+        return rng.uniform(1, 2, (m, k)), rng.uniform(1, 2, (k, n))
+    a, b = rng.uniform(-1, 1, (m, k)), rng.uniform(-1, 1, (k, n))
+    if name == "wide":
+        a = a * np.exp2(rng.integers(-40, 40, (m, k)))
+    elif name == "zero_col":
+        b[:, 7] = 0.0
+    elif name == "sparse":
+        a = a * (rng.random((m, k)) < 0.05)
+    elif name == "subnormal":
+        a = a * 2.0 ** -1060
+    elif name == "late_max":
+        a[5, :600] *= 1e-3  # row 5's large entries all lie past the 512-position window
+    return a, b
+
+
+CASES = [("u11", 256, 300, 260, 53), ("u11", 300, 1000, 512, 53), ("u12", 512, 256, 300, 53),
+         ("wide", 300, 400, 280, 53), ("zero_col", 256, 512, 256, 53), ("sparse", 260, 700, 300, 53),
+         ("subnormal", 256, 260, 256, 53), ("u11", 256, 300, 260, 50), ("u11", 256, 300, 260, 54),
+         ("u11", 1000, 640, 600, 53), ("late_max", 256, 1000, 300, 53)]
+
+
+@pytest.mark.parametrize("name,m,k,n,tb", CASES)
+def test_certified_decision_and_bits(gpu, port, name, m, k, n, tb):
+    import torch
+
+    a, b = _make(name, m, k, n, m + k + n)
+    coarse = port.esc_coarsened(a, b, 256, tb)[0]
+    want_esc = esc_certified(a, b, coarse, tb)
+    if name == "late_max":
+        assert want_esc == coarse and esc_certified(a, b, coarse, tb, window=k) == 1
+    path, _, s, _, _, _ = port.decide(0, 0, m, n, k, want_esc, Config(target_bits=tb))
+    cfg = gpu.AdpConfig(target_bits=tb, esc_method="certified")
+    # device path (CUDA tensors) and the streamed host path (numpy)
+    got_d, td = gpu.adp_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), config=cfg)
+    got_h, th = gpu.adp_gemm(a, b, config=cfg)
+    for t in (td, th):
+        assert t.esc_bits == want_esc, (t.esc_bits, want_esc, coarse)
+        assert t.path == PATHS[path]
+        if t.path == "emulated":
+            assert t.slices == s
+    want = port.emulated_gemm(a, b, s) if path == 0 else port.native_gemm(a, b)
+    assert_bitwise(got_d.cpu().numpy(), want, nan_equiv=False)
+    assert_bitwise(got_h, want, nan_equiv=False)
+    # the default (coarsened) method is untouched
+    _, tc_ = gpu.adp_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), config=gpu.AdpConfig(target_bits=tb))
+    assert tc_.esc_bits == coarse
+
+
+def test_certified_4096_u11_accuracy_and_sampled_bits(gpu, port):
+    import torch
+
+    from paper_2511_13778_b200 import grading
+
+    n = 4096
+    A = grading.gen_uniform_rect(n, n, 1, -1.0, 1.0)
+    B = grading.gen_uniform_rect(n, n, 2, -1.0, 1.0)
+    Cc, tc_ = gpu.adp_gemm(A, B)
+    Cx, tx = gpu.adp_gemm(A, B, config=gpu.AdpConfig(esc_method="certified"))
+    assert tc_.slices == 8 and tc_.esc_bits > 1
+    assert tx.path == "emulated" and tx.esc_bits == 1 and tx.slices == 7
+    ref, absab = grading.dd_gemm(A, B)
+    ec = grading.error_report(Cc, ref, absab=absab)
+    ex = grading.error_report(Cx, ref, absab=absab)
+    # both within a couple of units of 2^-52 |A||B| (componentwise bound of the method)
+    assert ex.max_ratio < 4.0 and ec.max_ratio < 4.0, (ex, ec)
+    rows = np.array([0, 1, 127, 128, 2047, 4095])
+    cols = np.array([0, 5, 63, 64, 1000, 4095])
+    want = port.emulated_gemm(A[rows].cpu().numpy(), B[:, cols].cpu().numpy(), 7)
+    assert_bitwise(Cx[rows][:, cols].cpu().numpy(), want, nan_equiv=False)
+    torch.cuda.synchronize()

@@ -1,7 +1,7 @@
 """Probe of the BASELINE configs beyond the headline on one B200: C5a
 (4096 x 4096 x 65536), C5b (65536 x 1024 x 1024) and C4 on one GPU
 (32768^3), U[-1,1] operands from the reference generator (seeds 1, 2), ADP
-auto with the target pair policy, ADP with all pairs, forced 7 slices, and
+auto with the target pair policy (coarsened and certified ESC), ADP with all pairs, forced 7 slices, and
 cuBLAS DGEMM; accuracy against the device double-double oracle.
 Usage: python tools/shapes_probe.py [c5a c5b c4 ...]"""
 import json
@@ -41,6 +41,7 @@ for name in (sys.argv[1:] or ["c5a", "c5b"]):
     it = max(2, min(20, int(2e13 / flop)))
     res = {"config": name, "m": m, "n": n, "k": k}
     for label, cfg in (("adp_target", adp.AdpConfig(pair_limit=adp.PAIRS_TARGET)),
+                       ("adp_target_certified", adp.AdpConfig(pair_limit=adp.PAIRS_TARGET, esc_method="certified")),
                        ("adp_full", adp.AdpConfig()),
                        ("emulate7_target", adp.AdpConfig(mode=adp.AdpMode.ForceEmulate, forced_slices=7,
                                                           pair_limit=adp.PAIRS_TARGET))):
@@ -53,7 +54,7 @@ for name in (sys.argv[1:] or ["c5a", "c5b"]):
         d = {"ms": ms, "tflops": flop / ms / 1e9, "slices": tr.slices, "esc_bits": tr.esc_bits, "pairs": tr.pairs,
              "variant": tr.gemm_variant, "k_chunks": tr.k_chunks, "path": tr.path,
              "stages": {kk: round(v, 3) for kk, v in st.items()}}
-        if label == "adp_target" and name != "c4":
+        if label.startswith("adp_target") and name != "c4":
             ref, absab = grading.dd_gemm(A, B)
             rep = grading.error_report(C, ref, absab=absab)
             d["max_rel_err"], d["max_ratio"] = rep.max_err, rep.max_ratio
