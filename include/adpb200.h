@@ -179,6 +179,11 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
  *            (record int32[out[0]])            -> all-gather into bstats_all
  *   phase 2  ESC of the local rows against every B column -> xchg (int32[2])
  *                                              -> max-allreduce xchg
+ *            (esc_method = ADPB200_ESC_CERTIFIED: the bstats record also holds
+ *            the slab's indicator plane, phase 2 certifies the local rows
+ *            against every column and sets bit 8 of xchg[0] when some (i, j)
+ *            fails; phase 3 applies the certificate only if no rank set it,
+ *            so the decision equals the single-GPU one)
  *   phase 3  decision with the global dimensions; slice the A rows; slice the
  *            B slab into `slab` = [scale | planes]. The caller copies xchg to
  *            the host and calls adpb200_dist_decision -> nsl planes:

@@ -23,6 +23,7 @@ using namespace adpb200;
 // Stage timing (adpb200_profile_*): CUDA events recorded on the caller's
 // stream around each pipeline stage, read back on request.
 constexpr int kStages = ADPB200_PROFILE_STAGES;
+constexpr int64_t kCertifyWindow = 512;  // k positions the certified ESC inspects
 constexpr int kMaxStreamChunks = 8;  // column chunks of B streamed over PCIe while the GEMM runs
 
 struct adpb200_context {
@@ -193,8 +194,6 @@ struct HostOut {
         return rc;
     }
 };
-
-constexpr int64_t kCertifyWindow = 512;  // k positions the certificate inspects
 
 // Certified ESC (adpb200_options.esc_method): exponent indicator planes of A
 // and B go to plane 0 of the slice buffers (free until slicing), one INT8 GEMM
@@ -410,11 +409,17 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     int32_t* amin = at<int32_t>(h, Lw.stats_a_min);
     int32_t* aline = at<int32_t>(h, Lw.line_a);
     const int64_t t = Lw.blocks, nr = io.nr;
-    const int64_t rec = 2 * t * nr + nr;
     const bool native_only = o.mode == ADPB200_MODE_NATIVE;
     const int64_t mn = std::min(std::min(P.tm, P.tn), P.tk);
     const bool esc_expected = (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
                               mn >= o.min_dim;
+    // certified ESC: each slab record also carries the slab's indicator plane over
+    // the first kw positions (blocked [k-block][nr][32 B]), all-gathered with the stats
+    const bool cert = o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected && cap >= 1 && P.K > 0;
+    const int64_t kw = std::min<int64_t>(P.K, kCertifyWindow), kwp = (kw + 31) / 32 * 32;
+    const int64_t rec0 = 2 * t * nr + nr;
+    const int64_t rec = rec0 + (o.esc_method == ADPB200_ESC_CERTIFIED ? nr * kwp / 4 : 0);
+    Plan* rplan = at<Plan>(h, Lw.rplan);
     const LineView bslab{P.b.ptr, nr, P.K, P.K, 1};
     if (phase == 1) {
         rc = cuda_check(cudaMemsetAsync(plan, 0, sizeof(Plan), st), "cudaMemsetAsync(plan)");
@@ -425,6 +430,13 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
             launch_stats(bslab, o.esc_block_len, io.bstats_local, io.bstats_local + t * nr, io.bstats_local + 2 * t * nr,
                          plan->counts + 3, &plan->exc, 2, 1, st, nl);
         }
+        if (cert) {
+            LineView bw = bslab;
+            bw.len = kw;
+            launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, 1);
+            launch_slice(bw, io.bstats_local + 2 * t * nr, reinterpret_cast<int8_t*>(io.bstats_local + rec0), nr,
+                         kwp * nr, 1, nullptr, rplan, 0, 1, st, nl, 1);
+        }
         tm.end(0);
         return cuda_check(cudaGetLastError(), "dist phase 1");
     }
@@ -433,13 +445,36 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
         if (esc_expected && P.M > 0)
             launch_esc(amax, amin, aline, io.bstats_all, io.bstats_all + t * nr, io.bstats_all + 2 * t * nr, P.M, P.N,
                        t, plan, &plan->esc_raw, &plan->esc_ran, st, nl, nr, rec);
+        if (cert && P.M > 0) {
+            // this rank's rows against every column: B indicator planes from the
+            // all-gathered records, A's from the local rows, one INT8 count GEMM
+            int8_t* pa = at<int8_t>(h, Lw.planes_a);
+            int8_t* pb = at<int8_t>(h, Lw.planes_b);
+            launch_gather_planes(reinterpret_cast<const int8_t*>(io.bstats_all), rec * 4, rec0 * 4, io.world, nr,
+                                 kwp / 32, 1, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, at<int32_t>(h, Lw.scale_b), st,
+                                 nl);
+            LineView aw = P.a;
+            aw.len = kw;
+            launch_slice(aw, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st, nl, 1);
+            GemmArgs g{};
+            g.plan = rplan;
+            g.M = P.M;
+            g.N = P.N;
+            g.K = kw;
+            g.scale_a = at<int32_t>(h, Lw.scale_a);
+            g.scale_b = at<int32_t>(h, Lw.scale_b);
+            g.alpha = 1.0;
+            g.partial = at<uint64_t>(h, Lw.partial);
+            g.zero_flag = &rplan->exc;
+            if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
+                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
+        }
         tm.end(1);
-        rc = cuda_check(cudaMemcpyAsync(io.xchg, &plan->exc, 8, cudaMemcpyDeviceToDevice, st), "export xchg");
-        return rc ? rc : cuda_check(cudaGetLastError(), "dist phase 2");
+        launch_dist_export(plan, rplan, io.xchg, cert ? 1 : 0, st, nl);
+        return cuda_check(cudaGetLastError(), "dist phase 2");
     }
     if (phase == 3) {
-        rc = cuda_check(cudaMemcpyAsync(&plan->exc, io.xchg, 8, cudaMemcpyDeviceToDevice, st), "import xchg");
-        if (rc) return rc;
+        launch_dist_import(plan, io.xchg, o.target_bits, cert ? 1 : 0, st, nl);
         tm.begin(2);
         launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, 0, trace, st, nl);
         tm.end(2);
@@ -947,7 +982,8 @@ int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* o
     const int64_t nr = n / world;
     const int64_t t = (k + o.esc_block_len - 1) / o.esc_block_len;
     const int64_t pitch = (int64_t)align_up(size_t(k), 32);
-    out[0] = 2 * t * nr + nr;
+    const int64_t kw = std::min<int64_t>(k, kCertifyWindow);
+    out[0] = 2 * t * nr + nr + (o.esc_method == ADPB200_ESC_CERTIFIED ? nr * ((kw + 31) / 32 * 32) / 4 : 0);
     out[1] = slab_hdr(nr);
     out[2] = pitch * nr;
     out[3] = out[1] + int64_t(plane_cap(o, 0, 0)) * out[2];
@@ -962,6 +998,14 @@ int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int
     int rc = adpb200_validate_options(&o);
     if (rc) return rc;
     DecideInput in{xchg[0] & 1, (xchg[0] >> 1) & 1, m_global, n, k, xchg[1]};
+    // the certified ESC as dist_import_kernel applies it on every rank
+    const int64_t mn = std::min(std::min(m_global, n), k);
+    const bool esc_expected =
+        (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) && mn >= o.min_dim;
+    const int delta = certify_delta(o.target_bits);
+    if (o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected && !(xchg[0] & kXchgCertFail) && delta >= 0 &&
+        in.esc_bits > 2 * delta + 1)
+        in.esc_bits = 2 * delta + 1;
     DecideOutput d = decide(in, o);
     out[0] = d.path;
     out[1] = d.path == ADPB200_PATH_EMULATED ? d.slices : 0;

@@ -67,6 +67,20 @@ __host__ __device__ inline int required_slices(int target_bits, int esc_bits) {
 // decide() (adp.cpp:46-96): identical gate order and FP64 cost model. Every
 // FP64 operation is written as an explicitly rounded intrinsic on the device
 // (no FMA contraction, matching -ffp-contract=off of the reference build).
+// Certified ESC (adpb200_options.esc_method): the indicator threshold delta for
+// s0 = required_slices(target_bits, 0), the fewest slices any input gets; 2 delta + 1
+// is the largest ESC s0 tolerates (-1: no certificate can help).
+__host__ __device__ inline int certify_delta(int target_bits) {
+    const int s0 = (target_bits + 2 + 7) / 8;
+    const int e0 = 8 * s0 - target_bits - 2;
+    return e0 >= 1 ? (e0 - 1) / 2 : -1;
+}
+// Multi-GPU exchange word 0 (max-reduced): exceptional bits 0-1, and with the
+// certified ESC this flag when some rank saw a zero indicator count or an
+// exceptional input (max-reduction keeps it set, and keeps the bits of an
+// exceptional rank because that rank sets the flag too).
+constexpr int32_t kXchgCertFail = 256;
+
 __host__ __device__ inline DecideOutput decide(const DecideInput& in, const adpb200_options& c) {
     DecideOutput d{ADPB200_PATH_NATIVE, ADPB200_REASON_OK, 0, 0, -1, 0.0};
     if (c.mode == ADPB200_MODE_NATIVE) {

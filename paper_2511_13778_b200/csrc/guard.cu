@@ -504,19 +504,17 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
 
 // ---- certified ESC ----------------------------------------------------------------
 // s0 = required_slices(target_bits, 0) is the fewest slices any input can get;
-// it tolerates esc <= e0 = 8 s0 - target_bits - 2. If some l has
+// it tolerates esc <= e0 = 8 s0 - target_bits - 2 (certify_delta). If some l has
 // e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta, the exact
 // largest product exponent z_ij (esc.cpp:61-87) is >= rowmax_i + colmax_j -
 // 2 delta, so span_ij <= 2 delta + 1. delta = (e0 - 1) / 2 makes that span
 // fit s0. The "some l" test for every (i, j) is one INT8 GEMM of 0/1 planes.
-__global__ void certify_prep_kernel(const Plan* plan, Plan* rplan, int target_bits, int64_t k) {
+__global__ void certify_prep_kernel(const Plan* plan, Plan* rplan, int target_bits, int64_t k, int force) {
     Plan r{};
     r.path = kPathDone;
-    const int s0 = (target_bits + 2 + 7) / 8;
-    const int e0 = 8 * s0 - target_bits - 2;
-    const int delta = e0 >= 1 ? (e0 - 1) / 2 : -1;
-    if (plan->esc_ran && plan->exc == 0 && delta >= 0 && plan->esc_raw > 2 * delta + 1 && k > 0 &&
-        k <= (int64_t(1) << 30)) {
+    const int delta = certify_delta(target_bits);
+    const bool wanted = force || (plan->esc_ran && plan->exc == 0 && plan->esc_raw > 2 * delta + 1);
+    if (wanted && delta >= 0 && k > 0 && k <= (int64_t(1) << 30)) {
         r.path = ADPB200_PATH_EMULATED;
         r.slices = 1;
         r.L = 0;
@@ -535,14 +533,43 @@ __global__ void certify_finish_kernel(Plan* plan, const Plan* rplan) {
     if (rplan->path == ADPB200_PATH_EMULATED && rplan->exc == 0) plan->esc_raw = 2 * rplan->aux + 1;
 }
 
+__global__ void dist_export_kernel(const Plan* plan, const Plan* rplan, int32_t* xchg, int certified) {
+    int32_t x0 = plan->exc;
+    if (certified && (plan->exc != 0 || (rplan->path == ADPB200_PATH_EMULATED && rplan->exc != 0)))
+        x0 |= kXchgCertFail;
+    xchg[0] = x0;
+    xchg[1] = plan->esc_raw;
+}
+
+__global__ void dist_import_kernel(Plan* plan, const int32_t* xchg, int target_bits, int certified) {
+    const int32_t x0 = xchg[0];
+    plan->exc = x0 & 3;
+    plan->esc_raw = xchg[1];
+    const int delta = certify_delta(target_bits);
+    if (certified && !(x0 & kXchgCertFail) && delta >= 0 && plan->esc_raw > 2 * delta + 1)
+        plan->esc_raw = 2 * delta + 1;
+}
+
 void launch_certify_prep(const Plan* plan, Plan* rplan, int target_bits, int64_t k, cudaStream_t st,
-                         uint64_t* nlaunch) {
-    certify_prep_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits, k);
+                         uint64_t* nlaunch, int force) {
+    certify_prep_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits, k, force);
     ++*nlaunch;
 }
 
 void launch_certify_finish(Plan* plan, const Plan* rplan, cudaStream_t st, uint64_t* nlaunch) {
     certify_finish_kernel<<<1, 1, 0, st>>>(plan, rplan);
+    ++*nlaunch;
+}
+
+void launch_dist_export(const Plan* plan, const Plan* rplan, int32_t* xchg, int certified, cudaStream_t st,
+                        uint64_t* nlaunch) {
+    dist_export_kernel<<<1, 1, 0, st>>>(plan, rplan, xchg, certified);
+    ++*nlaunch;
+}
+
+void launch_dist_import(Plan* plan, const int32_t* xchg, int target_bits, int certified, cudaStream_t st,
+                        uint64_t* nlaunch) {
+    dist_import_kernel<<<1, 1, 0, st>>>(plan, xchg, target_bits, certified);
     ++*nlaunch;
 }
 

@@ -102,6 +102,12 @@ def test_dist_decision_matches_decide():
     # the fast policy gathers s planes, the variant follows the diagonal count
     assert dist_decision([0, 1], 8192, 8192, 8192, AdpConfig(pair_limit=PAIRS_TARGET)) == (0, 7, 7, 64)
     assert dist_decision([0, 8], 8192, 8192, 8192, AdpConfig(pair_limit=PAIRS_TARGET)) == (0, 8, 8, 48)
+    # certified ESC: applied unless some rank flagged a zero count (256); exceptional still wins
+    cc = AdpConfig(pair_limit=PAIRS_TARGET, esc_method="certified")
+    assert dist_decision([0, 8], 8192, 8192, 8192, cc) == (0, 7, 7, 64)
+    assert dist_decision([256, 8], 8192, 8192, 8192, cc) == (0, 8, 8, 48)
+    assert dist_decision([257, 8], 8192, 8192, 8192, cc)[0] == 1
+    assert dist_decision([0, 8], 100, 8192, 8192, cc) == (1, 0, 0, 0)  # too small: no ESC, no certificate
 
 
 def _collective_worker(rank, world, port, results):

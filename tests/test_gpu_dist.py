@@ -44,7 +44,7 @@ def run_virtual(gens):
 
 
 def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3,
-              overlap=True):
+              overlap=True, zero_row=None):
     from paper_2511_13778_b200 import Handle
     from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
 
@@ -57,6 +57,11 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
     Ct = torch.rand((n, m), generator=g, device="cuda", dtype=torch.float64)
     if poison is not None:
         Bt[poison] = float("nan")
+    if zero_row is not None:  # row i of op(A) all zeros
+        if transa == "N":
+            Ast[:, zero_row] = 0.0
+        else:
+            Ast[zero_row, :] = 0.0
     ref = Ct.clone()
     lda = m if transa == "N" else k
     gpu.dgemm(transa, "N", m, n, k, alpha, Ast, lda, Bt, k, beta, ref, m, cfg)
@@ -123,3 +128,24 @@ def test_dist_forced_and_native_modes(gpu):
         got, ref, res = dist_case(gpu, 2, 512, 256, 512, cfg)
         assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
 
+
+
+@pytest.mark.parametrize("world,m,n,k", [(2, 640, 384, 512), (4, 1000, 512, 768), (3, 900, 384, 1536)])
+def test_dist_certified_esc(gpu, world, m, n, k):
+    """Certified ESC across ranks: B indicator planes travel with the slab stats,
+    each rank certifies its rows, the fail flag rides the max-allreduce; the
+    decision and C equal the single-GPU certified dgemm bitwise."""
+    cfg = gpu.AdpConfig(pair_limit=gpu.PAIRS_TARGET, esc_method="certified")
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, alpha=0.75, beta=-0.5)
+    assert all(r == res[0] for r in res)
+    assert res[0][0] == 0 and res[0][1] == 7
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    # one zero row on the last rank: its certificate fails, so every rank keeps the coarsened s
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, zero_row=m - 2)
+    assert all(r == res[0] for r in res)
+    assert res[0][0] == 0 and res[0][1] > 7
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    # NaN in a slab: native everywhere
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 5))
+    assert all(r[0] == 1 for r in res)
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
