@@ -200,8 +200,10 @@ struct HostOut {
 // counts per (i, j) the positions where both are on, and no zero count lowers
 // plan->esc_raw to 2 delta + 1 (guard.cu: certify_prep_kernel). Stream-ordered,
 // predicated on the coarsened result: nothing runs when it already gives s0.
+// rows_mode: a rank of the row partition (adpb200_dgemm_rows) certifies its rows
+// whatever its own coarsened result; the flag travels in the exchange word.
 int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, const Layout& Lw, Plan* plan,
-                cudaStream_t st) {
+                cudaStream_t st, bool rows_mode = false) {
     uint64_t* nl = &h->launches;
     Plan* rplan = at<Plan>(h, Lw.rplan);
     int8_t* pa = at<int8_t>(h, Lw.planes_a);
@@ -212,7 +214,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
     LineView va = P.a, vb = P.b;
     va.len = kw;
     vb.len = kw;
-    launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl);
+    launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, rows_mode ? 1 : 0);
     launch_slice(va, at<int32_t>(h, Lw.line_a), pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st,
                  nl, 1);
     launch_slice(vb, at<int32_t>(h, Lw.line_b), pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, nullptr, rplan, 0, 1, st,
@@ -229,7 +231,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
     g.zero_flag = &rplan->exc;
     if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, Lw.cap, g, st, nl))
         return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
-    launch_certify_finish(plan, rplan, st, nl);
+    if (!rows_mode) launch_certify_finish(plan, rplan, st, nl);
     return ADPB200_OK;
 }
 
@@ -286,16 +288,19 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     if (esc_expected && phase != 2)
         launch_esc(amax, amin, aline, bmax, bmin, bline, P.M, P.N, Lw.blocks, plan, &plan->esc_raw, &plan->esc_ran,
                    st, nl);
-    if (phase == 0 && certify_wanted(P, o, esc_expected, cap) && (rc = run_certify(h, P, o, Lw, plan, st))) return rc;
+    const bool cert = phase != 2 && certify_wanted(P, o, esc_expected, cap);
+    if (cert && (rc = run_certify(h, P, o, Lw, plan, st, phase == 1))) return rc;
     tm.end(1);
-    static_assert(offsetof(Plan, esc_raw) == offsetof(Plan, exc) + 4, "xchg layout");
     if (phase == 1) {
-        rc = cuda_check(cudaMemcpyAsync(xchg, &plan->exc, 8, cudaMemcpyDeviceToDevice, st), "export xchg");
-        return rc ? rc : cuda_check(cudaGetLastError(), "launch");
+        launch_dist_export(plan, at<Plan>(h, Lw.rplan), xchg, cert ? 1 : 0, st, nl);
+        return cuda_check(cudaGetLastError(), "launch");
     }
     if (phase == 2) {
-        rc = cuda_check(cudaMemcpyAsync(&plan->exc, xchg, 8, cudaMemcpyDeviceToDevice, st), "import xchg");
-        if (rc) return rc;
+        // the same certified-ESC rule on every rank (global dimensions only)
+        const bool cert_global = o.esc_method == ADPB200_ESC_CERTIFIED && fixed_slices <= 0 &&
+                                 (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
+                                 mn >= o.min_dim && cap >= 1;
+        launch_dist_import(plan, xchg, o.target_bits, cert_global ? 1 : 0, st, nl);
     }
     // decision
     tm.begin(2);
