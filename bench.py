@@ -48,6 +48,10 @@ def parse():
     p.add_argument("--esc", choices=["coarsened", "certified"], default="coarsened",
                    help="ESC method of the timed calls: the reference's coarsened ESC (default) or the "
                         "certified ESC option (single-GPU paths)")
+    p.add_argument("--dist", choices=["fused", "allgather"], default="fused",
+                   help="N > 1: fused = the GEMM reads every rank's B planes in place over NVLink (CUDA IPC "
+                        "peer mappings, phase 7); allgather = NCCL all-gather of the planes overlapped with "
+                        "the own-column GEMM (phases 5/6)")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
@@ -246,10 +250,18 @@ def main():
     Ct = torch.zeros((n, m), device=dev, dtype=torch.float64)                  # C: m x n col-major
     cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET, esc_method=args.esc)
     trace_buf = torch.zeros(_lib.TRACE_BYTES, dtype=torch.uint8, device=dev)
+    peers, dist_mode = None, args.dist if world > 1 else None
+    if world > 1 and args.dist == "fused":
+        from paper_2511_13778_b200.dist import PeerSlabs
+
+        try:  # slab buffers sized for the largest plane count any config here can ask for
+            peers = PeerSlabs(n, k, adp.AdpConfig(), device=dev.index)
+        except Exception as e:  # noqa: BLE001 — no IPC / peer access: fall back to the NCCL all-gather
+            dist_mode = f"allgather (fused unavailable: {str(e)[:120]})"
 
     def step(config=cfg, A=At, B=Bt, Cm=Ct, trace=None):
         if world > 1:
-            dgemm_dist("N", m_global, m, n, k, 1.0, A, m, B, 0.0, Cm, m, config, handle, trace=trace)
+            dgemm_dist("N", m_global, m, n, k, 1.0, A, m, B, 0.0, Cm, m, config, handle, trace=trace, peers=peers)
         else:
             adp.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
 
@@ -475,7 +487,8 @@ def main():
     if rank == 0:
         line = {
             "metric": "effective FP64 TFLOP/s (2mnk/t) of ADP DGEMM, 55-bit, "
-                      + ("32768^3 (BASELINE config 4)" if c4 else "8192^3"),
+                      + ("32768^3 (BASELINE config 4)" if c4 else
+                         ("8192^3" if (m, n, k) == (8192, 8192, 8192) else f"{m}x{n}x{k} per GPU")),
             "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong" if c4 else "weak", "vs_baseline": None,
             "dtype": "f64",
@@ -487,7 +500,10 @@ def main():
                        "m": m_global, "n": n, "k": k, "slices": trace.slices, "esc_bits": trace.esc_bits,
                        "path": trace.path, "pairs": pairs, "gemm_variant": trace.gemm_variant,
                        "parallelism": (f"row-block x{world}: A/C rows per rank, B column slabs; B exponent "
-                                       "stats + slice planes all-gathered, ADP decision max-allreduced (NCCL)")
+                                       "stats all-gathered, ADP decision max-allreduced (NCCL); B slice planes: "
+                                       + ("read in place by the GEMM over NVLink (fused phase 7)" if peers is not None
+                                          else "NCCL all-gather overlapped with the own-column GEMM")
+                                       + f" [--dist {dist_mode}]")
                        if world > 1 else "single GPU",
                        "esc_method": args.esc,
                        "l2": f"inputs larger than L2 ({m * k * 8 >> 20} MiB per operand, L2 126 MB)"},

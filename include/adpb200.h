@@ -198,9 +198,25 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
  *            (no-op when nsl = 0) — issue it, then wait for the all-gather;
  *   phase 6  gathered = all records: place them and run every other n-tile
  *            (or, when nsl = 0, the native GEMM against the gathered B).
+ * Fused alternative to phases 4-6 (no plane all-gather at all, nsl > 0 only):
+ *   phase 7  gathered = HOST array of `world` device pointers, entry r = rank
+ *            r's `slab` buffer as mapped in this process (cudaIpcOpenMemHandle
+ *            or peer access over NVLink; entry `rank` = the local slab). The
+ *            GEMM's TMA loads read each rank's B planes in place, tile by tile
+ *            (rank r's columns tiled on their own), and the epilogue reads the
+ *            scales from the record headers. Every rank must be past phase 3
+ *            before any rank starts phase 7, and slabs must stay untouched
+ *            until every rank has finished it (two barriers). world <= 8.
  * Same decision and slice count on every rank: the assembled C is
  * bit-identical to the single-GPU adpb200_dgemm('N'/transa, 'N'). */
 int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]);
+/* Slab buffers for phase 7, shared between the ranks' processes over CUDA IPC
+ * (NVLink peer mappings): alloc exports a cudaMalloc'd buffer's 64-byte handle,
+ * open maps a peer's handle (lazy peer access), close / free release them. */
+int adpb200_ipc_alloc(int device, int64_t bytes, void** ptr, uint8_t handle[64]);
+int adpb200_ipc_open(int device, const uint8_t handle[64], void** ptr);
+int adpb200_ipc_close(void* ptr);
+int adpb200_ipc_free(void* ptr);
 /* decide() on the reduced xchg (host copy): out = path, slices, nsl (planes to
  * gather; 0 on the native path), GEMM variant. */
 int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global,

@@ -108,6 +108,10 @@ def lib() -> C.CDLL:
         "adpb200_dist_decision": (C.c_int, [popt, C.POINTER(i32), i64, i64, i64, C.POINTER(i32)]),
         "adpb200_dgemm_dist": (C.c_int, [vp, C.c_int, i64, C.c_int, C.c_int, C.c_char, i64, i64, i64, f64, vp, i64,
                                          vp, f64, vp, i64, popt, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
+        "adpb200_ipc_alloc": (C.c_int, [C.c_int, i64, C.POINTER(vp), C.POINTER(C.c_uint8)]),
+        "adpb200_ipc_open": (C.c_int, [C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)]),
+        "adpb200_ipc_close": (C.c_int, [vp]),
+        "adpb200_ipc_free": (C.c_int, [vp]),
         "adpb200_geqrf_blocked": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, popt, vp]),
         "adpb200_qr_materialize_q": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "adpb200_qr_residual": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
@@ -133,7 +137,8 @@ EXPORTED = (
     "adpb200_adp_gemm_host", "adpb200_scan", "adpb200_block_stats",
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",
     "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read",
-    "adpb200_dist_sizes", "adpb200_dist_decision", "adpb200_dgemm_dist",
+    "adpb200_dist_sizes", "adpb200_dist_decision", "adpb200_dgemm_dist", "adpb200_ipc_alloc",
+    "adpb200_ipc_open", "adpb200_ipc_close", "adpb200_ipc_free",
     "adpb200_geqrf_blocked", "adpb200_qr_materialize_q", "adpb200_qr_residual",
     "adpb200_dd_gemm", "adpb200_error_report", "adpb200_gen_uniform_rect", "adpb200_gen_test2",
 )

@@ -497,6 +497,30 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     // tiles that only need this rank's own B columns (phase 5, `gathered` = own slab
     // record), the other tiles follow once the records are in (phase 6)
     if (phase >= 4 && P.M == 0) return ADPB200_OK;  // no rows on this rank: nothing to compute
+    if (phase == 7) {
+        // fused all-gather -> GEMM: the GEMM's TMA reads every rank's slab record in
+        // place (peer memory over NVLink), tile by tile; no gathered copy, no NCCL
+        GemmArgs g{};
+        g.plan = plan;
+        g.M = P.M;
+        g.N = P.N;
+        g.K = P.K;
+        g.scale_a = at<int32_t>(h, Lw.scale_a);
+        g.alpha = P.alpha;
+        g.beta = P.beta;
+        g.c_out = P.c_out;
+        g.ldc = P.ldc;
+        g.c_in = P.c_in;
+        g.ldc_in = P.ldc_in;
+        g.partial = at<uint64_t>(h, Lw.partial);
+        tm.begin(4);
+        const int prc = launch_igemm_peer(at<int8_t>(h, Lw.planes_a), Lw.slots_a, Lw.pitch / 32, cap,
+                                          static_cast<const int8_t* const*>(io.gathered), io.world, nr, slab_hdr(nr),
+                                          io.nsl, g, st, nl);
+        tm.end(4);
+        if (prc) return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the peer slab planes");
+        return cuda_check(cudaGetLastError(), "dist phase 7");
+    }
     if ((phase == 5 || phase == 6) && io.nsl > 0) {
         int8_t* pa = at<int8_t>(h, Lw.planes_a);
         int8_t* pb = at<int8_t>(h, Lw.planes_b);
@@ -995,6 +1019,36 @@ int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* o
     return ADPB200_OK;
 }
 
+int adpb200_ipc_alloc(int device, int64_t bytes, void** ptr, uint8_t handle[64]) {
+    if (!ptr || !handle || bytes <= 0) return fail(3, "ipc_alloc: bad arguments");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (!rc) rc = cuda_check(cudaMalloc(ptr, size_t(bytes)), "cudaMalloc(ipc)");
+    if (rc) return rc;
+    cudaIpcMemHandle_t hd;
+    rc = cuda_check(cudaIpcGetMemHandle(&hd, *ptr), "cudaIpcGetMemHandle");
+    if (rc) {
+        cudaFree(*ptr);
+        *ptr = nullptr;
+        return rc;
+    }
+    memcpy(handle, &hd, 64);
+    return ADPB200_OK;
+}
+
+int adpb200_ipc_open(int device, const uint8_t handle[64], void** ptr) {
+    if (!ptr || !handle) return fail(3, "ipc_open: bad arguments");
+    int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    if (rc) return rc;
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, handle, 64);
+    return cuda_check(cudaIpcOpenMemHandle(ptr, hd, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int adpb200_ipc_close(void* ptr) { return cuda_check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); }
+
+int adpb200_ipc_free(void* ptr) { return cuda_check(cudaFree(ptr), "cudaFree(ipc)"); }
+
 int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global, int64_t n, int64_t k,
                           int32_t out[4]) {
     adpb200_options o;
@@ -1032,7 +1086,9 @@ int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world,
                        int32_t* bstats_local, const int32_t* bstats_all, int32_t* xchg, int8_t* slab,
                        const void* gathered, int nsl, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_dist: null handle");
-    if (phase < 1 || phase > 6) return fail(3, "dgemm_dist: phase must be 1..6");
+    if (phase < 1 || phase > 7) return fail(3, "dgemm_dist: phase must be 1..7");
+    if (phase == 7 && (world > kMaxPeers || nsl < 1))
+        return fail(3, "dgemm_dist: phase 7 needs world <= 8 and nsl >= 1 (emulated path)");
     if (rank < 0 || rank >= world) return fail(3, "dgemm_dist: rank out of range");
     adpb200_options o;
     if (opt) o = *opt;

@@ -300,6 +300,7 @@ constexpr int kMaxBox = 18;
 struct PlaneMaps {
     CUtensorMap a[kMaxBox];
     CUtensorMap b[kMaxBox];
+    CUtensorMap bp[kMaxPeers];  // fused peer mode: rank r's slab planes, box of nsl slices
 };
 
 struct alignas(16) SmemSched {
@@ -448,6 +449,9 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
     const int64_t nt_end = g.nt_end > 0 && g.nt_end < nt_total ? g.nt_end : nt_total;
     const int64_t nt_off = g.nt_begin;
     lp.tiles_n = nt_end > nt_off ? nt_end - nt_off : 0;
+    // fused peer mode: every rank's columns tiled on their own
+    const int64_t peer_tpr = g.peer_world > 0 ? (g.peer_nr + NB - 1) / NB : 0;
+    if (g.peer_world > 0) lp.tiles_n = g.peer_world * peer_tpr;
     lp.ntiles = lp.tiles_m * lp.tiles_n;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
     const CUtensorMap* map_b = &maps.b[boxed ? nsl - 1 : 0];
     if (warp == 0 && lane == 0) {
         tc::tma_prefetch(map_a);
-        tc::tma_prefetch(map_b);
+        if (g.peer_world == 0) tc::tma_prefetch(map_b);
     }
     if (warp == C::kAllocWarp) tc::tmem_alloc(&hdr->tmem_slot, 512);
     tc::fence_before();
@@ -505,7 +509,13 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                     tc::mbar_expect_tx(&hdr->full[stage], lp.stage_bytes);
                     // pre-swizzled blocked planes viewed as (128 B = 4 lines, line/4, k-block,
                     // slice): a stage is one linear box per operand, 128-byte requests
-                    if (boxed) {
+                    if (g.peer_world > 0) {
+                        // B straight from the owning rank's slab record (NVLink peer memory)
+                        const int r = int(nt / peer_tpr);
+                        tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
+                        tc::tma_load_4d(sb, &maps.bp[r], &hdr->full[stage], 0, int((nt - r * peer_tpr) * (NB / 4)),
+                                        int(kb), 0);
+                    } else if (boxed) {
                         tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
                         tc::tma_load_4d(sb, map_b, &hdr->full[stage], 0, int(nt * (NB / 4)), int(kb), 0);
                     } else {
@@ -545,10 +555,20 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
             const int64_t row = mt * kBM + q * 32 + lane;
             const bool row_ok = row < g.M;
             const int ea = row_ok ? g.scale_a[row] : 0;
-            // the warp's column scales, one per lane (kCols <= 32), fetched before
+            // tile columns [col_base, col_base + NB), valid below col_end; the
+            // warp's column scales, one per lane (kCols <= 32), fetched before
             // waiting for the accumulators and shuffled out per element
-            const int64_t lane_col = nt * NB + jh * kCols + lane;
-            const int eb_lane = (lane < kCols && lane_col < g.N) ? __ldg(g.scale_b + lane_col) : 0;
+            int64_t col_base = nt * NB, col_end = g.N, scol0 = 0;
+            const int32_t* sbase = g.scale_b;
+            if (g.peer_world > 0) {
+                const int r = int(nt / peer_tpr);
+                col_base = r * g.peer_nr + (nt - r * peer_tpr) * NB;
+                col_end = (r + 1) * g.peer_nr < g.N ? (r + 1) * g.peer_nr : g.N;
+                sbase = g.peer_scale[r];  // rank r's record header: its columns' scales
+                scol0 = r * g.peer_nr;
+            }
+            const int64_t lane_col = col_base + jh * kCols + lane;
+            const int eb_lane = (lane < kCols && lane_col < col_end) ? __ldg(sbase + (lane_col - scol0)) : 0;
             for (int c = 0; c < lp.nchunks; ++c) {
                 tc::mbar_wait(&hdr->tmem_full, acc_phase);
                 tc::fence_after();
@@ -567,8 +587,8 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                             tc::tmem_wait_ld();
 #pragma unroll
                             for (int cc = 0; cc < 8; ++cc) {
-                                const int64_t col = nt * NB + jh * kCols + b * 8 + cc;
-                                if (row_ok && col < g.N && v[cc] == 0u) zero = true;
+                                const int64_t col = col_base + jh * kCols + b * 8 + cc;
+                                if (row_ok && col < col_end && v[cc] == 0u) zero = true;
                             }
                         }
                         tc::fence_before();
@@ -629,8 +649,8 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
 #pragma unroll
                         for (int jl = 0; jl < kCols; ++jl) {
                             const int ebj = __shfl_sync(0xffffffffu, eb_lane, jl);
-                            const int64_t col = nt * NB + jh * kCols + jl;
-                            if (!row_ok || col >= g.N || (g.debug & 2)) continue;
+                            const int64_t col = col_base + jh * kCols + jl;
+                            if (!row_ok || col >= col_end || (g.debug & 2)) continue;
                             uint64_t S[2];
                             S[0] = uint64_t(w[jl][0]) | (uint64_t(w[jl][1]) << 32);
                             if constexpr (kW == 3)
@@ -680,8 +700,8 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                     }
 #pragma unroll
                     for (int cc = 0; cc < C::kCW; ++cc) {
-                        const int64_t col = nt * NB + j0 + cc;
-                        if (!row_ok || col >= g.N || (g.debug & 2)) continue;
+                        const int64_t col = col_base + j0 + cc;
+                        if (!row_ok || col >= col_end || (g.debug & 2)) continue;
                         if (g.dump) {
                             int64_t* dst = g.dump + (row * g.N + col) * g.ndump;
 #pragma unroll
@@ -900,6 +920,71 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
                 nb, t / grid, 100.0 * wt / t, 100.0 * wf / t, 100.0 * wh / t, 100.0 * ho / t);
     }
     return 0;
+}
+
+namespace {
+struct PeerCacheEntry {
+    const int8_t* pa = nullptr;
+    const int8_t* peers[kMaxPeers] = {};
+    int64_t slots_a = -1, nkb = -1, nr = -1, hdr = -1;
+    int cap = -1, world = -1, nsl = -1;
+    PlaneMaps maps;
+};
+
+template <int NB>
+int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap,
+                   const int8_t* const* peer_slabs, int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g,
+                   cudaStream_t st) {
+    bool hit = e.pa == planes_a && e.slots_a == slots_a && e.nkb == nkb && e.cap == cap && e.world == world &&
+               e.nr == nr && e.hdr == hdr && e.nsl == nsl;
+    for (int r = 0; hit && r < world; ++r) hit = e.peers[r] == peer_slabs[r];
+    if (!hit) {
+        const int nbox = cap < kMaxBox ? cap : kMaxBox;
+        for (int i = 0; i < kMaxBox; ++i)
+            if (!encode_plane_map(&e.maps.a[i], planes_a, slots_a, nkb, cap, kBM, i < nbox ? i + 1 : 1)) return -1;
+        for (int r = 0; r < world; ++r)
+            if (!encode_plane_map(&e.maps.bp[r], peer_slabs[r] + hdr, nr, nkb, cap, NB, nsl)) return -1;
+        e.pa = planes_a;
+        e.slots_a = slots_a;
+        e.nkb = nkb;
+        e.cap = cap;
+        e.world = world;
+        e.nr = nr;
+        e.hdr = hdr;
+        e.nsl = nsl;
+        for (int r = 0; r < world; ++r) e.peers[r] = peer_slabs[r];
+    }
+    GemmArgs a = g;
+    a.peer_world = world;
+    a.peer_nr = nr;
+    for (int r = 0; r < world; ++r) a.peer_scale[r] = reinterpret_cast<const int32_t*>(peer_slabs[r]);
+    a.nt_begin = a.nt_end = 0;
+    a.debug = 0;
+    a.smem_bytes = kGemmSmemBytes;
+    const int64_t mt_total = (g.M + kBM - 1) / kBM;
+    const int64_t mt_end = g.mt_end > 0 && g.mt_end < mt_total ? g.mt_end : mt_total;
+    const int64_t tiles = (mt_end - g.mt_begin) * world * ((nr + NB - 1) / NB);
+    const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    if (grid < 1) return 0;
+    set_attr_once<NB>();
+    igemm_kernel<NB><<<grid, Cfg<NB>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+    return 0;
+}
+}  // namespace
+
+int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap, const int8_t* const* peer_slabs,
+                      int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g, cudaStream_t st,
+                      uint64_t* nlaunch) {
+    if (world < 1 || world > kMaxPeers || nsl < 1 || nsl > cap || nsl > kMaxBox || nr % 8 != 0) return -2;
+    static thread_local PeerCacheEntry cache[5];
+    int rc = 0;
+    if (!rc) rc = launch_peer_nb<64>(cache[0], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<48>(cache[1], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<32>(cache[2], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<16>(cache[3], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    *nlaunch += 5;
+    return rc;
 }
 
 }  // namespace adpb200

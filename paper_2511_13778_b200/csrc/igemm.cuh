@@ -12,6 +12,8 @@ constexpr size_t kPartialBytesPerCta = 131072;
 
 // Internal problem: C(i, j) = sum_l A(i, l) B(l, j), i < M (A-lines), j < N
 // (B-lines), both operands sliced K-major into planes [slice][line][pitch].
+constexpr int kMaxPeers = 8;  // ranks whose slab records one fused GEMM can read
+
 struct GemmArgs {
     const Plan* plan;
     int64_t M, N, K;
@@ -30,7 +32,20 @@ struct GemmArgs {
     int64_t mt_begin, mt_end;  // 128-row m-tile range to compute (mt_end 0 = all)
     int64_t nt_begin, nt_end;  // NB-column n-tile range to compute (nt_end 0 = all)
     int32_t* zero_flag;        // certified ESC: no C; set to 1 if any (i, j) has a zero diagonal-0 count
+    // fused all-gather -> GEMM (multi-GPU phase 7): B planes and scales read in place
+    // from every rank's slab record over peer memory; rank r owns columns
+    // [r*peer_nr, (r+1)*peer_nr), tiled on its own (partial last tile per rank)
+    int peer_world;            // 0: B from planes_b
+    int64_t peer_nr;
+    const int32_t* peer_scale[kMaxPeers];
 };
+
+// Fused peer variant of launch_igemm: B from world slab records ([scale int32 x nr |
+// pad to hdr][cap planes of nkb x nr x 32 B], peer_slabs[r] = rank r's record as
+// mapped in this process), nsl planes each. Launches every variant (one does work).
+int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap, const int8_t* const* peer_slabs,
+                      int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g, cudaStream_t st,
+                      uint64_t* nlaunch);
 
 // nb in {64, 32, 16, 8}; the kernel returns immediately unless plan->variant == nb.
 // planes_a / planes_b: blocked, pre-swizzled slice planes (cap planes of nkb

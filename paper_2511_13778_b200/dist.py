@@ -18,7 +18,7 @@ assembled C is bit-identical to the single-GPU result.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Optional, Tuple
+from typing import Optional, Sequence, Tuple
 
 import torch
 import torch.distributed as dist
@@ -43,7 +43,12 @@ def rows_of(rank: int, world: int, m: int, align: int = 128) -> Tuple[int, int]:
 def reduce_xchg(xchg: torch.Tensor, group=None) -> None:
     """Max-reduce the guardrail exchange block over the ranks (in place)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(xchg, op=dist.ReduceOp.MAX, group=group)
+        if dist.get_backend(group) == "gloo" and xchg.is_cuda:
+            t = xchg.cpu()
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            xchg.copy_(t)
+        else:
+            dist.all_reduce(xchg, op=dist.ReduceOp.MAX, group=group)
 
 
 def dgemm_rows(transa: str, transb: str, m_global: int, m: int, n: int, k: int, alpha: float, A: torch.Tensor,
@@ -99,7 +104,8 @@ def dist_decision(xchg_host, m_global: int, n: int, k: int, config: Optional[Adp
 def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
                      A: torch.Tensor, lda: int, B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int,
                      config: Optional[AdpConfig] = None, handle: Optional[Handle] = None,
-                     trace: Optional[torch.Tensor] = None, rank: int = 0, overlap: bool = True):
+                     trace: Optional[torch.Tensor] = None, rank: int = 0, overlap: bool = True,
+                     slab_ptrs: Optional[Sequence[int]] = None):
     """The B-distributed ADP DGEMM of one rank as a generator of collective
     requests, so that the same orchestration runs under torch.distributed
     (dgemm_dist) and under a single-process multi-rank driver (the tests):
@@ -111,6 +117,12 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
 
     With overlap (default) the B-plane all-gather runs while the GEMM tiles that
     need only this rank's own B columns compute (phases 5 and 6).
+
+    With slab_ptrs (every rank's slab buffer as mapped in this process, entry
+    `rank` its own: PeerSlabs over CUDA IPC, or plain buffers of one device in
+    the tests) there is no plane all-gather: after a barrier the fused phase 7
+    GEMM reads the B planes of every rank in place over peer memory
+        ("barrier",)               every rank past its phase 3 (slab sliced)
 
     Rank owns rows of op(A) / C (column-major local block, ldc) and the B
     column slab B_slab (k x n/world column-major, compact: a (n/world, k)
@@ -124,21 +136,28 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     bl = torch.empty(nrec, dtype=torch.int32, device=dev)
     ba = torch.empty(nrec * world, dtype=torch.int32, device=dev)
     xchg = torch.zeros(2, dtype=torch.int32, device=dev)
-    slab = torch.empty(cap_bytes, dtype=torch.int8, device=dev)
+    fused = slab_ptrs is not None
+    slab = None if fused else torch.empty(cap_bytes, dtype=torch.int8, device=dev)
+    slab_p = C.c_void_p(int(slab_ptrs[rank])) if fused else _ptr(slab)
     st = _stream(dev)
     tr = None if trace is None else C.c_void_p(trace.data_ptr())
 
     def phase(p, gathered=None, nsl=0):
         check(lib().adpb200_dgemm_dist(handle.h, p, m_global, world, rank, transa.encode()[:1], m, n, k, float(alpha),
                                        _ptr(A), lda, _ptr(B_slab), float(beta), _ptr(C_), ldc, C.byref(o), tr,
-                                       _ptr(bl), _ptr(ba), _ptr(xchg), _ptr(slab), gathered, int(nsl), st))
+                                       _ptr(bl), _ptr(ba), _ptr(xchg), slab_p, gathered, int(nsl), st))
 
     phase(1)
     yield ("all_gather", ba, bl)
     phase(2)
     yield ("all_reduce_max", xchg)
     phase(3)
-    path, s, nsl, _ = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)
+    path, s, nsl, _ = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)  # (syncs: slab sliced)
+    if nsl > 0 and fused:
+        yield ("barrier",)
+        ptrs = (C.c_void_p * world)(*[int(p) for p in slab_ptrs])
+        phase(7, C.cast(ptrs, C.c_void_p), nsl)
+        return (path, s, nsl)
     if nsl > 0:
         rec = hdr + nsl * plane_bytes
         gathered = torch.empty(rec * world, dtype=torch.int8, device=dev)
@@ -158,15 +177,71 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
 
 def dgemm_dist(transa: str, m_global: int, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
                B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int, config: Optional[AdpConfig] = None,
-               handle: Optional[Handle] = None, group=None, trace: Optional[torch.Tensor] = None):
+               handle: Optional[Handle] = None, group=None, trace: Optional[torch.Tensor] = None,
+               peers: Optional["PeerSlabs"] = None):
     """This rank's share of a row-partitioned ADP DGEMM with B distributed by
     column slabs: exponent stats and B slice planes all-gathered, the ADP
-    decision input max-allreduced, all over NCCL (torch.distributed)."""
+    decision input max-allreduced, all over NCCL (torch.distributed). With
+    `peers` (a PeerSlabs for this n, k) the plane all-gather is replaced by
+    the fused phase 7: the GEMM reads every rank's planes over NVLink."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     gen = dgemm_dist_steps(world, transa, m_global, m, n, k, alpha, A, lda, B_slab, beta, C_, ldc, config, handle,
-                           trace, rank=rank)
+                           trace, rank=rank, slab_ptrs=peers.next() if peers is not None else None)
     return drive_collectives(gen, world, group)
+
+
+class PeerSlabs:
+    """Slab record buffers for the fused phase 7, shared over CUDA IPC: each rank
+    cudaMallocs two (calls alternate between them, so a rank slicing call i+2 can
+    never overwrite planes a peer still reads for call i: every rank passes call
+    i+1's barrier only after its own call-i GEMM has completed), exports the IPC
+    handles, all-gathers them (torch.distributed, CPU objects) and maps its
+    peers' buffers (lazy NVLink peer access). `next()` -> the pointer list of
+    the buffer for the next call, entry r = rank r's buffer in this process."""
+
+    def __init__(self, n: int, k: int, config: Optional[AdpConfig] = None, group=None, device: int = 0):
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if self.world > 1 else 0
+        self.device = device
+        _, _, _, cap_bytes = dist_sizes(n, k, self.world, config)
+        self.own, self.opened, self.ptrs = [], [], []
+        handles = []
+        for _ in range(2):
+            p, h = C.c_void_p(), (C.c_uint8 * 64)()
+            check(lib().adpb200_ipc_alloc(device, cap_bytes, C.byref(p), h))
+            self.own.append(p.value)
+            handles.append(bytes(h))
+        allh = [None] * self.world
+        if self.world > 1:
+            dist.all_gather_object(allh, handles, group=group)
+        else:
+            allh = [handles]
+        for b in range(2):
+            row = []
+            for r in range(self.world):
+                if r == self.rank:
+                    row.append(self.own[b])
+                    continue
+                p = C.c_void_p()
+                check(lib().adpb200_ipc_open(device, (C.c_uint8 * 64).from_buffer_copy(allh[r][b]), C.byref(p)))
+                self.opened.append(p.value)
+                row.append(p.value)
+            self.ptrs.append(row)
+        self.calls = 0
+
+    def next(self):
+        p = self.ptrs[self.calls % 2]
+        self.calls += 1
+        return p
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        for p in self.opened:
+            lib().adpb200_ipc_close(C.c_void_p(p))
+        for p in self.own:
+            lib().adpb200_ipc_free(C.c_void_p(p))
+        self.opened, self.own, self.ptrs = [], [], []
 
 
 def drive_collectives(gen, world: int, group=None):
@@ -180,7 +255,12 @@ def drive_collectives(gen, world: int, group=None):
             if req[0] in ("all_gather", "all_gather_async"):
                 asy = req[0] == "all_gather_async"
                 if world > 1 and dist.get_backend(group) == "gloo":
-                    dist.all_gather(list(req[1].view(-1).chunk(world)), req[2].contiguous().view(-1), group=group)
+                    # (gloo: staged through host memory when the buffers live on a GPU)
+                    src = req[2].contiguous().view(-1)
+                    out = req[1].view(-1)
+                    parts = [torch.empty_like(src, device="cpu") for _ in range(world)]
+                    dist.all_gather(parts, src.cpu(), group=group)
+                    out.copy_(torch.cat(parts))
                 elif world > 1:
                     # async: NCCL's stream waits for the inputs; the caller's stream only waits at "wait"
                     work = dist.all_gather_into_tensor(req[1], req[2].contiguous(), group=group, async_op=asy)
@@ -194,6 +274,9 @@ def drive_collectives(gen, world: int, group=None):
                     pending = None
             elif req[0] == "all_reduce_max":
                 reduce_xchg(req[1], group)
+            elif req[0] == "barrier":
+                if world > 1:
+                    dist.barrier(group=group)
             else:
                 raise ValueError(f"unknown collective request {req[0]!r}")
             req = next(gen)

@@ -21,7 +21,7 @@ def run_virtual(gens):
     while True:
         kind = reqs[0][0]
         assert all(r[0] == kind for r in reqs), "ranks diverged"
-        if kind == "wait":
+        if kind in ("wait", "barrier"):
             pass
         elif kind in ("all_gather", "all_gather_async"):
             cat = torch.cat([r[2].reshape(-1) for r in reqs])
@@ -44,7 +44,7 @@ def run_virtual(gens):
 
 
 def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3,
-              overlap=True, zero_row=None):
+              overlap=True, zero_row=None, fused=False):
     from paper_2511_13778_b200 import Handle
     from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
 
@@ -66,6 +66,13 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
     lda = m if transa == "N" else k
     gpu.dgemm(transa, "N", m, n, k, alpha, Ast, lda, Bt, k, beta, ref, m, cfg)
     gens, blocks = [], []
+    slab_ptrs = None
+    if fused:  # the fused phase 7: every rank's slab buffer, read in place by all ranks' GEMMs
+        from paper_2511_13778_b200.dist import dist_sizes
+
+        cap_bytes = dist_sizes(n, k, world, cfg)[3]
+        slabs = [torch.empty(cap_bytes, dtype=torch.int8, device="cuda") for _ in range(world)]
+        slab_ptrs = [t.data_ptr() for t in slabs]
     for r in range(world):
         r0, r1 = rows_of(r, world, m)
         c0, c1 = cols_of(r, world, n)
@@ -76,7 +83,7 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
         Cb = Ct[:, r0:r1].contiguous()
         blocks.append(Cb)
         gens.append(dgemm_dist_steps(world, transa, m, mr, n, k, alpha, Ab, lda_r, Bs, beta, Cb, max(mr, 1), cfg,
-                                     Handle(0), rank=r, overlap=overlap))
+                                     Handle(0), rank=r, overlap=overlap, slab_ptrs=slab_ptrs))
     res = run_virtual(gens)
     torch.cuda.synchronize()
     assembled = torch.cat(blocks, dim=1)
@@ -147,5 +154,28 @@ def test_dist_certified_esc(gpu, world, m, n, k):
     assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
     # NaN in a slab: native everywhere
     got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 5))
+    assert all(r[0] == 1 for r in res)
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
+
+
+@pytest.mark.parametrize("world,m,n,k,cfgname", [(2, 640, 384, 512, "full"), (4, 1000, 512, 768, "target"),
+                                                 (8, 1024, 1024, 1024, "target"), (3, 700, 3 * 200, 900, "target"),
+                                                 (4, 512, 4 * 40, 640, "certified"), (2, 520, 2 * 104, 1100, "u12")])
+def test_dist_fused_peer_gemm(gpu, world, m, n, k, cfgname):
+    """Phase 7: no plane all-gather; the GEMM's TMA loads read each rank's slab
+    planes in place (here: buffers of one device standing in for the NVLink
+    peer mappings) with every rank's columns tiled on their own, including
+    slabs that are not a multiple of the variant's NB (partial last tile per
+    rank) and the 48-column variant (s = 8). C bit-identical to one GPU."""
+    cfg = {"full": gpu.AdpConfig(min_dim=8), "target": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET),
+           "certified": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET, esc_method="certified"),
+           "u12": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET)}[cfgname]
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, alpha=-0.5, beta=1.25, fused=True,
+                              lo=1.0 if cfgname == "u12" else -1.0)
+    assert all(r == res[0] for r in res)
+    assert res[0][0] == 0
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    # NaN in one slab: the fused path is not taken (native fallback gathers FP64 B)
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 3), fused=True)
     assert all(r[0] == 1 for r in res)
     assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
