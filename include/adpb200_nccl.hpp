@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "adpb200.h"
 
@@ -27,11 +28,61 @@ inline int cu(cudaError_t e) { return e == cudaSuccess ? ADPB200_OK : ADPB200_ER
 inline int nc(ncclResult_t r) { return r == ncclSuccess ? ADPB200_OK : ADPB200_ERR_RUNTIME; }
 }  // namespace nccl_detail
 
+// Slab buffers for the fused phase 7 (the GEMM reads every rank's B planes in
+// place over NVLink): two per rank (calls alternate, see dist.py PeerSlabs),
+// shared once per communicator through CUDA IPC handles all-gathered over NCCL.
+struct PeerSlabs {
+    int world = 0, rank = 0, device = 0, calls = 0;
+    void* own[2] = {nullptr, nullptr};
+    std::vector<void*> ptrs[2];  // entry r: rank r's buffer in this process
+};
+
+inline int peer_slabs_create(PeerSlabs& ps, ncclComm_t comm, int rank, int world, int device, int64_t n, int64_t k,
+                             const adpb200_options* opt, cudaStream_t st) {
+    using namespace nccl_detail;
+    int64_t sz[4];
+    int rc = adpb200_dist_sizes(n, k, world, opt, sz);
+    if (rc) return rc;
+    ps.world = world;
+    ps.rank = rank;
+    ps.device = device;
+    std::vector<uint8_t> mine(128), all(size_t(128) * world);
+    for (int b = 0; b < 2 && !rc; ++b) rc = adpb200_ipc_alloc(device, sz[3], &ps.own[b], mine.data() + 64 * b);
+    uint8_t* dbuf = nullptr;
+    if (!rc) rc = cu(cudaMalloc(&dbuf, all.size()));
+    if (!rc) rc = cu(cudaMemcpyAsync(dbuf + 128 * rank, mine.data(), 128, cudaMemcpyHostToDevice, st));
+    if (!rc) rc = nc(ncclAllGather(dbuf + 128 * rank, dbuf, 128, ncclUint8, comm, st));
+    if (!rc) rc = cu(cudaMemcpyAsync(all.data(), dbuf, all.size(), cudaMemcpyDeviceToHost, st));
+    if (!rc) rc = cu(cudaStreamSynchronize(st));
+    if (dbuf) cudaFree(dbuf);
+    for (int b = 0; b < 2 && !rc; ++b) {
+        ps.ptrs[b].assign(world, nullptr);
+        for (int r = 0; r < world && !rc; ++r) {
+            if (r == rank) ps.ptrs[b][r] = ps.own[b];
+            else rc = adpb200_ipc_open(device, all.data() + 128 * r + 64 * b, &ps.ptrs[b][r]);
+        }
+    }
+    return rc;
+}
+
+inline void peer_slabs_destroy(PeerSlabs& ps) {
+    cudaDeviceSynchronize();
+    for (int b = 0; b < 2; ++b) {
+        for (int r = 0; r < int(ps.ptrs[b].size()); ++r)
+            if (r != ps.rank && ps.ptrs[b][r]) adpb200_ipc_close(ps.ptrs[b][r]);
+        if (ps.own[b]) adpb200_ipc_free(ps.own[b]);
+        ps.own[b] = nullptr;
+        ps.ptrs[b].clear();
+    }
+}
+
 // Returns an adpb200 status (0 ok, 2 runtime incl. CUDA/NCCL failures, 3 contract).
+// peers (optional, from peer_slabs_create for this n, k): the fused phase 7 —
+// no plane all-gather; after a barrier every rank's GEMM reads the planes in place.
 inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int world, char transa, int64_t m_global,
                            int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                            const double* B_slab, double beta, double* C, int64_t ldc, const adpb200_options* opt,
-                           adpb200_trace* trace_dev, cudaStream_t st) {
+                           adpb200_trace* trace_dev, cudaStream_t st, PeerSlabs* peers = nullptr) {
     using namespace nccl_detail;
     int64_t sz[4];
     int rc = adpb200_dist_sizes(n, k, world, opt, sz);
@@ -48,10 +99,12 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
         return adpb200_dgemm_dist(h, p, m_global, world, rank, transa, m, n, k, alpha, A, lda, B_slab, beta, C, ldc,
                                   opt, trace_dev, bl, ba, xchg, slab, g, nsl, st);
     };
+    const std::vector<void*>* pp = peers ? &peers->ptrs[peers->calls++ % 2] : nullptr;
     rc = cu(cudaMallocAsync(&bl, size_t(nrec) * 4, st));
     if (!rc) rc = cu(cudaMallocAsync(&ba, size_t(nrec) * 4 * world, st));
     if (!rc) rc = cu(cudaMallocAsync(&xchg, 8, st));
-    if (!rc) rc = cu(cudaMallocAsync(&slab, size_t(cap_bytes), st));
+    if (pp) slab = static_cast<int8_t*>((*pp)[rank]);
+    else if (!rc) rc = cu(cudaMallocAsync(&slab, size_t(cap_bytes), st));
     if (!rc) rc = cu(cudaMemsetAsync(xchg, 0, 8, st));
     // 1: exponent statistics of the A rows and the B slab; all-gather the slab records
     if (!rc) rc = phase(1, nullptr, 0);
@@ -65,7 +118,12 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
     if (!rc) rc = cu(cudaStreamSynchronize(st));
     if (!rc) rc = adpb200_dist_decision(opt, xh, m_global, n, k, dec);
     const int nsl = dec[2];
-    if (!rc && nsl > 0) {
+    if (!rc && nsl > 0 && pp) {
+        // every rank's slab is sliced (the host sync above) once this barrier passes
+        rc = nc(ncclAllReduce(xchg, xchg, 1, ncclInt32, ncclMax, comm, st));
+        if (!rc) rc = cu(cudaStreamSynchronize(st));
+        if (!rc) rc = phase(7, pp->data(), nsl);
+    } else if (!rc && nsl > 0) {
         // B planes all-gathered on a second stream while this rank's own columns compute
         const int64_t rec = hdr + int64_t(nsl) * plane_bytes;
         rc = cu(cudaMallocAsync(&gathered, size_t(rec) * world, st));
@@ -89,7 +147,7 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
     if (bl) cudaFreeAsync(bl, st);
     if (ba) cudaFreeAsync(ba, st);
     if (xchg) cudaFreeAsync(xchg, st);
-    if (slab) cudaFreeAsync(slab, st);
+    if (slab && !pp) cudaFreeAsync(slab, st);
     if (gathered) cudaFreeAsync(gathered, st);
     if (bfull) cudaFreeAsync(bfull, st);
     if (comm_st) {

@@ -40,14 +40,22 @@ int main() {
     cudaMalloc(&dC1, C0.size() * 8);
     cudaMalloc(&dC2, C0.size() * 8);
     int bad_total = 0;
-    for (int poison = 0; poison < 2; ++poison) {
+    adpb200::PeerSlabs peers;
+    if (adpb200::peer_slabs_create(peers, comm, 0, 1, 0, n, k, &o, st)) {
+        std::fprintf(stderr, "peer_slabs_create: %s\n", adpb200_last_error());
+        return 2;
+    }
+    const std::vector<double> B0 = B;
+    for (int run = 0; run < 4; ++run) {
+        const int poison = run & 1, fused = run >> 1;
+        B = B0;
         if (poison) B[123] = std::nan("");
         cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
         cudaMemcpy(dB, B.data(), B.size() * 8, cudaMemcpyHostToDevice);
         cudaMemcpy(dC1, C0.data(), C0.size() * 8, cudaMemcpyHostToDevice);
         cudaMemcpy(dC2, C0.data(), C0.size() * 8, cudaMemcpyHostToDevice);
         int rc = adpb200::dgemm_dist_nccl(h, comm, 0, 1, 'N', m, m, n, k, 1.25, dA, m, dB, 0.5, dC1, m, &o, nullptr,
-                                          st);
+                                          st, fused ? &peers : nullptr);
         if (!rc) rc = adpb200_dgemm(h, 'N', 'N', m, n, k, 1.25, dA, m, dB, k, 0.5, dC2, m, &o, nullptr, st);
         cudaStreamSynchronize(st);
         if (rc) {
@@ -65,9 +73,11 @@ int main() {
             const bool both_nan = c1[i] != c1[i] && c2[i] != c2[i];
             if (x != y && !both_nan) ++bad;
         }
-        std::printf("%s: %d of %zu differ\n", poison ? "fallback" : "emulated", bad, c1.size());
+        std::printf("%s%s: %d of %zu differ\n", fused ? "fused " : "", poison ? "fallback" : "emulated", bad,
+                    c1.size());
         bad_total += bad;
     }
+    adpb200::peer_slabs_destroy(peers);
     ncclCommDestroy(comm);
     adpb200_destroy(h);
     return bad_total ? 1 : 0;
