@@ -367,6 +367,15 @@ def main():
                 "peak_source": peak_src + "; int8 ops = 2mnk x pairs",
                 "frac_of_2x_bf16": (achieved / (2.0 * pk["bf16_tflops"])) if achieved else None,
                 "clock_note": "the GEMM runs power-capped (sw_power_cap, ~1000 W): see clocks", "pairs": pairs}
+    # the same kernel against the dense kind::i8 rate at the SM clock nvidia-smi saw under load
+    # (148 SMs x 8192 MAC/clk x 2 ops): how much of the power-capped clock's peak it uses
+    load_clk = None
+    if clocks:
+        soak = clocks.get("soak_after_timed_region") or {}
+        load_clk = soak.get("sm_mhz") or clocks.get("sm_mhz")
+    if achieved and load_clk:
+        roofline["peak_at_load_clock"] = 148 * 8192 * 2 * load_clk * 1e6 / 1e12
+        roofline["frac_at_load_clock"] = achieved / roofline["peak_at_load_clock"]
 
     extra = {}
     if not args.quick:

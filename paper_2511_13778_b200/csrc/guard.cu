@@ -535,7 +535,8 @@ __global__ void certify_finish_kernel(Plan* plan, const Plan* rplan) {
 
 __global__ void dist_export_kernel(const Plan* plan, const Plan* rplan, int32_t* xchg, int certified) {
     int32_t x0 = plan->exc;
-    if (certified && (plan->exc != 0 || (rplan->path == ADPB200_PATH_EMULATED && rplan->exc != 0)))
+    // (an unarmed certificate plan counts as failed: no count GEMM ran)
+    if (certified && (plan->exc != 0 || rplan->path != ADPB200_PATH_EMULATED || rplan->exc != 0))
         x0 |= kXchgCertFail;
     xchg[0] = x0;
     xchg[1] = plan->esc_raw;

@@ -1,7 +1,7 @@
 """Turn a tools/profile_round.sh run (gpurun_out/<tag>_*) into the tracked
 summaries under profiles/: launch-list shares, ncu_summary.json (the bench's
 roofline.traffic source), ncu details pages, probe outputs.
-Usage: python tools/summarize_profiles.py [tag]   (default r01b)"""
+Usage: python tools/summarize_profiles.py [tag]   (default r01c)"""
 import collections
 import csv
 import json
@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01b"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01c"
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
 
@@ -62,6 +62,34 @@ for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
 open(os.path.join(P, f"{tag}_launches.txt"), "w").write("\n".join(lines) + "\n")
 shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(P, f"{tag}_launches.csv"))
 
+# launch list of one certified-ESC call on U[-1,1] (the certificate's kernels beside the rest)
+cpath = os.path.join(G, f"{tag}_launches_certified.csv")
+if os.path.exists(cpath):
+    cagg = collections.OrderedDict()
+    chdr = None
+    for r in csv.reader(open(cpath)):
+        if r and r[0] == "ID":
+            chdr = r
+            continue
+        if chdr and len(r) == len(chdr):
+            d = dict(zip(chdr, r))
+            if d.get("Metric Name") != "gpu__time_duration.sum":
+                continue
+            us = float(d["Metric Value"].replace(",", "")) * SCALE[d["Metric Unit"]]
+            k = d["Kernel Name"].split("(")[0].replace("adpb200::<unnamed>::", "").replace("void ", "")
+            a = cagg.setdefault(k, [0, 0.0])
+            a[0] += 1
+            a[1] += us
+    cours = {k: v for k, v in cagg.items() if not k.startswith("at::") and "uniform" not in k}
+    ctot = sum(v[1] for v in cours.values())
+    cl = ["# ncu launch list: python tools/one_call.py --u11 --certified (8192^3 U[-1,1], certified ESC, 2 calls)",
+          "# the certificate = certify_prep/finish + slice kernels in indicator mode (K = 512) + one igemm<64> launch",
+          f"{'kernel':48s} {'launches':>8s} {'total_us':>12s} {'per_launch_us':>14s} {'share_of_ours':>13s}"]
+    for k, v in sorted(cagg.items(), key=lambda x: -x[1][1]):
+        sh = f"{100 * v[1] / ctot:12.1f}%" if k in cours else "   (setup)"
+        cl.append(f"{k[:48]:48s} {v[0]:8d} {v[1]:12.3f} {v[1] / v[0]:14.4f} {sh}")
+    open(os.path.join(P, f"{tag}_launches_certified.txt"), "w").write("\n".join(cl) + "\n")
+
 # ncu details + summary
 ig, igu = raw(os.path.join(G, f"{tag}_igemm64.ncu-rep"))[0]
 gk = {}
@@ -99,7 +127,7 @@ for nm in ("igemm64", "guard"):
     open(os.path.join(P, f"{tag}_{nm}_ncu_details.txt" if nm == "guard" else f"{tag}_igemm64_ncu_details.txt"),
          "w").write(out)
 for f in ("mma_peak.jsonl", "qr_probe.jsonl", "esc_block.jsonl", "shapes.jsonl", "fp64_chain.json", "small.jsonl",
-          "e2e.json"):
+          "e2e.json", "pcie.json"):
     src = os.path.join(G, f"{tag}_{f}")
     if os.path.exists(src):
         keep = [l for l in open(src) if l.startswith("{")]
