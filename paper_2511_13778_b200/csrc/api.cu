@@ -175,6 +175,42 @@ int plane_cap(const adpb200_options& o, int fixed_slices, int fixed_limit) {
     return cap;
 }
 
+// GEMM arguments of the product C = alpha op(A) op(B) + beta C_in on P's output,
+// with the workspace's A scales and exact-partials scratch.
+GemmArgs product_args(adpb200_context* h, const Layout& Lw, const Problem& P, const Plan* plan,
+                      const int32_t* scale_b) {
+    GemmArgs g{};
+    g.plan = plan;
+    g.M = P.M;
+    g.N = P.N;
+    g.K = P.K;
+    g.scale_a = at<int32_t>(h, Lw.scale_a);
+    g.scale_b = scale_b;
+    g.alpha = P.alpha;
+    g.beta = P.beta;
+    g.c_out = P.c_out;
+    g.ldc = P.ldc;
+    g.c_in = P.c_in;
+    g.ldc_in = P.ldc_in;
+    g.partial = at<uint64_t>(h, Lw.partial);
+    return g;
+}
+
+// GEMM arguments of the certified ESC's count GEMM (no C; zero-count flag in rplan->exc).
+GemmArgs count_args(adpb200_context* h, const Layout& Lw, const Problem& P, Plan* rplan, int64_t kw) {
+    GemmArgs g{};
+    g.plan = rplan;
+    g.M = P.M;
+    g.N = P.N;
+    g.K = kw;
+    g.scale_a = at<int32_t>(h, Lw.scale_a);
+    g.scale_b = at<int32_t>(h, Lw.scale_b);
+    g.alpha = 1.0;
+    g.partial = at<uint64_t>(h, Lw.partial);
+    g.zero_flag = &rplan->exc;
+    return g;
+}
+
 constexpr int kHostChunks = 4;  // row chunks of the host-buffer path (GEMM chunk i || D2H chunk i-1); 8 measured slower
 
 // Destination of C on the host for the host-buffer entry points.
@@ -219,16 +255,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
                  nl, 1);
     launch_slice(vb, at<int32_t>(h, Lw.line_b), pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, nullptr, rplan, 0, 1, st,
                  nl, 1);
-    GemmArgs g{};
-    g.plan = rplan;
-    g.M = P.M;
-    g.N = P.N;
-    g.K = kw;
-    g.scale_a = at<int32_t>(h, Lw.scale_a);
-    g.scale_b = at<int32_t>(h, Lw.scale_b);
-    g.alpha = 1.0;
-    g.partial = at<uint64_t>(h, Lw.partial);
-    g.zero_flag = &rplan->exc;
+    const GemmArgs g = count_args(h, Lw, P, rplan, kw);
     if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, Lw.cap, g, st, nl))
         return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
     if (!rows_mode) launch_certify_finish(plan, rplan, st, nl);
@@ -321,20 +348,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, fixed_slices, cap, st, nl);
         tm.end(3);
         // K4/K5: one launch per GEMM variant; exactly one does work
-        GemmArgs g{};
-        g.plan = plan;
-        g.M = P.M;
-        g.N = P.N;
-        g.K = P.K;
-        g.scale_a = sa;
-        g.scale_b = sb;
-        g.alpha = P.alpha;
-        g.beta = P.beta;
-        g.c_out = P.c_out;
-        g.ldc = P.ldc;
-        g.c_in = P.c_in;
-        g.ldc_in = P.ldc_in;
-        g.partial = at<uint64_t>(h, Lw.partial);
+        GemmArgs g = product_args(h, Lw, P, plan, sb);
         g.dump = dump;
         g.ndump = ndump;
         int variants[5] = {64, 48, 32, 16, 8};
@@ -461,16 +475,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
             LineView aw = P.a;
             aw.len = kw;
             launch_slice(aw, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st, nl, 1);
-            GemmArgs g{};
-            g.plan = rplan;
-            g.M = P.M;
-            g.N = P.N;
-            g.K = kw;
-            g.scale_a = at<int32_t>(h, Lw.scale_a);
-            g.scale_b = at<int32_t>(h, Lw.scale_b);
-            g.alpha = 1.0;
-            g.partial = at<uint64_t>(h, Lw.partial);
-            g.zero_flag = &rplan->exc;
+            const GemmArgs g = count_args(h, Lw, P, rplan, kw);
             if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
                 return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
         }
@@ -500,19 +505,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     if (phase == 7) {
         // fused all-gather -> GEMM: the GEMM's TMA reads every rank's slab record in
         // place (peer memory over NVLink), tile by tile; no gathered copy, no NCCL
-        GemmArgs g{};
-        g.plan = plan;
-        g.M = P.M;
-        g.N = P.N;
-        g.K = P.K;
-        g.scale_a = at<int32_t>(h, Lw.scale_a);
-        g.alpha = P.alpha;
-        g.beta = P.beta;
-        g.c_out = P.c_out;
-        g.ldc = P.ldc;
-        g.c_in = P.c_in;
-        g.ldc_in = P.ldc_in;
-        g.partial = at<uint64_t>(h, Lw.partial);
+        const GemmArgs g = product_args(h, Lw, P, plan, nullptr);
         tm.begin(4);
         const int prc = launch_igemm_peer(at<int8_t>(h, Lw.planes_a), Lw.slots_a, Lw.pitch / 32, cap,
                                           static_cast<const int8_t* const*>(io.gathered), io.world, nr, slab_hdr(nr),
@@ -535,20 +528,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
             launch_gather_planes(static_cast<const int8_t*>(io.gathered), rec_bytes, slab_hdr(nr), io.world, nr, nkb,
                                  io.nsl, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb, st, nl);
         tm.end(3);
-        GemmArgs g{};
-        g.plan = plan;
-        g.M = P.M;
-        g.N = P.N;
-        g.K = P.K;
-        g.scale_a = at<int32_t>(h, Lw.scale_a);
-        g.scale_b = sb;
-        g.alpha = P.alpha;
-        g.beta = P.beta;
-        g.c_out = P.c_out;
-        g.ldc = P.ldc;
-        g.c_in = P.c_in;
-        g.ldc_in = P.ldc_in;
-        g.partial = at<uint64_t>(h, Lw.partial);
+        GemmArgs g = product_args(h, Lw, P, plan, sb);
         tm.begin(4);
         for (int nb : {64, 48, 32, 16, 8}) {
             // n-tiles entirely inside this rank's columns [rank*nr, (rank+1)*nr)
@@ -587,20 +567,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
         launch_gather_planes(static_cast<const int8_t*>(io.gathered), rec_bytes, slab_hdr(nr), io.world, nr, nkb,
                              io.nsl, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb, st, nl);
         tm.end(3);
-        GemmArgs g{};
-        g.plan = plan;
-        g.M = P.M;
-        g.N = P.N;
-        g.K = P.K;
-        g.scale_a = at<int32_t>(h, Lw.scale_a);
-        g.scale_b = sb;
-        g.alpha = P.alpha;
-        g.beta = P.beta;
-        g.c_out = P.c_out;
-        g.ldc = P.ldc;
-        g.c_in = P.c_in;
-        g.ldc_in = P.ldc_in;
-        g.partial = at<uint64_t>(h, Lw.partial);
+        GemmArgs g = product_args(h, Lw, P, plan, sb);
         tm.begin(4);
         for (int nb : {64, 48, 32, 16, 8})
             if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, nkb, cap, g, st, nl))
@@ -691,20 +658,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
     launch_set_plan(spec, s_spec, o.pair_limit, P.K, st, nl);
     launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, spec, 0, cap, st, nl);
-    GemmArgs g{};
-    g.plan = spec;
-    g.M = P.M;
-    g.N = P.N;
-    g.K = P.K;
-    g.scale_a = sa;
-    g.scale_b = sb;
-    g.alpha = P.alpha;
-    g.beta = P.beta;
-    g.c_out = P.c_out;
-    g.ldc = P.ldc;
-    g.c_in = P.c_in;
-    g.ldc_in = P.ldc_in;
-    g.partial = at<uint64_t>(h, Lw.partial);
+    GemmArgs g = product_args(h, Lw, P, spec, sb);
     for (int c = 0; c < nchunks; ++c) {
         const int64_t c0 = c * chunk, c1 = std::min(P.N, c0 + chunk), lines = c1 - c0;
         rc = cuda_check(cudaStreamWaitEvent(st, h->h2d_ev[c], 0), "cudaStreamWaitEvent(B chunk)");
