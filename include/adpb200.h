@@ -261,6 +261,13 @@ int adpb200_decompose(adpb200_handle handle, const double* A, int64_t rows, int6
 int adpb200_slice_pair_mm(adpb200_handle handle, const double* A, const double* B, int64_t m,
                           int64_t n, int64_t k, int slices, int pair_limit, int64_t* acc,
                           void* stream);
+/* recompose (igemm.cpp:99-127): out (m x n row-major FP64) from the diagonal
+ * accumulators of slice_pair_mm (2*slices-1 per element) and the decompose scales
+ * (row_scale: m, col_scale: n): S = sum_D acc_D 2^(8(dmax-D)) exactly, one RNE
+ * rounding of S 2^(row+col-14-8 dmax), r = alpha v (+ beta C, C read iff beta != 0). */
+int adpb200_recompose(adpb200_handle handle, const int64_t* acc, int64_t m, int64_t n, int slices,
+                      const int32_t* row_scale, const int32_t* col_scale, double alpha, double beta,
+                      const double* c_in, double* out, void* stream);
 /* emulated_gemm (igemm.cpp:129-137): fixed slices, no guardrails. */
 int adpb200_emulated_gemm(adpb200_handle handle, const double* A, const double* B, int64_t m,
                           int64_t n, int64_t k, double alpha, double beta, const double* c_in,

@@ -21,6 +21,7 @@ from .adp import (  # noqa: F401
     esc_coarsened,
     native_gemm,
     parse_mode,
+    recompose,
     required_slices,
     scan_matrix,
     slice_pair_mm,

@@ -352,6 +352,25 @@ def slice_pair_mm(a, b, slices: int, pair_limit: int = PAIRS_FULL, handle: Optio
     return acc.cpu().numpy() if host else acc
 
 
+def recompose(acc, row_scale, col_scale, alpha: float = 1.0, beta: float = 0.0, c=None,
+              handle: Optional[Handle] = None):
+    """recompose (igemm.cpp:99-127): FP64 [m][n] from int64 acc[m][n][2s-1] + the decompose scales."""
+    host = not isinstance(acc, torch.Tensor)
+    m, n, nd = acc.shape
+    if nd % 2 == 0:
+        raise ValueError("recompose: acc must hold 2s-1 diagonals")
+    dev = _device(acc.device.index if isinstance(acc, torch.Tensor) else None)
+    handle = handle or Handle.default(dev.index)
+    A = torch.as_tensor(acc, dtype=torch.int64).to(dev).contiguous()
+    rs = torch.as_tensor(row_scale, dtype=torch.int32).to(dev).contiguous()
+    cs = torch.as_tensor(col_scale, dtype=torch.int32).to(dev).contiguous()
+    Cin = _to_dev(c, dev) if c is not None else None
+    out = torch.empty((m, n), dtype=torch.float64, device=dev)
+    check(lib().adpb200_recompose(handle.h, _ptr(A), m, n, (nd + 1) // 2, _ptr(rs), _ptr(cs), float(alpha),
+                                  float(beta), _ptr(Cin), _ptr(out), _stream(dev)))
+    return out.cpu().numpy() if host else out
+
+
 def decompose(a, orient: int, slices: int, handle: Optional[Handle] = None):
     """decompose (slicing.cpp:90-136): (digits[s][lines][len] int8, scale_exp[lines])."""
     host = not isinstance(a, torch.Tensor)

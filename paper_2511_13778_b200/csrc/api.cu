@@ -1295,6 +1295,20 @@ int adpb200_emulated_gemm(adpb200_handle h, const double* A, const double* B, in
     return run_pipeline(h, P, o, nullptr, static_cast<cudaStream_t>(stream), slices, pair_limit, nullptr, 0);
 }
 
+int adpb200_recompose(adpb200_handle h, const int64_t* acc, int64_t m, int64_t n, int slices,
+                      const int32_t* row_scale, const int32_t* col_scale, double alpha, double beta,
+                      const double* c_in, double* out, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "recompose: null handle");
+    if (slices < 1 || slices > kMaxSlices) return fail(3, "recompose: slices must be in [1, 32]");
+    if (m < 0 || n < 0) return fail(3, "recompose: negative dimension");
+    if (beta != 0.0 && !c_in) return fail(3, "recompose: beta != 0 needs C");  // igemm.cpp:104-107
+    if (m > 0 && n > 0 && (!acc || !row_scale || !col_scale || !out)) return fail(3, "recompose: null buffer");
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    launch_recompose(acc, m, n, 2 * slices - 1, row_scale, col_scale, alpha, beta, c_in, out, st, &h->launches);
+    return cuda_check(cudaGetLastError(), "recompose");
+}
+
 int adpb200_slice_pair_mm(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,
                           int slices, int pair_limit, int64_t* acc, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "slice_pair_mm: null handle");

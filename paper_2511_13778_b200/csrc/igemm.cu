@@ -987,4 +987,40 @@ int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int 
     return rc;
 }
 
+// ---- recompose stage export (igemm.cpp:99-127) -------------------------------------
+namespace {
+// One thread per output: S = sum_D acc_D 256^(dmax - D) exactly (9 limbs cover
+// dmax <= 62 plus the int64 terms), one rounding with the epilogue's
+// round_limbs, then alpha / beta as separate roundings.
+__global__ void recompose_kernel(const int64_t* __restrict__ acc, int64_t m, int64_t n, int ndiag,
+                                 const int32_t* __restrict__ row_scale, const int32_t* __restrict__ col_scale,
+                                 double alpha, double beta, const double* __restrict__ c_in, double* __restrict__ out) {
+    const int64_t total = m * n;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = e / n, j = e - i * n;
+        const int64_t* a = acc + e * ndiag;
+        uint64_t S[9];
+        const int64_t x0 = a[0];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) S[q] = q == 0 ? uint64_t(x0) : (x0 < 0 ? ~0ull : 0ull);
+        for (int d = 1; d < ndiag; ++d) limbs_shl8_add<9>(S, a[d]);
+        const int exp2 = row_scale[i] + col_scale[j] - 14 - 8 * (ndiag - 1);
+        double r = __dmul_rn(alpha, round_limbs<9>(S, exp2));
+        if (beta != 0.0) r = __dadd_rn(r, __dmul_rn(beta, c_in[e]));
+        out[e] = r;
+    }
+}
+}  // namespace
+
+void launch_recompose(const int64_t* acc, int64_t m, int64_t n, int ndiag, const int32_t* row_scale,
+                      const int32_t* col_scale, double alpha, double beta, const double* c_in, double* out,
+                      cudaStream_t st, uint64_t* nlaunch) {
+    const int64_t total = m * n;
+    if (total == 0) return;
+    const int64_t want = (total + 255) / 256;
+    const int grid = int(want < int64_t(num_sms()) * 8 ? want : int64_t(num_sms()) * 8);
+    recompose_kernel<<<grid, 256, 0, st>>>(acc, m, n, ndiag, row_scale, col_scale, alpha, beta, c_in, out);
+    ++*nlaunch;
+}
+
 }  // namespace adpb200

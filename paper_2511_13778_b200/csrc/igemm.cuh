@@ -53,6 +53,11 @@ int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int 
 int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t slots_a, int64_t slots_b,
                  int64_t nkb, int cap, const GemmArgs& g, cudaStream_t st, uint64_t* nlaunch);
 
+// recompose (igemm.cpp:99-127): acc = m x n x ndiag int64 element-major, row-major out.
+void launch_recompose(const int64_t* acc, int64_t m, int64_t n, int ndiag, const int32_t* row_scale,
+                      const int32_t* col_scale, double alpha, double beta, const double* c_in, double* out,
+                      cudaStream_t st, uint64_t* nlaunch);
+
 // K6: native FP64 fallback in the reference's summation order (ascending k,
 // separate multiply and add: oracle.cpp:7-28). Runs iff the plan says
 // native (or always when plan == nullptr).
