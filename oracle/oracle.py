@@ -420,29 +420,43 @@ def exponent_field(a: np.ndarray) -> np.ndarray:
     return np.where(ok, e.astype(np.int64) - 1, NEG_SENTINEL)
 
 
+def certify_delta(target_bits: int, level: int = 0) -> int:
+    """Indicator threshold of certificate level `level` (targets s0 + level slices,
+    s0 = required_slices(target_bits, 0), esc.cpp:8-12): 2 delta + 1 is the largest
+    ESC those slices tolerate; -1 when the level cannot help."""
+    s = (target_bits + 2 + 7) // 8 + level
+    e = 8 * s - target_bits - 2
+    return (e - 1) // 2 if e >= 1 else -1
+
+
 def esc_certified(a, b, coarse_esc: int, target_bits: int = 53, window: int = 512) -> int:
     """Numpy restatement of the certified ESC (adpb200_options.esc_method = 1,
-    guard.cu certify_prep_kernel): with s0 = required_slices(target_bits, 0)
-    (esc.cpp:8-12), e0 = 8 s0 - target_bits - 2 and delta = (e0 - 1) // 2, the
-    result is 2 delta + 1 when every (i, j) has some l with
-    e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta (then the exact
-    z_ij of esc_exact, esc.cpp:61-87, is >= rowmax_i + colmax_j - 2 delta and
-    span_ij <= 2 delta + 1), and coarse_esc otherwise or when coarse_esc is
-    already <= 2 delta + 1. Only the first `window` positions l are inspected
-    (row / column maxima over the whole line), like api.cu's kCertifyWindow."""
-    s0 = (target_bits + 2 + 7) // 8
-    e0 = 8 * s0 - target_bits - 2
-    delta = (e0 - 1) // 2 if e0 >= 1 else -1
-    if delta < 0 or coarse_esc <= 2 * delta + 1:
+    guard.cu certify_prep_kernel / certified_esc). Level l holds when every (i, j)
+    has some position l among the first `window` with e(a_il) >= rowmax_i - delta_l
+    and e(b_lj) >= colmax_j - delta_l (row / column maxima over whole lines): then
+    the exact z_ij of esc_exact (esc.cpp:61-87) is >= rowmax_i + colmax_j - 2 delta_l
+    and span_ij <= 2 delta_l + 1. A level is tested only when the coarsened ESC
+    exceeds its bound; level 0 wins over level 1; otherwise coarse_esc stays."""
+    d0, d1 = certify_delta(target_bits, 0), certify_delta(target_bits, 1)
+    l0 = d0 >= 0 and coarse_esc > 2 * d0 + 1
+    l1 = d1 >= 0 and coarse_esc > 2 * d1 + 1
+    if not (l0 or l1):
         return coarse_esc
     ea, eb = exponent_field(a), exponent_field(b)
     rmax = ea.max(axis=1, initial=NEG_SENTINEL)
     cmax = eb.max(axis=0, initial=NEG_SENTINEL)
     ea, eb = ea[:, :window], eb[:window, :]
-    p = ((ea != NEG_SENTINEL) & (ea >= rmax[:, None] - delta)).astype(np.float64)
-    q = ((eb != NEG_SENTINEL) & (eb >= cmax[None, :] - delta)).astype(np.float64)
-    counts = p @ q  # exact: 0/1 products, sums <= k < 2^53
-    return 2 * delta + 1 if bool((counts > 0).all()) else coarse_esc
+
+    def holds(delta):
+        p = ((ea != NEG_SENTINEL) & (ea >= rmax[:, None] - delta)).astype(np.float64)
+        q = ((eb != NEG_SENTINEL) & (eb >= cmax[None, :] - delta)).astype(np.float64)
+        return bool(((p @ q) > 0).all())  # exact: 0/1 products, sums <= window < 2^53
+
+    if l0 and holds(d0):
+        return 2 * d0 + 1
+    if l1 and holds(d1):
+        return 2 * d1 + 1
+    return coarse_esc
 
 
 def fold_round(acc_row: np.ndarray, exp2: int) -> float:

@@ -250,7 +250,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
     LineView va = P.a, vb = P.b;
     va.len = kw;
     vb.len = kw;
-    launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, rows_mode ? 1 : 0);
+    launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, rows_mode ? 1 : 0, std::min(Lw.cap, 2));
     launch_slice(va, at<int32_t>(h, Lw.line_a), pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st,
                  nl, 1);
     launch_slice(vb, at<int32_t>(h, Lw.line_b), pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, nullptr, rplan, 0, 1, st,
@@ -258,7 +258,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
     const GemmArgs g = count_args(h, Lw, P, rplan, kw);
     if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, Lw.cap, g, st, nl))
         return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
-    if (!rows_mode) launch_certify_finish(plan, rplan, st, nl);
+    if (!rows_mode) launch_certify_finish(plan, rplan, o.target_bits, st, nl);
     return ADPB200_OK;
 }
 
@@ -437,7 +437,8 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     const bool cert = o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected && cap >= 1 && P.K > 0;
     const int64_t kw = std::min<int64_t>(P.K, kCertifyWindow), kwp = (kw + 31) / 32 * 32;
     const int64_t rec0 = 2 * t * nr + nr;
-    const int64_t rec = rec0 + (o.esc_method == ADPB200_ESC_CERTIFIED ? nr * kwp / 4 : 0);
+    const int cplanes = o.esc_method == ADPB200_ESC_CERTIFIED ? std::min(certify_planes(o.target_bits), cap) : 0;
+    const int64_t rec = rec0 + int64_t(cplanes) * nr * kwp / 4;
     Plan* rplan = at<Plan>(h, Lw.rplan);
     const LineView bslab{P.b.ptr, nr, P.K, P.K, 1};
     if (phase == 1) {
@@ -452,7 +453,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
         if (cert) {
             LineView bw = bslab;
             bw.len = kw;
-            launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, 1);
+            launch_certify_prep(plan, rplan, o.target_bits, kw, st, nl, 1, cplanes);
             launch_slice(bw, io.bstats_local + 2 * t * nr, reinterpret_cast<int8_t*>(io.bstats_local + rec0), nr,
                          kwp * nr, 1, nullptr, rplan, 0, 1, st, nl, 1);
         }
@@ -470,7 +471,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
             int8_t* pa = at<int8_t>(h, Lw.planes_a);
             int8_t* pb = at<int8_t>(h, Lw.planes_b);
             launch_gather_planes(reinterpret_cast<const int8_t*>(io.bstats_all), rec * 4, rec0 * 4, io.world, nr,
-                                 kwp / 32, 1, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, at<int32_t>(h, Lw.scale_b), st,
+                                 kwp / 32, cplanes, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, at<int32_t>(h, Lw.scale_b), st,
                                  nl);
             LineView aw = P.a;
             aw.len = kw;
@@ -966,7 +967,9 @@ int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* o
     const int64_t t = (k + o.esc_block_len - 1) / o.esc_block_len;
     const int64_t pitch = (int64_t)align_up(size_t(k), 32);
     const int64_t kw = std::min<int64_t>(k, kCertifyWindow);
-    out[0] = 2 * t * nr + nr + (o.esc_method == ADPB200_ESC_CERTIFIED ? nr * ((kw + 31) / 32 * 32) / 4 : 0);
+    const int cplanes =
+        o.esc_method == ADPB200_ESC_CERTIFIED ? std::min(certify_planes(o.target_bits), plane_cap(o, 0, 0)) : 0;
+    out[0] = 2 * t * nr + nr + int64_t(cplanes) * nr * ((kw + 31) / 32 * 32) / 4;
     out[1] = slab_hdr(nr);
     out[2] = pitch * nr;
     out[3] = out[1] + int64_t(plane_cap(o, 0, 0)) * out[2];
@@ -1015,10 +1018,8 @@ int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int
     const int64_t mn = std::min(std::min(m_global, n), k);
     const bool esc_expected =
         (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) && mn >= o.min_dim;
-    const int delta = certify_delta(o.target_bits);
-    if (o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected && !(xchg[0] & kXchgCertFail) && delta >= 0 &&
-        in.esc_bits > 2 * delta + 1)
-        in.esc_bits = 2 * delta + 1;
+    if (o.esc_method == ADPB200_ESC_CERTIFIED && esc_expected)
+        in.esc_bits = certified_esc(in.esc_bits, (xchg[0] >> kXchgCertShift) & 3, o.target_bits);
     DecideOutput d = decide(in, o);
     out[0] = d.path;
     out[1] = d.path == ADPB200_PATH_EMULATED ? d.slices : 0;

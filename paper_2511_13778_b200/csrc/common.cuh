@@ -45,8 +45,10 @@ struct Plan {
     int32_t kchunk;    // k elements per int32 accumulation chunk
     int32_t nchunks;
     double cost;
-    int32_t aux;  // certified-ESC plan: the indicator threshold delta
-    int32_t pad[3];
+    int32_t aux;   // certified-ESC plan: indicator threshold delta of plane 0
+    int32_t aux2;  //   ... of plane 1 (two-level plans)
+    int32_t lvl0;  //   certificate level plane 0 stands for (0, or 1 when level 0 cannot help)
+    int32_t pad[1];
 };
 
 struct DecideInput {
@@ -67,19 +69,29 @@ __host__ __device__ inline int required_slices(int target_bits, int esc_bits) {
 // decide() (adp.cpp:46-96): identical gate order and FP64 cost model. Every
 // FP64 operation is written as an explicitly rounded intrinsic on the device
 // (no FMA contraction, matching -ffp-contract=off of the reference build).
-// Certified ESC (adpb200_options.esc_method): the indicator threshold delta for
-// s0 = required_slices(target_bits, 0), the fewest slices any input gets; 2 delta + 1
-// is the largest ESC s0 tolerates (-1: no certificate can help).
-__host__ __device__ inline int certify_delta(int target_bits) {
-    const int s0 = (target_bits + 2 + 7) / 8;
-    const int e0 = 8 * s0 - target_bits - 2;
-    return e0 >= 1 ? (e0 - 1) / 2 : -1;
+// Certified ESC (adpb200_options.esc_method): the indicator threshold delta of
+// certificate level l, which targets s0 + l slices (s0 = required_slices(
+// target_bits, 0), the fewest any input gets): 2 delta + 1 is the largest ESC
+// s0 + l slices tolerate (-1: that level cannot help).
+__host__ __device__ inline int certify_delta(int target_bits, int level = 0) {
+    const int s = (target_bits + 2 + 7) / 8 + level;
+    const int e = 8 * s - target_bits - 2;
+    return e >= 1 ? (e - 1) / 2 : -1;
+}
+// The certified ESC from the coarsened one and the certificate outcome v:
+// 0 = level 0 holds for every (i, j), 1 = only level 1 does, 2 = neither.
+__host__ __device__ inline int certified_esc(int coarse, int v, int target_bits) {
+    const int d0 = certify_delta(target_bits, 0), d1 = certify_delta(target_bits, 1);
+    if (v == 0 && d0 >= 0 && coarse > 2 * d0 + 1) return 2 * d0 + 1;
+    if (v <= 1 && d1 >= 0 && coarse > 2 * d1 + 1) return 2 * d1 + 1;
+    return coarse;
 }
 // Multi-GPU exchange word 0 (max-reduced): exceptional bits 0-1, and with the
-// certified ESC this flag when some rank saw a zero indicator count or an
-// exceptional input (max-reduction keeps it set, and keeps the bits of an
-// exceptional rank because that rank sets the flag too).
-constexpr int32_t kXchgCertFail = 256;
+// certified ESC the rank's outcome v in bits 8-9 (max over ranks = the global
+// outcome; an exceptional rank reports v = 2, so the maximum also keeps its
+// exceptional bits).
+constexpr int kXchgCertShift = 8;
+constexpr int32_t kXchgCertFail = 2 << kXchgCertShift;
 
 __host__ __device__ inline DecideOutput decide(const DecideInput& in, const adpb200_options& c) {
     DecideOutput d{ADPB200_PATH_NATIVE, ADPB200_REASON_OK, 0, 0, -1, 0.0};

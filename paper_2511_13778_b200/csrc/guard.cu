@@ -504,40 +504,59 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
 
 // ---- certified ESC ----------------------------------------------------------------
 // s0 = required_slices(target_bits, 0) is the fewest slices any input can get;
-// it tolerates esc <= e0 = 8 s0 - target_bits - 2 (certify_delta). If some l has
-// e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta, the exact
-// largest product exponent z_ij (esc.cpp:61-87) is >= rowmax_i + colmax_j -
-// 2 delta, so span_ij <= 2 delta + 1. delta = (e0 - 1) / 2 makes that span
-// fit s0. The "some l" test for every (i, j) is one INT8 GEMM of 0/1 planes.
-__global__ void certify_prep_kernel(const Plan* plan, Plan* rplan, int target_bits, int64_t k, int force) {
+// s0 + l slices tolerate esc <= e_l = 8 (s0 + l) - target_bits - 2. If some
+// position l has e(a_il) >= rowmax_i - delta and e(b_lj) >= colmax_j - delta,
+// the exact largest product exponent z_ij (esc.cpp:61-87) is >= rowmax_i +
+// colmax_j - 2 delta, so span_ij <= 2 delta + 1; delta_l = (e_l - 1) / 2
+// (certify_delta) makes that span fit s0 + l slices. The "some l" test for every
+// (i, j) is an INT8 GEMM of 0/1 planes: one plane per operand for one level, two
+// (level 0, level 1) when the coarsened ESC asks for more than s0 + 1 slices;
+// the two-plane GEMM's diagonals 0 and 2 hold the two levels' counts.
+__global__ void certify_prep_kernel(const Plan* plan, Plan* rplan, int target_bits, int64_t k, int force,
+                                    int max_planes) {
     Plan r{};
     r.path = kPathDone;
-    const int delta = certify_delta(target_bits);
-    const bool wanted = force || (plan->esc_ran && plan->exc == 0 && plan->esc_raw > 2 * delta + 1);
-    if (wanted && delta >= 0 && k > 0 && k <= (int64_t(1) << 30)) {
+    const int d0 = certify_delta(target_bits, 0), d1 = certify_delta(target_bits, 1);
+    const int coarse = plan->esc_raw;
+    const bool ok = force || (plan->esc_ran && plan->exc == 0);
+    // levels worth testing: force (multi-GPU) tests both, the outcome combines later
+    const bool l0 = ok && d0 >= 0 && (force || coarse > 2 * d0 + 1);
+    const bool l1 = ok && d1 >= 0 && (force || coarse > 2 * d1 + 1) && (max_planes >= 2 || !l0);
+    if ((l0 || l1) && k > 0 && k <= (int64_t(1) << 30)) {
+        const int planes = (l0 && l1) ? 2 : 1;
         r.path = ADPB200_PATH_EMULATED;
-        r.slices = 1;
-        r.L = 0;
-        r.nsl = 1;
-        r.pairs = 1;
+        r.slices = planes;
+        r.L = 2 * (planes - 1);  // pairs d_a + d_b <= L: (0,0) [+ (0,1), (1,0), (1,1)]
+        r.nsl = planes;
+        r.pairs = planes * planes;
         r.variant = 64;
         r.kchunk = int32_t((k + 31) / 32 * 32);  // counts <= k: one int32 chunk
         r.nchunks = 1;
-        r.aux = delta;
-        r.exc = 0;  // the GEMM's zero-count flag
+        r.aux = l0 ? d0 : d1;
+        r.aux2 = d1;
+        r.lvl0 = l0 ? 0 : 1;
+        r.exc = 0;  // the GEMM's zero-count flags: bit 0 plane-0 level, bit 1 plane-1 level
     }
     *rplan = r;
 }
 
-__global__ void certify_finish_kernel(Plan* plan, const Plan* rplan) {
-    if (rplan->path == ADPB200_PATH_EMULATED && rplan->exc == 0) plan->esc_raw = 2 * rplan->aux + 1;
+// outcome v of an armed certificate plan (0, 1 or 2 as in certified_esc)
+__device__ __forceinline__ int certify_outcome(const Plan* rplan) {
+    if (rplan->path != ADPB200_PATH_EMULATED) return 2;
+    if (!(rplan->exc & 1)) return rplan->lvl0;
+    if (rplan->nsl == 2 && !(rplan->exc & 2)) return 1;
+    return 2;
+}
+
+__global__ void certify_finish_kernel(Plan* plan, const Plan* rplan, int target_bits) {
+    if (rplan->path == ADPB200_PATH_EMULATED)
+        plan->esc_raw = certified_esc(plan->esc_raw, certify_outcome(rplan), target_bits);
 }
 
 __global__ void dist_export_kernel(const Plan* plan, const Plan* rplan, int32_t* xchg, int certified) {
     int32_t x0 = plan->exc;
-    // (an unarmed certificate plan counts as failed: no count GEMM ran)
-    if (certified && (plan->exc != 0 || rplan->path != ADPB200_PATH_EMULATED || rplan->exc != 0))
-        x0 |= kXchgCertFail;
+    // (an unarmed certificate plan or an exceptional rank reports v = 2)
+    if (certified) x0 |= int32_t(plan->exc != 0 ? 2 : certify_outcome(rplan)) << kXchgCertShift;
     xchg[0] = x0;
     xchg[1] = plan->esc_raw;
 }
@@ -546,19 +565,17 @@ __global__ void dist_import_kernel(Plan* plan, const int32_t* xchg, int target_b
     const int32_t x0 = xchg[0];
     plan->exc = x0 & 3;
     plan->esc_raw = xchg[1];
-    const int delta = certify_delta(target_bits);
-    if (certified && !(x0 & kXchgCertFail) && delta >= 0 && plan->esc_raw > 2 * delta + 1)
-        plan->esc_raw = 2 * delta + 1;
+    if (certified) plan->esc_raw = certified_esc(plan->esc_raw, (x0 >> kXchgCertShift) & 3, target_bits);
 }
 
 void launch_certify_prep(const Plan* plan, Plan* rplan, int target_bits, int64_t k, cudaStream_t st,
-                         uint64_t* nlaunch, int force) {
-    certify_prep_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits, k, force);
+                         uint64_t* nlaunch, int force, int max_planes) {
+    certify_prep_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits, k, force, max_planes);
     ++*nlaunch;
 }
 
-void launch_certify_finish(Plan* plan, const Plan* rplan, cudaStream_t st, uint64_t* nlaunch) {
-    certify_finish_kernel<<<1, 1, 0, st>>>(plan, rplan);
+void launch_certify_finish(Plan* plan, const Plan* rplan, int target_bits, cudaStream_t st, uint64_t* nlaunch) {
+    certify_finish_kernel<<<1, 1, 0, st>>>(plan, rplan, target_bits);
     ++*nlaunch;
 }
 

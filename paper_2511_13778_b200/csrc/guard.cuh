@@ -56,10 +56,15 @@ void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, in
 // `plan` into the indicator-GEMM plan `rplan` (path kPathDone when there is
 // nothing to certify); finish lowers plan->esc_raw to 2*delta+1 when no
 // (i, j) count came out zero.
-// force = 1 (multi-GPU phases) arms rplan whatever this rank's coarsened result.
+// force = 1 (multi-GPU phases) arms rplan whatever this rank's coarsened result;
+// max_planes (1 or 2) bounds the indicator planes per operand (= certificate levels).
 void launch_certify_prep(const Plan* plan, Plan* rplan, int target_bits, int64_t k, cudaStream_t st,
-                         uint64_t* nlaunch, int force = 0);
-void launch_certify_finish(Plan* plan, const Plan* rplan, cudaStream_t st, uint64_t* nlaunch);
+                         uint64_t* nlaunch, int force = 0, int max_planes = 2);
+// Indicator planes per operand a forced (multi-GPU) certificate uses.
+inline int certify_planes(int target_bits) {
+    return (certify_delta(target_bits, 0) >= 0 ? 1 : 0) + (certify_delta(target_bits, 1) >= 0 ? 1 : 0);
+}
+void launch_certify_finish(Plan* plan, const Plan* rplan, int target_bits, cudaStream_t st, uint64_t* nlaunch);
 // Multi-GPU exchange block {exceptional | kXchgCertFail, esc_raw}: export before the
 // max-allreduce, import after it (the certificate applied when no rank failed it).
 void launch_dist_export(const Plan* plan, const Plan* rplan, int32_t* xchg, int certified, cudaStream_t st,

@@ -577,23 +577,28 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                 const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16);
                 if constexpr (NB == 64) {
                     if (g.zero_flag) {
-                        // certified ESC: diagonal 0 holds the indicator-product counts;
-                        // one zero count among the valid (i, j) voids the certificate
-                        bool zero = false;
+                        // certified ESC: diagonal 0 (and 2 for a two-level plan) holds the
+                        // indicator-product counts; one zero count among the valid (i, j)
+                        // voids that level's certificate
+                        uint32_t zero = 0;
+                        for (int lv = 0; lv < (ndiag >= 3 ? 2 : 1); ++lv) {
 #pragma unroll
-                        for (int b = 0; b < kCols / 8; ++b) {
-                            uint32_t v[8];
-                            tc::tmem_ld<8>(trow + uint32_t(jh * kCols + b * 8), v);
-                            tc::tmem_wait_ld();
+                            for (int b = 0; b < kCols / 8; ++b) {
+                                uint32_t v[8];
+                                tc::tmem_ld<8>(trow + uint32_t(2 * lv * NB + jh * kCols + b * 8), v);
+                                tc::tmem_wait_ld();
 #pragma unroll
-                            for (int cc = 0; cc < 8; ++cc) {
-                                const int64_t col = col_base + jh * kCols + b * 8 + cc;
-                                if (row_ok && col < col_end && v[cc] == 0u) zero = true;
+                                for (int cc = 0; cc < 8; ++cc) {
+                                    const int64_t col = col_base + jh * kCols + b * 8 + cc;
+                                    if (row_ok && col < col_end && v[cc] == 0u) zero |= 1u << lv;
+                                }
                             }
                         }
                         tc::fence_before();
                         tc::mbar_arrive(&hdr->tmem_empty);
-                        if (__any_sync(0xffffffffu, zero) && lane == 0) atomicOr(g.zero_flag, 1);
+#pragma unroll
+                        for (int lv = 0; lv < 2; ++lv)
+                            if (__any_sync(0xffffffffu, (zero >> lv) & 1u) && lane == 0) atomicOr(g.zero_flag, 1 << lv);
                         acc_phase ^= 1;
                         continue;
                     }

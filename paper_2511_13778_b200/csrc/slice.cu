@@ -170,7 +170,8 @@ struct SliceArgs {
     int32_t* scale;
     const Plan* plan;
     int slices_fixed;
-    int indicator;         // certified ESC: one plane of (e >= line_max - plan->aux) bytes
+    int indicator;         // certified ESC: plan->nsl planes of (e >= line_max - delta) bytes,
+                           // delta = plan->aux (plane 0) / plan->aux2 (plane 1)
 };
 
 // Certified-ESC indicator bytes of 8 elements: 1 where the element is finite,
@@ -242,14 +243,16 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
         const int64_t p0 = g * 8;
         const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
         if constexpr (S == 0) {
-            uint32_t lo, hi;
-            indicator_bytes(cur, lm, a.plan->aux, lo, hi);
-            int8_t* out = a.planes + plane_off(a, 0, line, p0);
-            if (kVec && nvalid == 8) {
-                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
-            } else {
-                const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-                for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
+            for (int d = 0; d < nsl; ++d) {
+                uint32_t lo, hi;
+                indicator_bytes(cur, lm, d == 0 ? a.plan->aux : a.plan->aux2, lo, hi);
+                int8_t* out = a.planes + plane_off(a, d, line, p0);
+                if (kVec && nvalid == 8) {
+                    *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+                } else {
+                    const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+                    for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
+                }
             }
         } else if constexpr (S <= 16) {
             typename Word<S>::T X[8];
@@ -376,13 +379,16 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) bits[q] = tile[og * 8 + q][ol];
     if (a.indicator) {
-        uint32_t lo, hi;
-        indicator_bytes(bits, lm, a.plan->aux, lo, hi);
-        const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-        int8_t* out = a.planes + plane_off(a, 0, line, p0);
-        if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
-        else
-            for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, 0, line, p0 + q)] = int8_t(w >> (8 * q));
+        for (int d = 0; d < nsl; ++d) {
+            uint32_t lo, hi;
+            indicator_bytes(bits, lm, d == 0 ? a.plan->aux : a.plan->aux2, lo, hi);
+            const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+            int8_t* out = a.planes + plane_off(a, d, line, p0);
+            if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0)
+                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+            else
+                for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, d, line, p0 + q)] = int8_t(w >> (8 * q));
+        }
         return;
     }
     switch (s) {

@@ -44,7 +44,7 @@ def run_virtual(gens):
 
 
 def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3,
-              overlap=True, zero_row=None, fused=False):
+              overlap=True, zero_row=None, fused=False, mutate=None):
     from paper_2511_13778_b200 import Handle
     from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
 
@@ -57,6 +57,8 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
     Ct = torch.rand((n, m), generator=g, device="cuda", dtype=torch.float64)
     if poison is not None:
         Bt[poison] = float("nan")
+    if mutate is not None:
+        mutate(Ast, Bt)
     if zero_row is not None:  # row i of op(A) all zeros
         if transa == "N":
             Ast[:, zero_row] = 0.0
@@ -152,6 +154,20 @@ def test_dist_certified_esc(gpu, world, m, n, k):
     assert all(r == res[0] for r in res)
     assert res[0][0] == 0 and res[0][1] > 7
     assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    # a wide exponent range: level 0 fails somewhere, level 1 (s0 + 1 = 8 slices) holds everywhere
+    def widen(Ast, Bt):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(5)
+        Ast.mul_(torch.exp2(torch.randint(-40, 40, Ast.shape, generator=g, device="cuda").double()))
+
+    got, ref, res = dist_case(gpu, world, m, n, k, cfg, mutate=widen)
+    assert all(r == res[0] for r in res)
+    assert res[0][0] == 0 and res[0][1] == 8
+    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    for fused in (True,):
+        got, ref, res = dist_case(gpu, world, m, n, k, cfg, mutate=widen, fused=fused)
+        assert res[0][1] == 8
+        assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
     # NaN in a slab: native everywhere
     got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 5))
     assert all(r[0] == 1 for r in res)

@@ -37,7 +37,8 @@ def _make(name, m, k, n, seed):
 CASES = [("u11", 256, 300, 260, 53), ("u11", 300, 1000, 512, 53), ("u12", 512, 256, 300, 53),
          ("wide", 300, 400, 280, 53), ("zero_col", 256, 512, 256, 53), ("sparse", 260, 700, 300, 53),
          ("subnormal", 256, 260, 256, 53), ("u11", 256, 300, 260, 50), ("u11", 256, 300, 260, 54),
-         ("u11", 1000, 640, 600, 53), ("late_max", 256, 1000, 300, 53)]
+         ("u11", 1000, 640, 600, 53), ("late_max", 256, 1000, 300, 53), ("wide", 300, 400, 280, 54),
+         ("wide", 300, 600, 280, 50)]
 
 
 @pytest.mark.parametrize("name,m,k,n,tb", CASES)
@@ -49,6 +50,8 @@ def test_certified_decision_and_bits(gpu, port, name, m, k, n, tb):
     want_esc = esc_certified(a, b, coarse, tb)
     if name == "late_max":
         assert want_esc == coarse and esc_certified(a, b, coarse, tb, window=k) == 1
+    if name == "wide" and tb == 53:
+        assert want_esc == 9 < coarse  # the second certificate level
     path, _, s, _, _, _ = port.decide(0, 0, m, n, k, want_esc, Config(target_bits=tb))
     cfg = gpu.AdpConfig(target_bits=tb, esc_method="certified")
     # device path (CUDA tensors) and the streamed host path (numpy)
