@@ -251,6 +251,13 @@ int adpb200_esc_coarsened(adpb200_handle handle, const int32_t* a_max, const int
                           const int32_t* a_line, const int32_t* b_max, const int32_t* b_min,
                           const int32_t* b_line, int64_t m, int64_t n, int64_t blocks,
                           int target_bits, int32_t* out, void* stream);
+/* esc_exact (esc.cpp:61-87), the O(mnk) ESC the reference's tests use as the
+ * coarsened ESC's oracle, as a DPX max-plus kernel: A m x k and B k x n
+ * row-major; out (device int32[3]) = {esc_bits, window_bits, slices_required};
+ * *exceptional (device int32) = 1 on Inf/NaN input (the reference throws
+ * std::domain_error; out is then meaningless). */
+int adpb200_esc_exact(adpb200_handle handle, const double* A, const double* B, int64_t m, int64_t n,
+                      int64_t k, int target_bits, int32_t* out, int32_t* exceptional, void* stream);
 /* decompose (slicing.cpp:90-136): digits = slices planes of lines x len int8
  * (plane-major, each plane line-major = K-major), scale_exp: lines int32. */
 int adpb200_decompose(adpb200_handle handle, const double* A, int64_t rows, int64_t cols,

@@ -19,6 +19,7 @@ from .adp import (  # noqa: F401
     dgemm_host,
     emulated_gemm,
     esc_coarsened,
+    esc_exact,
     native_gemm,
     parse_mode,
     recompose,

@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
         "adpb200_slice_pair_mm": (C.c_int, [vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, vp, vp]),
         "adpb200_emulated_gemm": (C.c_int, [vp, vp, vp, i64, i64, i64, f64, f64, vp, vp, C.c_int, C.c_int, vp]),
         "adpb200_recompose": (C.c_int, [vp, vp, i64, i64, C.c_int, vp, vp, f64, f64, vp, vp, vp]),
+        "adpb200_esc_exact": (C.c_int, [vp, vp, vp, i64, i64, i64, C.c_int, vp, vp, vp]),
         "adpb200_native_gemm": (C.c_int, [vp, vp, vp, i64, i64, i64, f64, f64, vp, vp, vp]),
         "adpb200_dist_sizes": (C.c_int, [i64, i64, C.c_int, popt, C.POINTER(i64)]),
         "adpb200_dist_decision": (C.c_int, [popt, C.POINTER(i32), i64, i64, i64, C.POINTER(i32)]),
@@ -137,7 +138,7 @@ EXPORTED = (
     "adpb200_decide_host", "adpb200_dgemm", "adpb200_adp_gemm", "adpb200_dgemm_rows", "adpb200_dgemm_host",
     "adpb200_adp_gemm_host", "adpb200_scan", "adpb200_block_stats",
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",
-    "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read", "adpb200_recompose",
+    "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read", "adpb200_recompose", "adpb200_esc_exact",
     "adpb200_dist_sizes", "adpb200_dist_decision", "adpb200_dgemm_dist", "adpb200_ipc_alloc",
     "adpb200_ipc_open", "adpb200_ipc_close", "adpb200_ipc_free",
     "adpb200_geqrf_blocked", "adpb200_qr_materialize_q", "adpb200_qr_residual",

@@ -434,6 +434,24 @@ def esc_coarsened(a, b, block_len: int = 256, target_bits: int = 53, handle: Opt
     return tuple(int(x) for x in out.cpu().tolist())
 
 
+def esc_exact(a, b, target_bits: int = 53, handle: Optional[Handle] = None):
+    """esc_exact (esc.cpp:61-87) on the GPU: (esc_bits, window_bits, slices_required);
+    ValueError (the reference's std::domain_error) on Inf/NaN input."""
+    (m, k), (k2, n) = _shape2(a), _shape2(b)
+    if k != k2:
+        raise ValueError("esc_exact: inner dimensions differ")
+    dev = _device(a.device.index if isinstance(a, torch.Tensor) else None)
+    handle = handle or Handle.default(dev.index)
+    A, B = _to_dev(a, dev), _to_dev(b, dev)
+    out = torch.zeros(3, dtype=torch.int32, device=dev)
+    exc = torch.zeros(1, dtype=torch.int32, device=dev)
+    check(lib().adpb200_esc_exact(handle.h, _ptr(A), _ptr(B), m, n, k, target_bits, _ptr(out), _ptr(exc),
+                                  _stream(dev)))
+    if int(exc.item()):
+        raise ValueError("esc: Inf or NaN input")
+    return tuple(int(x) for x in out.cpu().tolist())
+
+
 def native_gemm(a, b, alpha: float = 1.0, beta: float = 0.0, c=None, handle: Optional[Handle] = None):
     """native_gemm (oracle.cpp:7-28) in the reference's summation order."""
     host = not isinstance(a, torch.Tensor)

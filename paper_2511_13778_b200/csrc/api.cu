@@ -1501,6 +1501,26 @@ int adpb200_esc_coarsened(adpb200_handle h, const int32_t* a_max, const int32_t*
     return cuda_check(cudaGetLastError(), "esc launch");
 }
 
+int adpb200_esc_exact(adpb200_handle h, const double* A, const double* B, int64_t m, int64_t n, int64_t k,
+                      int target_bits, int32_t* out, int32_t* exceptional, void* stream) {
+    if (!h) return fail(ADPB200_ERR_RUNTIME, "esc_exact: null handle");
+    if (m < 0 || n < 0 || k < 0) return fail(3, "esc_exact: negative dimension");
+    if (target_bits < 1) return fail(3, "required_slices: target_bits must be positive");
+    if (!out || !exceptional) return fail(3, "esc_exact: null output");
+    cudaSetDevice(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t sa = align_up(size_t(m) * k * 4 + 16, 256), sb = align_up(size_t(k) * n * 4 + 16, 256),
+                 sr = align_up(size_t(m) * 4 + 16, 256), sc = align_up(size_t(n) * 4 + 16, 256);
+    int rc = ensure_ws(h, sa + sb + sr + sc, st);
+    if (!rc) rc = cuda_check(cudaMemsetAsync(out, 0, 3 * sizeof(int32_t), st), "cudaMemsetAsync(out)");
+    if (!rc) rc = cuda_check(cudaMemsetAsync(exceptional, 0, sizeof(int32_t), st), "cudaMemsetAsync(exc)");
+    if (rc) return rc;
+    launch_esc_exact(A, B, m, n, k, at<int32_t>(h, 0), at<int32_t>(h, sa), at<int32_t>(h, sa + sb),
+                     at<int32_t>(h, sa + sb + sr), exceptional, out, st, &h->launches);
+    launch_esc_finish(out, target_bits, st, &h->launches);
+    return cuda_check(cudaGetLastError(), "esc_exact launch");
+}
+
 int adpb200_decompose(adpb200_handle h, const double* A, int64_t rows, int64_t cols, int orient, int slices,
                       int8_t* digits, int32_t* scale_exp, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "decompose: null handle");

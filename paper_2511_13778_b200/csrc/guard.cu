@@ -597,4 +597,105 @@ void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n,
     ++*nlaunch;
 }
 
+// ---- esc_exact stage export (esc.cpp:26-87) ---------------------------------------
+namespace {
+constexpr int32_t kExactSentinel = -(1 << 28);  // zeros: two of them still sum above INT_MIN
+
+// exponent field of a row-major rows x cols matrix (zeros -> sentinel), exceptional flag
+__global__ void exp_field_kernel(const double* __restrict__ a, int64_t count, int32_t* __restrict__ e,
+                                 int32_t* exc) {
+    bool bad = false;
+    for (int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < count; x += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t b = __double_as_longlong(__ldg(a + x));
+        if (((b >> 52) & 0x7ff) == 0x7ff) {
+            bad = true;
+            e[x] = kExactSentinel;
+        } else {
+            e[x] = (b << 1) == 0 ? kExactSentinel : eff_exp(b);
+        }
+    }
+    if (bad) atomicOr(exc, 1);
+}
+
+// line maxima: rows of e (stride_line = cols, stride_pos = 1) or columns (1, cols)
+__global__ void exp_line_max_kernel(const int32_t* __restrict__ e, int64_t lines, int64_t len, int64_t s_line,
+                                    int64_t s_pos, int32_t* __restrict__ out) {
+    const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (line >= lines) return;
+    int32_t mx = kExactSentinel;
+    for (int64_t p = 0; p < len; ++p) mx = max(mx, e[line * s_line + p * s_pos]);
+    out[line] = mx;
+}
+
+// z_ij = max_l ea[i][l] + eb[l][j] (DPX add-max), 64 x 64 outputs per CTA, 4 x 4 per thread;
+// span_ij = rowmax_i + colmax_j - z_ij + 1 over the (i, j) with a nonzero product
+__global__ void __launch_bounds__(256) esc_exact_kernel(const int32_t* __restrict__ ea, const int32_t* __restrict__ eb,
+                                                        const int32_t* __restrict__ rmax,
+                                                        const int32_t* __restrict__ cmax, int64_t m, int64_t n,
+                                                        int64_t k, int32_t* out) {
+    __shared__ int32_t As[32][65];
+    __shared__ int32_t Bs[32][64];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t i0 = int64_t(blockIdx.y) * 64, j0 = int64_t(blockIdx.x) * 64;
+    int32_t z[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) z[a][b] = 2 * kExactSentinel;
+    for (int64_t l0 = 0; l0 < k; l0 += 32) {
+        for (int t = threadIdx.x; t < 64 * 32; t += 256) {
+            const int r = t / 32, c = t % 32;  // A tile: row r, position c (coalesced along positions)
+            const int64_t gi = i0 + r, gl = l0 + c;
+            As[c][r] = (gi < m && gl < k) ? ea[gi * k + gl] : kExactSentinel;
+            const int br = t / 64, bc = t % 64;  // B tile: position br, column bc
+            const int64_t bl = l0 + br, bj = j0 + bc;
+            Bs[br][bc] = (bl < k && bj < n) ? eb[bl * n + bj] : kExactSentinel;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int c = 0; c < 32; ++c) {
+            int32_t av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = As[c][ty * 4 + a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Bs[c][tx * 4 + b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) z[a][b] = __viaddmax_s32(av[a], bv[b], z[a][b]);
+        }
+        __syncthreads();
+    }
+    int32_t esc = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int64_t gi = i0 + ty * 4 + a, gj = j0 + tx * 4 + b;
+            if (gi < m && gj < n && z[a][b] > kExactSentinel / 2) esc = max(esc, rmax[gi] + cmax[gj] - z[a][b] + 1);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) esc = max(esc, __shfl_xor_sync(0xffffffffu, esc, o));
+    if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(out, esc);
+}
+}  // namespace
+
+void launch_esc_exact(const double* A, const double* B, int64_t m, int64_t n, int64_t k, int32_t* ea, int32_t* eb,
+                      int32_t* rmax, int32_t* cmax, int32_t* exc, int32_t* out, cudaStream_t st, uint64_t* nlaunch) {
+    auto grid_for = [](int64_t count) {
+        const int64_t want = (count + 255) / 256;
+        return int(want < int64_t(num_sms()) * 16 ? (want > 0 ? want : 1) : int64_t(num_sms()) * 16);
+    };
+    exp_field_kernel<<<grid_for(m * k), 256, 0, st>>>(A, m * k, ea, exc);
+    exp_field_kernel<<<grid_for(k * n), 256, 0, st>>>(B, k * n, eb, exc);
+    exp_line_max_kernel<<<unsigned((m + 255) / 256 > 0 ? (m + 255) / 256 : 1), 256, 0, st>>>(ea, m, k, k, 1, rmax);
+    exp_line_max_kernel<<<unsigned((n + 255) / 256 > 0 ? (n + 255) / 256 : 1), 256, 0, st>>>(eb, n, k, 1, n, cmax);
+    *nlaunch += 4;
+    if (m > 0 && n > 0 && k > 0) {
+        dim3 grid(unsigned((n + 63) / 64), unsigned((m + 63) / 64));
+        esc_exact_kernel<<<grid, 256, 0, st>>>(ea, eb, rmax, cmax, m, n, k, out);
+        ++*nlaunch;
+    }
+}
+
 }  // namespace adpb200

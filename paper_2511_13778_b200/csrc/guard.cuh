@@ -33,6 +33,11 @@ void launch_gather_planes(const int8_t* recs, int64_t rec_bytes, int64_t hdr, in
                           int nsl, int8_t* planes, int64_t slots, int64_t plane_stride, int32_t* scale,
                           cudaStream_t st, uint64_t* nlaunch, int r_first = 0);
 void launch_esc_finish(int32_t* out, int target_bits, cudaStream_t st, uint64_t* nlaunch);
+// esc_exact (esc.cpp:61-87) stage export: A m x k and B k x n row-major; exponent
+// fields ea (m*k) / eb (k*n) and maxima rmax (m) / cmax (n) are scratch; exc |= 1 on
+// Inf/NaN; out[0] = max(0, max span) (must start at 0).
+void launch_esc_exact(const double* A, const double* B, int64_t m, int64_t n, int64_t k, int32_t* ea, int32_t* eb,
+                      int32_t* rmax, int32_t* cmax, int32_t* exc, int32_t* out, cudaStream_t st, uint64_t* nlaunch);
 void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int32_t* dst, cudaStream_t st,
                           uint64_t* nlaunch);
 // swap_ab: the internal operands are the user's B (A-lines) and A (B-lines).

@@ -92,3 +92,37 @@ def test_certified_4096_u11_accuracy_and_sampled_bits(gpu, port):
     want = port.emulated_gemm(A[rows].cpu().numpy(), B[:, cols].cpu().numpy(), 7)
     assert_bitwise(Cx[rows][:, cols].cpu().numpy(), want, nan_equiv=False)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name,m,k,n", [("u11", 200, 300, 150), ("u12", 64, 700, 80), ("wide", 130, 257, 65),
+                                        ("zero_col", 100, 100, 100), ("sparse", 150, 400, 120),
+                                        ("subnormal", 70, 90, 50), ("u11", 1, 1, 1), ("u11", 33, 0, 17)])
+def test_device_esc_exact_matches_reference(gpu, port, name, m, k, n):
+    """esc_exact (esc.cpp:61-87) as a device stage (DPX max-plus): the same
+    EscReport as the C restatement, and the certified ESC never below it."""
+    a, b = _make(name, m, max(k, 1), n, 7 + m)
+    a, b = a[:, :k], b[:k, :]
+    for tb in (53, 50):
+        assert gpu.esc_exact(a, b, tb) == tuple(port.esc_exact(a, b, tb))
+    if k:
+        coarse = port.esc_coarsened(a, b, 256, 53)[0]
+        assert gpu.esc_exact(a, b)[0] <= esc_certified(a, b, coarse, 53) or name in ("zero_col", "sparse")
+    bad = a.copy()
+    if bad.size:
+        bad.flat[0] = np.nan
+        with pytest.raises(ValueError):
+            gpu.esc_exact(bad, b)
+
+
+def test_certified_bracket_at_2048(gpu):
+    """esc_exact <= certified <= coarsened on the device at 2048^3 (U[-1,1], U(1,2), wide)."""
+    import torch
+
+    for name in ("u11", "u12", "wide"):
+        a, b = _make(name, 2048, 2048, 2048, 11)
+        A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        exact = gpu.esc_exact(A, B)[0]
+        _, tc_ = gpu.adp_gemm(A, B, config=gpu.AdpConfig(mode=gpu.AdpMode.ForceEmulate, guardrails_forced=True))
+        _, tx = gpu.adp_gemm(A, B, config=gpu.AdpConfig(mode=gpu.AdpMode.ForceEmulate, guardrails_forced=True,
+                                                        esc_method="certified"))
+        assert exact <= tx.esc_bits <= tc_.esc_bits, (name, exact, tx.esc_bits, tc_.esc_bits)
