@@ -48,10 +48,10 @@ def parse():
     p.add_argument("--esc", choices=["coarsened", "certified"], default="coarsened",
                    help="ESC method of the timed calls: the reference's coarsened ESC (default) or the "
                         "certified ESC option (single-GPU paths)")
-    p.add_argument("--dist", choices=["fused", "allgather"], default="fused",
-                   help="N > 1: fused = the GEMM reads every rank's B planes in place over NVLink (CUDA IPC "
-                        "peer mappings, phase 7); allgather = NCCL all-gather of the planes overlapped with "
-                        "the own-column GEMM (phases 5/6)")
+    p.add_argument("--dist", choices=["fused", "allgather"], default="allgather",
+                   help="N > 1: allgather (default) = NCCL all-gather of the B planes overlapped with the "
+                        "own-column GEMM (phases 5/6); fused = the GEMM reads every rank's B planes in place "
+                        "over NVLink (CUDA IPC peer mappings, phase 7; not yet timed on an NVLink node)")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
