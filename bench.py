@@ -48,10 +48,12 @@ def parse():
     p.add_argument("--esc", choices=["coarsened", "certified"], default="coarsened",
                    help="ESC method of the timed calls: the reference's coarsened ESC (default) or the "
                         "certified ESC option (single-GPU paths)")
-    p.add_argument("--dist", choices=["fused", "allgather"], default="allgather",
+    p.add_argument("--dist", choices=["fused", "pull", "allgather"], default="allgather",
                    help="N > 1: allgather (default) = NCCL all-gather of the B planes overlapped with the "
                         "own-column GEMM (phases 5/6); fused = the GEMM reads every rank's B planes in place "
-                        "over NVLink (CUDA IPC peer mappings, phase 7; not yet timed on an NVLink node)")
+                        "over NVLink (CUDA IPC peer mappings, phase 7); pull = the copy engines pull each "
+                        "peer's planes while the GEMM of the previous rank's columns runs (phase 7 per rank). "
+                        "fused / pull are not yet timed on an NVLink node")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
@@ -251,17 +253,20 @@ def main():
     cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET, esc_method=args.esc)
     trace_buf = torch.zeros(_lib.TRACE_BYTES, dtype=torch.uint8, device=dev)
     peers, dist_mode = None, args.dist if world > 1 else None
-    if world > 1 and args.dist == "fused":
+    if world > 1 and args.dist in ("fused", "pull"):
         from paper_2511_13778_b200.dist import PeerSlabs
 
         try:  # slab buffers sized for the largest plane count any config here can ask for
             peers = PeerSlabs(n, k, adp.AdpConfig(), device=dev.index)
-        except Exception as e:  # noqa: BLE001 — no IPC / peer access: fall back to the NCCL all-gather
-            dist_mode = f"allgather (fused unavailable: {str(e)[:120]})"
+        except Exception as e:  # noqa: BLE001 — no IPC / peer access (raised on every rank alike):
+            # fall back to the NCCL all-gather
+            dist_mode = f"allgather ({args.dist} unavailable: {str(e)[:160]})"
+            print(f"bench: {dist_mode}", file=sys.stderr, flush=True)
 
     def step(config=cfg, A=At, B=Bt, Cm=Ct, trace=None):
         if world > 1:
-            dgemm_dist("N", m_global, m, n, k, 1.0, A, m, B, 0.0, Cm, m, config, handle, trace=trace, peers=peers)
+            dgemm_dist("N", m_global, m, n, k, 1.0, A, m, B, 0.0, Cm, m, config, handle, trace=trace, peers=peers,
+                       pull=args.dist == "pull")
         else:
             adp.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, Cm, m, config, handle, trace=trace)
 
@@ -310,19 +315,6 @@ def main():
     wall1 = time.time()
     launches = handle.launches() - launches0
     clocks = sampler.stop(wall0, wall1)
-    if clocks is not None and clocks["samples"] < 10 and not c4:
-        # a short timed region leaves few samples (nvidia-smi polls every 100 ms and
-        # its power reading lags): soak the same step for ~2 s, sampled the same way,
-        # and report it beside the timed-region samples
-        soak = ClockSampler(dev.index)
-        soak.start()
-        time.sleep(0.5)
-        s0 = time.time()
-        while time.time() - s0 < 2.0:
-            for _ in range(10):
-                step()
-            torch.cuda.synchronize()
-        clocks["soak_after_timed_region"] = soak.stop(s0 + 0.5, time.time())
     stage = handle.profile_read()
     handle.profile_enable(0)
     ms = e0.elapsed_time(e1) / args.steps
@@ -330,6 +322,19 @@ def main():
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    if clocks is not None and clocks["samples"] < 10 and not c4:
+        # a short timed region leaves few samples (nvidia-smi polls every 100 ms and
+        # its power reading lags): soak the same step for ~2 s, sampled the same way,
+        # and report it beside the timed-region samples. The step count comes from
+        # the max-reduced ms, so every rank runs the same collectives.
+        soak = ClockSampler(dev.index)
+        soak.start()
+        time.sleep(0.5)
+        s0 = time.time()
+        for _ in range(max(10, min(2000, int(2000.0 / max(ms, 1e-3))))):
+            step()
+        barrier()
+        clocks["soak_after_timed_region"] = soak.stop(s0 + 0.5, time.time())
     flops_global = 2.0 * m_global * n * k
     value = flops_global / (ms * 1e-3) / 1e12
 
@@ -510,7 +515,9 @@ def main():
                        "path": trace.path, "pairs": pairs, "gemm_variant": trace.gemm_variant,
                        "parallelism": (f"row-block x{world}: A/C rows per rank, B column slabs; B exponent "
                                        "stats all-gathered, ADP decision max-allreduced (NCCL); B slice planes: "
-                                       + ("read in place by the GEMM over NVLink (fused phase 7)" if peers is not None
+                                       + ({"fused": "read in place by the GEMM over NVLink (fused phase 7)",
+                                           "pull": "pulled rank by rank by the copy engines under the GEMM "
+                                                   "(phase 7 per rank)"}.get(args.dist) if peers is not None
                                           else "NCCL all-gather overlapped with the own-column GEMM")
                                        + f" [--dist {dist_mode}]")
                        if world > 1 else "single GPU",

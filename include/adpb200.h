@@ -207,6 +207,10 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
  *            scales from the record headers. Every rank must be past phase 3
  *            before any rank starts phase 7, and slabs must stay untouched
  *            until every rank has finished it (two barriers). world <= 8.
+ *            A null entry skips that rank's columns: one launch per rank, each
+ *            after a pull of that rank's record into local memory
+ *            (adpb200_copy_async on a copy stream), pipelines the transfer of
+ *            rank r+1's planes with the GEMM of rank r's columns.
  * Same decision and slice count on every rank: the assembled C is
  * bit-identical to the single-GPU adpb200_dgemm('N'/transa, 'N'). */
 int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]);
@@ -217,6 +221,9 @@ int adpb200_ipc_alloc(int device, int64_t bytes, void** ptr, uint8_t handle[64])
 int adpb200_ipc_open(int device, const uint8_t handle[64], void** ptr);
 int adpb200_ipc_close(void* ptr);
 int adpb200_ipc_free(void* ptr);
+/* Stream-ordered copy between any device pointers of this process, incl. IPC-mapped
+ * peer buffers (the copy engines pull over NVLink). */
+int adpb200_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
 /* decide() on the reduced xchg (host copy): out = path, slices, nsl (planes to
  * gather; 0 on the native path), GEMM variant. */
 int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global,

@@ -114,6 +114,7 @@ def lib() -> C.CDLL:
         "adpb200_ipc_open": (C.c_int, [C.c_int, C.POINTER(C.c_uint8), C.POINTER(vp)]),
         "adpb200_ipc_close": (C.c_int, [vp]),
         "adpb200_ipc_free": (C.c_int, [vp]),
+        "adpb200_copy_async": (C.c_int, [vp, vp, i64, vp]),
         "adpb200_geqrf_blocked": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, popt, vp]),
         "adpb200_qr_materialize_q": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "adpb200_qr_residual": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
@@ -140,7 +141,7 @@ EXPORTED = (
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",
     "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read", "adpb200_recompose", "adpb200_esc_exact",
     "adpb200_dist_sizes", "adpb200_dist_decision", "adpb200_dgemm_dist", "adpb200_ipc_alloc",
-    "adpb200_ipc_open", "adpb200_ipc_close", "adpb200_ipc_free",
+    "adpb200_ipc_open", "adpb200_ipc_close", "adpb200_ipc_free", "adpb200_copy_async",
     "adpb200_geqrf_blocked", "adpb200_qr_materialize_q", "adpb200_qr_residual",
     "adpb200_dd_gemm", "adpb200_error_report", "adpb200_gen_uniform_rect", "adpb200_gen_test2",
 )

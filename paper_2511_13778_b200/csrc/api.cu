@@ -1004,6 +1004,13 @@ int adpb200_ipc_open(int device, const uint8_t handle[64], void** ptr) {
 
 int adpb200_ipc_close(void* ptr) { return cuda_check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle"); }
 
+int adpb200_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(3, "copy_async: bad arguments");
+    if (bytes == 0) return ADPB200_OK;
+    return cuda_check(cudaMemcpyAsync(dst, src, size_t(bytes), cudaMemcpyDefault, static_cast<cudaStream_t>(stream)),
+                      "cudaMemcpyAsync(pull)");
+}
+
 int adpb200_ipc_free(void* ptr) { return cuda_check(cudaFree(ptr), "cudaFree(ipc)"); }
 
 int adpb200_dist_decision(const adpb200_options* opt, const int32_t xchg[2], int64_t m_global, int64_t n, int64_t k,

@@ -562,10 +562,11 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
             const int32_t* sbase = g.scale_b;
             if (g.peer_world > 0) {
                 const int r = int(nt / peer_tpr);
-                col_base = r * g.peer_nr + (nt - r * peer_tpr) * NB;
-                col_end = (r + 1) * g.peer_nr < g.N ? (r + 1) * g.peer_nr : g.N;
-                sbase = g.peer_scale[r];  // rank r's record header: its columns' scales
-                scol0 = r * g.peer_nr;
+                const int64_t rid = g.peer_rank[r];
+                col_base = rid * g.peer_nr + (nt - r * peer_tpr) * NB;
+                col_end = (rid + 1) * g.peer_nr < g.N ? (rid + 1) * g.peer_nr : g.N;
+                sbase = g.peer_scale[r];  // rank rid's record header: its columns' scales
+                scol0 = rid * g.peer_nr;
             }
             const int64_t lane_col = col_base + jh * kCols + lane;
             const int eb_lane = (lane < kCols && lane_col < col_end) ? __ldg(sbase + (lane_col - scol0)) : 0;
@@ -933,16 +934,17 @@ struct PeerCacheEntry {
     const int8_t* peers[kMaxPeers] = {};
     int64_t slots_a = -1, nkb = -1, nr = -1, hdr = -1;
     int cap = -1, world = -1, nsl = -1;
+    int ranks[kMaxPeers] = {};
     PlaneMaps maps;
 };
 
 template <int NB>
 int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap,
-                   const int8_t* const* peer_slabs, int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g,
-                   cudaStream_t st) {
+                   const int8_t* const* peer_slabs, const int* ranks, int world, int64_t nr, int64_t hdr, int nsl,
+                   const GemmArgs& g, cudaStream_t st) {
     bool hit = e.pa == planes_a && e.slots_a == slots_a && e.nkb == nkb && e.cap == cap && e.world == world &&
                e.nr == nr && e.hdr == hdr && e.nsl == nsl;
-    for (int r = 0; hit && r < world; ++r) hit = e.peers[r] == peer_slabs[r];
+    for (int r = 0; hit && r < world; ++r) hit = e.peers[r] == peer_slabs[r] && e.ranks[r] == ranks[r];
     if (!hit) {
         const int nbox = cap < kMaxBox ? cap : kMaxBox;
         for (int i = 0; i < kMaxBox; ++i)
@@ -957,12 +959,18 @@ int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, i
         e.nr = nr;
         e.hdr = hdr;
         e.nsl = nsl;
-        for (int r = 0; r < world; ++r) e.peers[r] = peer_slabs[r];
+        for (int r = 0; r < world; ++r) {
+            e.peers[r] = peer_slabs[r];
+            e.ranks[r] = ranks[r];
+        }
     }
     GemmArgs a = g;
     a.peer_world = world;
     a.peer_nr = nr;
-    for (int r = 0; r < world; ++r) a.peer_scale[r] = reinterpret_cast<const int32_t*>(peer_slabs[r]);
+    for (int r = 0; r < world; ++r) {
+        a.peer_scale[r] = reinterpret_cast<const int32_t*>(peer_slabs[r]);
+        a.peer_rank[r] = ranks[r];
+    }
     a.nt_begin = a.nt_end = 0;
     a.debug = 0;
     a.smem_bytes = kGemmSmemBytes;
@@ -981,13 +989,23 @@ int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int 
                       int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g, cudaStream_t st,
                       uint64_t* nlaunch) {
     if (world < 1 || world > kMaxPeers || nsl < 1 || nsl > cap || nsl > kMaxBox || nr % 8 != 0) return -2;
+    // the ranks whose columns this launch computes (null entries are skipped)
+    const int8_t* act[kMaxPeers];
+    int ranks[kMaxPeers];
+    int na = 0;
+    for (int r = 0; r < world; ++r)
+        if (peer_slabs[r]) {
+            act[na] = peer_slabs[r];
+            ranks[na++] = r;
+        }
+    if (na == 0) return 0;
     static thread_local PeerCacheEntry cache[5];
     int rc = 0;
-    if (!rc) rc = launch_peer_nb<64>(cache[0], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<48>(cache[1], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<32>(cache[2], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<16>(cache[3], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, peer_slabs, world, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<64>(cache[0], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<48>(cache[1], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<32>(cache[2], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<16>(cache[3], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
     *nlaunch += 5;
     return rc;
 }

@@ -35,14 +35,16 @@ struct GemmArgs {
     // fused all-gather -> GEMM (multi-GPU phase 7): B planes and scales read in place
     // from every rank's slab record over peer memory; rank r owns columns
     // [r*peer_nr, (r+1)*peer_nr), tiled on its own (partial last tile per rank)
-    int peer_world;            // 0: B from planes_b
+    int peer_world;            // 0: B from planes_b; else the number of ranks whose tiles run
     int64_t peer_nr;
     const int32_t* peer_scale[kMaxPeers];
+    int peer_rank[kMaxPeers];  // global rank of each of those entries (its column offset)
 };
 
 // Fused peer variant of launch_igemm: B from world slab records ([scale int32 x nr |
 // pad to hdr][cap planes of nkb x nr x 32 B], peer_slabs[r] = rank r's record as
-// mapped in this process), nsl planes each. Launches every variant (one does work).
+// mapped in this process, or nullptr to skip rank r's columns), nsl planes each.
+// Launches every variant (one does work).
 int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap, const int8_t* const* peer_slabs,
                       int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g, cudaStream_t st,
                       uint64_t* nlaunch);

@@ -105,7 +105,7 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
                      A: torch.Tensor, lda: int, B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int,
                      config: Optional[AdpConfig] = None, handle: Optional[Handle] = None,
                      trace: Optional[torch.Tensor] = None, rank: int = 0, overlap: bool = True,
-                     slab_ptrs: Optional[Sequence[int]] = None):
+                     slab_ptrs: Optional[Sequence[int]] = None, pull: bool = False):
     """The B-distributed ADP DGEMM of one rank as a generator of collective
     requests, so that the same orchestration runs under torch.distributed
     (dgemm_dist) and under a single-process multi-rank driver (the tests):
@@ -123,6 +123,10 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     the tests) there is no plane all-gather: after a barrier the fused phase 7
     GEMM reads the B planes of every rank in place over peer memory
         ("barrier",)               every rank past its phase 3 (slab sliced)
+    and with pull=True the copy engines pull each peer's record into local
+    memory on a side stream while the GEMM of the previous rank's columns runs
+    (one phase-7 launch per rank, own columns first): the transfer overlaps the
+    math rank by rank and the GEMM reads local, L2-cached planes.
 
     Rank owns rows of op(A) / C (column-major local block, ldc) and the B
     column slab B_slab (k x n/world column-major, compact: a (n/world, k)
@@ -155,8 +159,32 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     path, s, nsl, _ = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)  # (syncs: slab sliced)
     if nsl > 0 and fused:
         yield ("barrier",)
-        ptrs = (C.c_void_p * world)(*[int(p) for p in slab_ptrs])
-        phase(7, C.cast(ptrs, C.c_void_p), nsl)
+        if not pull:
+            ptrs = (C.c_void_p * world)(*[int(p) for p in slab_ptrs])
+            phase(7, C.cast(ptrs, C.c_void_p), nsl)
+            return (path, s, nsl)
+        rec = hdr + nsl * plane_bytes
+        staging = torch.empty(rec * world, dtype=torch.int8, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(dev)
+        staging.record_stream(side)
+        side.wait_stream(cur)
+        order = [(rank + j) % world for j in range(world)]
+        ready = {}
+        with torch.cuda.stream(side):
+            for r in order[1:]:
+                check(lib().adpb200_copy_async(C.c_void_p(staging.data_ptr() + r * rec), C.c_void_p(int(slab_ptrs[r])),
+                                               rec, C.c_void_p(side.cuda_stream)))
+                ready[r] = torch.cuda.Event()
+                ready[r].record(side)
+        for r in order:
+            ptrs = (C.c_void_p * world)()
+            if r == rank:
+                ptrs[r] = int(slab_ptrs[r])
+            else:
+                cur.wait_event(ready[r])
+                ptrs[r] = staging.data_ptr() + r * rec
+            phase(7, C.cast(ptrs, C.c_void_p), nsl)
         return (path, s, nsl)
     if nsl > 0:
         rec = hdr + nsl * plane_bytes
@@ -178,16 +206,17 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
 def dgemm_dist(transa: str, m_global: int, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
                B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int, config: Optional[AdpConfig] = None,
                handle: Optional[Handle] = None, group=None, trace: Optional[torch.Tensor] = None,
-               peers: Optional["PeerSlabs"] = None):
+               peers: Optional["PeerSlabs"] = None, pull: bool = False):
     """This rank's share of a row-partitioned ADP DGEMM with B distributed by
     column slabs: exponent stats and B slice planes all-gathered, the ADP
     decision input max-allreduced, all over NCCL (torch.distributed). With
     `peers` (a PeerSlabs for this n, k) the plane all-gather is replaced by
-    the fused phase 7: the GEMM reads every rank's planes over NVLink."""
+    the fused phase 7: the GEMM reads every rank's planes over NVLink (pull=True:
+    the copy engines pull them rank by rank while the GEMM runs on local copies)."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
     gen = dgemm_dist_steps(world, transa, m_global, m, n, k, alpha, A, lda, B_slab, beta, C_, ldc, config, handle,
-                           trace, rank=rank, slab_ptrs=peers.next() if peers is not None else None)
+                           trace, rank=rank, slab_ptrs=peers.next() if peers is not None else None, pull=pull)
     return drive_collectives(gen, world, group)
 
 
@@ -206,29 +235,48 @@ class PeerSlabs:
         self.device = device
         _, _, _, cap_bytes = dist_sizes(n, k, self.world, config)
         self.own, self.opened, self.ptrs = [], [], []
-        handles = []
-        for _ in range(2):
-            p, h = C.c_void_p(), (C.c_uint8 * 64)()
-            check(lib().adpb200_ipc_alloc(device, cap_bytes, C.byref(p), h))
-            self.own.append(p.value)
-            handles.append(bytes(h))
-        allh = [None] * self.world
-        if self.world > 1:
-            dist.all_gather_object(allh, handles, group=group)
-        else:
-            allh = [handles]
-        for b in range(2):
-            row = []
-            for r in range(self.world):
-                if r == self.rank:
-                    row.append(self.own[b])
-                    continue
-                p = C.c_void_p()
-                check(lib().adpb200_ipc_open(device, (C.c_uint8 * 64).from_buffer_copy(allh[r][b]), C.byref(p)))
-                self.opened.append(p.value)
-                row.append(p.value)
-            self.ptrs.append(row)
+        self.group = group
+        # every step is agreed on by all ranks, so a failure on one rank raises on all
+        # of them (no rank is left waiting in a collective the others never enter)
+        handles, err = [], None
+        try:
+            for _ in range(2):
+                p, h = C.c_void_p(), (C.c_uint8 * 64)()
+                check(lib().adpb200_ipc_alloc(device, cap_bytes, C.byref(p), h))
+                self.own.append(p.value)
+                handles.append(bytes(h))
+        except Exception as e:  # noqa: BLE001 — reported on every rank below
+            err = f"rank {self.rank}: {e}"
+        allh = self._gather(None if err else handles, err)
+        try:
+            for b in range(2):
+                row = []
+                for r in range(self.world):
+                    if r == self.rank:
+                        row.append(self.own[b])
+                        continue
+                    p = C.c_void_p()
+                    check(lib().adpb200_ipc_open(device, (C.c_uint8 * 64).from_buffer_copy(allh[r][b]),
+                                                 C.byref(p)))
+                    self.opened.append(p.value)
+                    row.append(p.value)
+                self.ptrs.append(row)
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {self.rank}: {e}"
+        self._gather(err is None, err)
         self.calls = 0
+
+    def _gather(self, item, err):
+        """all_gather_object of `item`; raises on every rank if any rank reported an error."""
+        got = [(item, err)]
+        if self.world > 1:
+            got = [None] * self.world
+            dist.all_gather_object(got, (item, err), group=self.group)
+        errs = [e for _, e in got if e]
+        if errs:
+            self.close()
+            raise RuntimeError("PeerSlabs: " + "; ".join(errs))
+        return [x for x, _ in got]
 
     def next(self):
         p = self.ptrs[self.calls % 2]
@@ -237,9 +285,9 @@ class PeerSlabs:
 
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
-        for p in self.opened:
+        for p in getattr(self, "opened", []):
             lib().adpb200_ipc_close(C.c_void_p(p))
-        for p in self.own:
+        for p in getattr(self, "own", []):
             lib().adpb200_ipc_free(C.c_void_p(p))
         self.opened, self.own, self.ptrs = [], [], []
 

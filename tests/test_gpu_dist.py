@@ -44,7 +44,7 @@ def run_virtual(gens):
 
 
 def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=None, lo=-1.0, seed=3,
-              overlap=True, zero_row=None, fused=False, mutate=None):
+              overlap=True, zero_row=None, fused=False, mutate=None, pull=False):
     from paper_2511_13778_b200 import Handle
     from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, rows_of
 
@@ -85,7 +85,7 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
         Cb = Ct[:, r0:r1].contiguous()
         blocks.append(Cb)
         gens.append(dgemm_dist_steps(world, transa, m, mr, n, k, alpha, Ab, lda_r, Bs, beta, Cb, max(mr, 1), cfg,
-                                     Handle(0), rank=r, overlap=overlap, slab_ptrs=slab_ptrs))
+                                     Handle(0), rank=r, overlap=overlap, slab_ptrs=slab_ptrs, pull=pull))
     res = run_virtual(gens)
     torch.cuda.synchronize()
     assembled = torch.cat(blocks, dim=1)
@@ -186,11 +186,12 @@ def test_dist_fused_peer_gemm(gpu, world, m, n, k, cfgname):
     cfg = {"full": gpu.AdpConfig(min_dim=8), "target": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET),
            "certified": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET, esc_method="certified"),
            "u12": gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET)}[cfgname]
-    got, ref, res = dist_case(gpu, world, m, n, k, cfg, alpha=-0.5, beta=1.25, fused=True,
-                              lo=1.0 if cfgname == "u12" else -1.0)
-    assert all(r == res[0] for r in res)
-    assert res[0][0] == 0
-    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
+    for pull in (False, True):  # in place / pulled rank by rank into local copies
+        got, ref, res = dist_case(gpu, world, m, n, k, cfg, alpha=-0.5, beta=1.25, fused=True, pull=pull,
+                                  lo=1.0 if cfgname == "u12" else -1.0)
+        assert all(r == res[0] for r in res)
+        assert res[0][0] == 0
+        assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
     # NaN in one slab: the fused path is not taken (native fallback gathers FP64 B)
     got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 3), fused=True)
     assert all(r[0] == 1 for r in res)

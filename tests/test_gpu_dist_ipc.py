@@ -26,7 +26,7 @@ def _operands():
     return A, B
 
 
-def _worker(rank, world, port, esc, out_dir):
+def _worker(rank, world, port, esc, out_dir, pull):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -45,7 +45,7 @@ def _worker(rank, world, port, esc, out_dir):
     peers = PeerSlabs(N, K, cfg)
     outs = []
     for _ in range(3):  # both buffers of the double buffer, then the first again
-        res = dgemm_dist("N", M, r1 - r0, N, K, 1.0, Ab, r1 - r0, Bs, 0.0, Cb, r1 - r0, cfg, peers=peers)
+        res = dgemm_dist("N", M, r1 - r0, N, K, 1.0, Ab, r1 - r0, Bs, 0.0, Cb, r1 - r0, cfg, peers=peers, pull=pull)
         torch.cuda.synchronize()
         outs.append(Cb.cpu().clone())
     torch.distributed.barrier()
@@ -55,13 +55,13 @@ def _worker(rank, world, port, esc, out_dir):
     torch.distributed.destroy_process_group()
 
 
-@pytest.mark.parametrize("esc", ["coarsened", "certified"])
-def test_fused_phase7_over_cuda_ipc(gpu, tmp_path, esc):
+@pytest.mark.parametrize("esc,pull", [("coarsened", False), ("certified", False), ("coarsened", True)])
+def test_fused_phase7_over_cuda_ipc(gpu, tmp_path, esc, pull):
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     world = 2
-    mp.start_processes(_worker, args=(world, port, esc, str(tmp_path)), nprocs=world, start_method="spawn")
+    mp.start_processes(_worker, args=(world, port, esc, str(tmp_path), pull), nprocs=world, start_method="spawn")
     A, B = _operands()
     ref = torch.zeros((N, M), dtype=torch.float64, device="cuda")
     gpu.dgemm("N", "N", M, N, K, 1.0, A.cuda(), M, B.cuda(), K, 0.0, ref, M,
