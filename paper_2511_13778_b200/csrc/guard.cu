@@ -126,15 +126,24 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmax_out,
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit, int transposed, int64_t tstride) {
+                                                         int exc_bit, int transposed, int64_t tstride, int groups) {
+    // 256 / groups adjacent lines x `groups` position groups per CTA: a warp loads a
+    // 256-byte coalesced row across 32 lines, and a block's positions are split over
+    // the groups (combined through shared memory) when the matrix is too small to
+    // fill the SMs with one thread per (line, block)
+    __shared__ int smax[8][256], smin[8][256];
     int nan = 0, inf = 0, negz = 0;
-    const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int width = 256 / groups;
+    const int li = threadIdx.x % width, grp = threadIdx.x / width;
+    const int64_t line = int64_t(blockIdx.x) * width + li;
+    const int64_t per = (block_len + groups - 1) / groups;
     for (int64_t blk = blockIdx.y; blk < blocks; blk += gridDim.y) {
+        int bmax = kNegSentinel, bmin = -kNegSentinel;
         if (line < v.lines) {
-            const int64_t lo = blk * block_len;
-            const int64_t hi = lo + block_len < v.len ? lo + block_len : v.len;
+            const int64_t b0 = blk * block_len, b1 = b0 + block_len < v.len ? b0 + block_len : v.len;
+            const int64_t lo = b0 + grp * per;
+            const int64_t hi = lo + per < b1 ? lo + per : b1;
             const double* p = v.ptr + line;
-            int bmax = kNegSentinel, bmin = -kNegSentinel;
             int64_t pos = lo;
             for (; pos + 3 < hi; pos += 4) {
                 uint64_t bb[4];
@@ -160,11 +169,23 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                     bmin = min(bmin, e);
                 }
             }
-            bool any = bmax != kNegSentinel;
+        }
+        if (groups > 1) {
+            smax[grp][li] = bmax;
+            smin[grp][li] = bmin;
+            __syncthreads();
+        }
+        if (grp == 0 && line < v.lines) {
+            for (int g = 1; g < groups; ++g) {
+                bmax = max(bmax, smax[g][li]);
+                bmin = min(bmin, smin[g][li]);
+            }
+            const bool any = bmax != kNegSentinel;
             const int64_t o = transposed ? blk * tstride + line : line * blocks + blk;
             bmax_out[o] = any ? bmax : kNegSentinel;
             bmin_out[o] = any ? bmin : kNegSentinel;
         }
+        if (groups > 1) __syncthreads();
     }
     flush_counts(nan, inf, negz, counts, exc_flag, exc_bit);
 }
@@ -439,9 +460,13 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
             stats_rows_kernel<<<grid, 256, 0, st>>>(w, block_len, blocks, bmax, bmin, counts, exc_flag,
                                                     exc_bit, transposed, tstride);
         } else {
-            dim3 grid((unsigned)((v.lines + 255) / 256), (unsigned)(blocks < 65535 ? blocks : 65535));
+            // position groups per (line, block): enough threads to fill the SMs (one group at 8192^2)
+            int groups = 1;
+            while (groups < 8 && v.lines * blocks * groups < int64_t(num_sms()) * 1024) groups *= 2;
+            const int width = 256 / groups;
+            dim3 grid((unsigned)((v.lines + width - 1) / width), (unsigned)(blocks < 65535 ? blocks : 65535));
             stats_cols_kernel<<<grid, 256, 0, st>>>(v, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit, transposed, tstride);
+                                                    exc_bit, transposed, tstride, groups);
         }
         ++*nlaunch;
     }
