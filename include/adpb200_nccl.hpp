@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -33,6 +34,7 @@ inline int nc(ncclResult_t r) { return r == ncclSuccess ? ADPB200_OK : ADPB200_E
 // shared once per communicator through CUDA IPC handles all-gathered over NCCL.
 struct PeerSlabs {
     int world = 0, rank = 0, device = 0, calls = 0;
+    bool pull = false;           // copy engines pull each peer's record under the GEMM (phase 7 per rank)
     void* own[2] = {nullptr, nullptr};
     std::vector<void*> ptrs[2];  // entry r: rank r's buffer in this process
 };
@@ -122,7 +124,34 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
         // every rank's slab is sliced (the host sync above) once this barrier passes
         rc = nc(ncclAllReduce(xchg, xchg, 1, ncclInt32, ncclMax, comm, st));
         if (!rc) rc = cu(cudaStreamSynchronize(st));
-        if (!rc) rc = phase(7, pp->data(), nsl);
+        if (!rc && !peers->pull) rc = phase(7, pp->data(), nsl);
+        if (!rc && peers->pull) {
+            // own columns first, then rank by rank: the copy engines pull rank r's record
+            // into local memory on a side stream while the GEMM of the previous rank runs
+            const int64_t rec = hdr + int64_t(nsl) * plane_bytes;
+            std::vector<cudaEvent_t> ready(world, nullptr);
+            rc = cu(cudaMallocAsync(&gathered, size_t(rec) * world, st));
+            if (!rc) rc = cu(cudaStreamCreateWithFlags(&comm_st, cudaStreamNonBlocking));
+            if (!rc) rc = cu(cudaEventCreateWithFlags(&ev_slab, cudaEventDisableTiming));
+            if (!rc) rc = cu(cudaEventRecord(ev_slab, st));
+            if (!rc) rc = cu(cudaStreamWaitEvent(comm_st, ev_slab, 0));
+            for (int j = 1; j < world && !rc; ++j) {
+                const int r = (rank + j) % world;
+                rc = adpb200_copy_async(gathered + int64_t(r) * rec, (*pp)[r], rec, comm_st);
+                if (!rc) rc = cu(cudaEventCreateWithFlags(&ready[r], cudaEventDisableTiming));
+                if (!rc) rc = cu(cudaEventRecord(ready[r], comm_st));
+            }
+            std::vector<const void*> one(world, nullptr);
+            for (int j = 0; j < world && !rc; ++j) {
+                const int r = (rank + j) % world;
+                std::fill(one.begin(), one.end(), nullptr);
+                one[r] = r == rank ? (*pp)[r] : static_cast<const void*>(gathered + int64_t(r) * rec);
+                if (r != rank) rc = cu(cudaStreamWaitEvent(st, ready[r], 0));
+                if (!rc) rc = phase(7, one.data(), nsl);
+            }
+            for (cudaEvent_t e : ready)
+                if (e) cudaEventDestroy(e);
+        }
     } else if (!rc && nsl > 0) {
         // B planes all-gathered on a second stream while this rank's own columns compute
         const int64_t rec = hdr + int64_t(nsl) * plane_bytes;

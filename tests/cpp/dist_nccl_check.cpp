@@ -46,8 +46,9 @@ int main() {
         return 2;
     }
     const std::vector<double> B0 = B;
-    for (int run = 0; run < 4; ++run) {
-        const int poison = run & 1, fused = run >> 1;
+    for (int run = 0; run < 6; ++run) {
+        const int poison = run & 1, fused = run >> 1;  // 0: all-gather, 1: in place, 2: pulled
+        peers.pull = fused == 2;
         B = B0;
         if (poison) B[123] = std::nan("");
         cudaMemcpy(dA, A.data(), A.size() * 8, cudaMemcpyHostToDevice);
@@ -73,8 +74,8 @@ int main() {
             const bool both_nan = c1[i] != c1[i] && c2[i] != c2[i];
             if (x != y && !both_nan) ++bad;
         }
-        std::printf("%s%s: %d of %zu differ\n", fused ? "fused " : "", poison ? "fallback" : "emulated", bad,
-                    c1.size());
+        std::printf("%s%s: %d of %zu differ\n", fused == 2 ? "pulled " : (fused ? "fused " : ""),
+                    poison ? "fallback" : "emulated", bad, c1.size());
         bad_total += bad;
     }
     adpb200::peer_slabs_destroy(peers);
