@@ -210,12 +210,31 @@ __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
 // ---- lines contiguous (ps == 1): a thread slices 8 consecutive positions ----------
 template <int S, bool kVec>
 __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t groups, int64_t span) {
-    const int64_t tasks = a.v.lines * groups;
+    // A warp covers 4 lines x 64 positions (lane = 8 x line + group): per plane it
+    // stores two full 128-byte rows of the blocked layout (4 adjacent line slots x
+    // 32 B) and reads 4 runs of 512 B. Fewer than 4 lines: one line per warp.
+    const bool quad = a.v.lines >= 4;
+    const int64_t gw = (groups + 7) / 8;
+    const int64_t tasks = quad ? (a.v.lines + 3) / 4 * gw * 32 : a.v.lines * groups;
+    auto decode = [&](int64_t task, int64_t& line, int64_t& g) {
+        if (quad) {
+            const int64_t wt = task >> 5;
+            const int lane = int(task & 31);
+            line = (wt / gw) * 4 + (lane >> 3);
+            g = (wt % gw) * 8 + (lane & 7);
+            return line < a.v.lines && g < groups;
+        }
+        line = task / groups;
+        g = task - line * groups;
+        return true;
+    };
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     // the next task's 64 bytes are requested before this task is sliced and
     // stored: two loads in flight per thread keep HBM busier
     auto load = [&](int64_t task, uint64_t (&bits)[8]) {
-        const int64_t line = task / groups, p0 = (task - line * groups) * 8;
+        int64_t line, g;
+        if (!decode(task, line, g)) return;
+        const int64_t p0 = g * 8;
         const double* lp = a.v.ptr + line * a.v.ls;
         if (kVec && p0 + 8 <= a.v.len) {
 #pragma unroll
@@ -236,7 +255,12 @@ __device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t g
     for (; task < tasks; task += stride) {
         uint64_t nxt[8];
         if (task + stride < tasks) load(task + stride, nxt);
-        const int64_t line = task / groups, g = task - line * groups;
+        int64_t line, g;
+        if (!decode(task, line, g)) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+            continue;
+        }
         const int lm = a.line_max[line];
         const int E = lm == kNegSentinel ? 0 : lm + 2;
         if (g == 0 && a.scale) a.scale[line] = E;
