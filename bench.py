@@ -148,6 +148,18 @@ def reference_arm(args):
     # the reference's own generator (gen_uniform_rect, xoshiro256++), U(1,2), seeds 1 and 2
     a = orc.gen_uniform_rect(rs, k, 1, 1.0, 2.0)
     b = orc.gen_uniform_rect(k, cs, 2, 1.0, 2.0)
+    # keep the whole --steps K --warmup W run within ~2.5 minutes: one probe call sizes
+    # the column count of the sample (multiples of 256, at least 256)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        orc.time_call(1, a, b)
+    else:
+        orc.adp_gemm(a, b)
+    probe = time.perf_counter() - t0
+    budget = 150.0 / max(1, args.warmup + args.steps)
+    if probe > budget:
+        cs = max(256, int(cs * budget / probe) // 256 * 256)
+        b = np.ascontiguousarray(b[:, :cs])
     times = []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
