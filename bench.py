@@ -69,6 +69,18 @@ def peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def cpu_model() -> str:
+    """The host CPU model (the CPU baseline's hardware, like `lscpu`)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ---------------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
@@ -179,7 +191,7 @@ def reference_arm(args):
         "dtype": "f64", "data": "synthetic U(1,2): the reference's gen_uniform_rect (xoshiro256++) seeds 1, 2",
         "config": {"workload": f"reference adp_gemm (CPU, OpenMP) on a {rs}x{cs}x{k} block of the "
                                f"{args.size}^3 ADP DGEMM", "sample_m": rs, "sample_n": cs, "k": k},
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "cpu": cpu_model(), "kind": kind,
                          "sample": f"{rs}x{cs}x{k} block of C per step"},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -202,7 +214,7 @@ def cpu_baseline(A_host_rows, B_host, k):
         orc.adp_gemm(a, b)
         dt = time.perf_counter() - t0
     m, n = a.shape[0], b.shape[1]
-    return {"value": 2.0 * m * n * k / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+    return {"value": 2.0 * m * n * k / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "cpu": cpu_model(), "kind": kind,
             "sample": f"reference adp_gemm on a {m}x{n}x{k} block of the same operands ({dt:.1f} s)"}
 
 
