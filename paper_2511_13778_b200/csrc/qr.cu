@@ -65,137 +65,146 @@ __device__ __forceinline__ double seq_dot(double init, const double* __restrict_
     return acc;
 }
 
-// Panel factorisation of f[p0:m, p0:p0+pw] (row-major f, leading dimension ld).
-// P: column-major scratch (rows x pw). v: the current reflector column (shared
-// memory when it fits, else global scratch). Outputs: the panel written back to
-// f, y (rows x pw) and yT (pw x rows) row-major, t and tT (pw x pw) row-major.
-__global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict__ f, int64_t ld, int64_t m, int64_t p0,
-                                                              int pw, double* __restrict__ P, double* __restrict__ y,
-                                                              double* __restrict__ yT, double* __restrict__ t,
-                                                              double* __restrict__ tT, double* __restrict__ vglob) {
-    extern __shared__ double vsh[];
-    const int64_t rows = m - p0;
-    double* v = vglob ? vglob : vsh;
-    double* q2 = v + rows;  // (v[r] / amax)^2, computed in parallel, summed in order by one thread
-    const int tid = threadIdx.x, nth = blockDim.x;
-    __shared__ double tau_s[1024];
-    __shared__ double z_s[1024];
-    __shared__ double red_s[32];
-    __shared__ double v0_s, beta_s, x0_s, tail_s;
-    __shared__ int mode_s;
-    for (int64_t e = tid; e < rows * pw; e += nth) {
+// ---- panel factorisation, one column step at a time across CTAs --------------------
+// The panel f[p0:m, p0:p0+pw] is copied into P (column-major rows x pw). Column j's
+// reflector is made by one CTA (its two sequential sums on two threads); then every
+// later column of the panel is updated by its own CTA, which stages the reflector and
+// the column in shared memory so that its one sequential dot runs at shared-memory
+// latency. Every sum keeps the reference's order and rounding (make_reflector
+// qr.cpp:26-47, apply_reflector :51-60); the parallelism is only across columns and
+// across the element-independent divisions / updates.
+
+__global__ void panel_load_kernel(const double* __restrict__ f, int64_t ld, int64_t p0, int64_t rows, int pw,
+                                  double* __restrict__ P) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pw; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / pw, j = e - r * pw;
         P[j * rows + r] = f[(p0 + r) * ld + p0 + j];
     }
+}
+
+// make_reflector (qr.cpp:26-47) for panel column j; tau[j] to global memory
+__global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __restrict__ P, int64_t rows, int j,
+                                                                  double* __restrict__ tau,
+                                                                  double* __restrict__ vglob) {
+    extern __shared__ double vsh[];
+    double* v = vglob ? vglob : vsh;
+    double* q2 = v + rows;  // (v[r] / amax)^2, computed in parallel, summed in order by one thread
+    const int tid = threadIdx.x, nth = blockDim.x;
+    __shared__ double red_s[32];
+    __shared__ double v0_s, beta_s, x0_s, tail_s;
+    __shared__ int mode_s;
+    double* col = P + int64_t(j) * rows;
+    for (int64_t r = j + tid; r < rows; r += nth) v[r] = col[r];
     __syncthreads();
-    for (int j = 0; j < pw; ++j) {
-        double* col = P + int64_t(j) * rows;
-        for (int64_t r = j + tid; r < rows; r += nth) v[r] = col[r];
-        __syncthreads();
-        // ---- make_reflector (qr.cpp:26-47)
-        // column_norm's max (qr.cpp:15): exact and order-free, reduced in parallel
-        double amax = 0.0;
-        for (int64_t r = j + tid; r < rows; r += nth) {
-            const double a = fabs(v[r]);
-            amax = amax < a ? a : amax;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double b = __shfl_xor_sync(0xffffffffu, amax, o);
-            amax = amax < b ? b : amax;
-        }
-        if ((tid & 31) == 0) red_s[tid >> 5] = amax;
-        __syncthreads();
-        amax = red_s[0];
-        for (int w = 1; w < (nth + 31) / 32; ++w) amax = amax < red_s[w] ? red_s[w] : amax;
-        // the squares (f/amax)^2 of column_norm (qr.cpp:17-19) are element-independent:
-        // divide in parallel (a division costs ~100 cycles on one thread), sum in order below
-        if (amax != 0.0)
-            for (int64_t r = j + tid; r < rows; r += nth) {
-                const double q = __ddiv_rn(v[r], amax);
-                q2[r] = __dmul_rn(q, q);
-            }
-        __syncthreads();
-        // the two sequential sums run concurrently on two warps, each in reference order
-        if (tid == 0) tail_s = seq_dot(0.0, v, v, j + 1, rows);  // tail_ss (qr.cpp:29)
-        if (tid == 32 % nth) {
-            double ss = 0.0;
-            if (amax != 0.0) {
-                int64_t r = j;
-                for (; r + 16 <= rows; r += 16) {
-                    double b[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) b[u] = q2[r + u];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) ss = __dadd_rn(ss, b[u]);
-                }
-                for (; r < rows; ++r) ss = __dadd_rn(ss, q2[r]);
-            }
-            beta_s = amax != 0.0 ? __dmul_rn(amax, __dsqrt_rn(ss)) : 0.0;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            const double x0 = v[j], tail = tail_s;
-            if (tail == 0.0) {
-                mode_s = 0;
-                if (x0 >= 0.0) {
-                    tau_s[j] = 0.0;
-                } else {
-                    col[j] = -x0;
-                    v[j] = -x0;
-                    tau_s[j] = 2.0;
-                }
-            } else {
-                const double beta = beta_s;
-                v0_s = x0 > 0.0 ? __ddiv_rn(-tail, __dadd_rn(x0, beta)) : __dsub_rn(x0, beta);
-                x0_s = x0;
-                mode_s = 1;
-            }
-        }
-        __syncthreads();
-        if (mode_s == 1) {
-            const double v0 = v0_s;
-            for (int64_t r = j + 1 + tid; r < rows; r += nth) {
-                const double q = __ddiv_rn(v[r], v0);
-                v[r] = q;
-                col[r] = q;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                col[j] = beta_s;
-                v[j] = beta_s;
-                tau_s[j] = __ddiv_rn(__dsub_rn(beta_s, x0_s), beta_s);
-            }
-        }
-        __syncthreads();
-        // ---- apply_reflector (qr.cpp:51-60) to the panel's later columns, one thread each
-        const double tau = tau_s[j];
-        if (tau != 0.0) {
-            for (int cc = j + 1 + tid; cc < pw; cc += nth) {
-                double* dst = P + int64_t(cc) * rows;
-                const double dot = seq_dot(dst[j], v, dst, j + 1, rows);
-                const double w = __dmul_rn(tau, dot);
-                dst[j] = __dsub_rn(dst[j], w);
-                // the update is element-independent: load a chunk, then store it (the
-                // stores would otherwise serialise every load behind them: v may alias)
-                int64_t r = j + 1;
-                for (; r + 16 <= rows; r += 16) {
-                    double d[16], vv[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        d[u] = dst[r + u];
-                        vv[u] = v[r + u];
-                    }
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) dst[r + u] = __dsub_rn(d[u], __dmul_rn(w, vv[u]));
-                }
-                for (; r < rows; ++r) dst[r] = __dsub_rn(dst[r], __dmul_rn(w, v[r]));
-            }
-        }
-        __syncthreads();
+    // column_norm's max (qr.cpp:15): exact and order-free, reduced in parallel
+    double amax = 0.0;
+    for (int64_t r = j + tid; r < rows; r += nth) {
+        const double a = fabs(v[r]);
+        amax = amax < a ? a : amax;
     }
-    // write the panel back; build_y (qr.cpp:64-71)
-    for (int64_t e = tid; e < rows * pw; e += nth) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double b = __shfl_xor_sync(0xffffffffu, amax, o);
+        amax = amax < b ? b : amax;
+    }
+    if ((tid & 31) == 0) red_s[tid >> 5] = amax;
+    __syncthreads();
+    amax = red_s[0];
+    for (int w = 1; w < (nth + 31) / 32; ++w) amax = amax < red_s[w] ? red_s[w] : amax;
+    // the squares (f/amax)^2 of column_norm (qr.cpp:17-19) are element-independent:
+    // divide in parallel (a division costs ~100 cycles on one thread), sum in order below
+    if (amax != 0.0)
+        for (int64_t r = j + tid; r < rows; r += nth) {
+            const double q = __ddiv_rn(v[r], amax);
+            q2[r] = __dmul_rn(q, q);
+        }
+    __syncthreads();
+    // the two sequential sums run concurrently on two warps, each in reference order
+    if (tid == 0) tail_s = seq_dot(0.0, v, v, j + 1, rows);  // tail_ss (qr.cpp:29)
+    if (tid == 32 % nth) {
+        double ss = 0.0;
+        if (amax != 0.0) {
+            int64_t r = j;
+            for (; r + 16 <= rows; r += 16) {
+                double b[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) b[u] = q2[r + u];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) ss = __dadd_rn(ss, b[u]);
+            }
+            for (; r < rows; ++r) ss = __dadd_rn(ss, q2[r]);
+        }
+        beta_s = amax != 0.0 ? __dmul_rn(amax, __dsqrt_rn(ss)) : 0.0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const double x0 = v[j], tail = tail_s;
+        if (tail == 0.0) {
+            mode_s = 0;
+            if (x0 >= 0.0) {
+                tau[j] = 0.0;
+            } else {
+                col[j] = -x0;
+                tau[j] = 2.0;
+            }
+        } else {
+            const double beta = beta_s;
+            v0_s = x0 > 0.0 ? __ddiv_rn(-tail, __dadd_rn(x0, beta)) : __dsub_rn(x0, beta);
+            x0_s = x0;
+            mode_s = 1;
+        }
+    }
+    __syncthreads();
+    if (mode_s == 1) {
+        const double v0 = v0_s;
+        for (int64_t r = j + 1 + tid; r < rows; r += nth) col[r] = __ddiv_rn(v[r], v0);
+        if (tid == 0) {
+            col[j] = beta_s;
+            tau[j] = __ddiv_rn(__dsub_rn(beta_s, x0_s), beta_s);
+        }
+    }
+}
+
+// apply_reflector (qr.cpp:51-60) of column j to panel column j + 1 + blockIdx.x
+__global__ void __launch_bounds__(kPanelThreads) apply_kernel(double* __restrict__ P, int64_t rows, int j,
+                                                              const double* __restrict__ tau, int staged) {
+    const double tj = tau[j];
+    if (tj == 0.0) return;
+    extern __shared__ double sh[];
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const double* vcol = P + int64_t(j) * rows;
+    double* dst = P + int64_t(j + 1 + blockIdx.x) * rows;
+    const double* sv = vcol;
+    const double* sd = dst;
+    if (staged) {
+        double* v = sh;
+        double* d = sh + rows;
+        for (int64_t r = j + tid; r < rows; r += nth) {
+            v[r] = vcol[r];
+            d[r] = dst[r];
+        }
+        __syncthreads();
+        sv = v;
+        sd = d;
+    }
+    __shared__ double w_s, head_s;
+    if (tid == 0) {
+        const double dot = seq_dot(sd[j], sv, sd, j + 1, rows);
+        const double w = __dmul_rn(tj, dot);
+        w_s = w;
+        head_s = __dsub_rn(sd[j], w);
+    }
+    __syncthreads();
+    const double w = w_s;
+    // element-independent update; with staging the new values go straight to P
+    for (int64_t r = j + 1 + tid; r < rows; r += nth) dst[r] = __dsub_rn(sd[r], __dmul_rn(w, sv[r]));
+    if (tid == 0) dst[j] = head_s;
+}
+
+// write the panel back to f; build_y (qr.cpp:64-71)
+__global__ void panel_store_kernel(const double* __restrict__ P, double* __restrict__ f, int64_t ld, int64_t p0,
+                                   int64_t rows, int pw, double* __restrict__ y, double* __restrict__ yT) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pw; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / pw, j = e - r * pw;
         const double val = P[j * rows + r];
         f[(p0 + r) * ld + p0 + j] = val;
@@ -203,31 +212,47 @@ __global__ void __launch_bounds__(kPanelThreads) panel_kernel(double* __restrict
         y[r * pw + j] = yv;
         yT[j * rows + r] = yv;
     }
-    // build_t (qr.cpp:75-94), T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) (Y^T y_j)
+}
+
+// build_t's z (qr.cpp:79-85): z(i, j) = sum_{r >= j} y(r, i) y(r, j) for i < j, y(j, j) = 1
+// first, then the tails; one CTA per j (column j staged in shared memory when it fits)
+__global__ void __launch_bounds__(kPanelThreads) build_z_kernel(const double* __restrict__ P, int64_t rows, int pw,
+                                                                double* __restrict__ z, int staged) {
+    extern __shared__ double sh[];
+    const int j = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+    if (j == 0) return;
+    const double* cj = P + int64_t(j) * rows;
+    if (staged) {
+        for (int64_t r = j + tid; r < rows; r += nth) sh[r] = cj[r];
+        __syncthreads();
+        cj = sh;
+    }
+    for (int i = tid; i < j; i += nth) {
+        const double* ci = P + int64_t(i) * rows;
+        const double first = __dmul_rn(ci[j], 1.0);
+        z[int64_t(i) * pw + j] = seq_dot(__dadd_rn(0.0, first), ci, cj, j + 1, rows);
+    }
+}
+
+// build_t (qr.cpp:75-94): T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) z(:, j); and T^T
+__global__ void __launch_bounds__(kPanelThreads) build_t_kernel(const double* __restrict__ tau,
+                                                                const double* __restrict__ z, int pw,
+                                                                double* __restrict__ t, double* __restrict__ tT) {
+    const int tid = threadIdx.x, nth = blockDim.x;
     for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) t[e] = 0.0;
     __syncthreads();
     for (int j = 0; j < pw; ++j) {
-        if (tid == 0) t[j * pw + j] = tau_s[j];
-        if (j > 0) {
-            // z_i = sum_{r >= j} y(r, i) y(r, j), i < j: y(j, j) = 1 first, then the tails
-            const double* cj = P + int64_t(j) * rows;
-            for (int i = tid; i < j; i += nth) {
-                const double* ci = P + int64_t(i) * rows;
-                const double first = __dmul_rn(ci[j], 1.0);
-                z_s[i] = seq_dot(__dadd_rn(0.0, first), ci, cj, j + 1, rows);
-            }
-            __syncthreads();
-            for (int i = tid; i < j; i += nth) {
-                double dot = 0.0;
-                for (int l = i; l < j; ++l) dot = __dadd_rn(dot, __dmul_rn(t[i * pw + l], z_s[l]));
-                t[i * pw + j] = __dmul_rn(-tau_s[j], dot);
-            }
+        if (tid == 0) t[j * pw + j] = tau[j];
+        for (int i = tid; i < j; i += nth) {
+            double dot = 0.0;
+            for (int l = i; l < j; ++l) dot = __dadd_rn(dot, __dmul_rn(t[i * pw + l], z[int64_t(l) * pw + j]));
+            t[i * pw + j] = __dmul_rn(-tau[j], dot);
         }
         __syncthreads();
     }
     for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) {
-        const int64_t i = e / pw, j = e - i * pw;
-        tT[j * pw + i] = t[e];
+        const int64_t i = e / pw, jj = e - i * pw;
+        tT[jj * pw + i] = t[e];
     }
 }
 
@@ -340,14 +365,19 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
     double* w2 = bw2.alloc(size_t(pwmax) * (n - pwmax));
     double* up = bup.alloc(size_t(m) * (n - pwmax));
     if (!P || !y || !yT || !t || !tT || !as || !w1 || !w2 || !up) return 2;
-    DevBuf bvg(st);
+    DevBuf bvg(st), btau(st), bz(st);
     double* vg = nullptr;
     if (2 * size_t(m) * sizeof(double) > kPanelSmemMax) {
         vg = bvg.alloc(2 * size_t(m));
         if (!vg) return 2;
     }
+    double* tau = btau.alloc(size_t(pwmax));
+    double* z = bz.alloc(size_t(pwmax) * pwmax);
+    if (!tau || !z) return 2;
     static bool attr = [] {
-        cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(reflector_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(build_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
         return true;
     }();
     (void)attr;
@@ -356,11 +386,24 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         const int pw = (int)std::min(panel, n - p0);
         const int64_t rows = m - p0, nt = n - p0 - pw;
         const int threads = kPanelThreads;
-        // the reflector column in shared memory when it fits (sequential sums at smem latency)
+        // the reflector column (and, for the updates, the target column) in shared
+        // memory when it fits: sequential sums at shared-memory latency
         const size_t vbytes = 2 * size_t(rows) * sizeof(double);
         const bool vsmem = vbytes <= kPanelSmemMax;
-        panel_kernel<<<1, threads, vsmem ? vbytes : 0, st>>>(f, n, m, p0, pw, P, y, yT, t, tT, vsmem ? nullptr : vg);
+        panel_load_kernel<<<grid_for(rows * pw), 256, 0, st>>>(f, n, p0, rows, pw, P);
         ++*nl;
+        for (int j = 0; j < pw; ++j) {
+            reflector_kernel<<<1, threads, vsmem ? vbytes : 0, st>>>(P, rows, j, tau, vsmem ? nullptr : vg);
+            ++*nl;
+            if (j + 1 < pw) {
+                apply_kernel<<<unsigned(pw - j - 1), threads, vsmem ? vbytes : 0, st>>>(P, rows, j, tau, vsmem ? 1 : 0);
+                ++*nl;
+            }
+        }
+        panel_store_kernel<<<grid_for(rows * pw), 256, 0, st>>>(P, f, n, p0, rows, pw, y, yT);
+        build_z_kernel<<<unsigned(pw), threads, vsmem ? vbytes / 2 : 0, st>>>(P, rows, pw, z, vsmem ? 1 : 0);
+        build_t_kernel<<<1, threads, 0, st>>>(tau, z, pw, t, tT);
+        *nl += 3;
         copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
         ++*nl;
         if (nt > 0) {
