@@ -126,3 +126,32 @@ def test_certified_bracket_at_2048(gpu):
         _, tx = gpu.adp_gemm(A, B, config=gpu.AdpConfig(mode=gpu.AdpMode.ForceEmulate, guardrails_forced=True,
                                                         esc_method="certified"))
         assert exact <= tx.esc_bits <= tc_.esc_bits, (name, exact, tx.esc_bits, tc_.esc_bits)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T")])
+def test_certified_streamed_dgemm_host_matches_device(gpu, ta, tb):
+    """adpb200_dgemm_host (B streamed in column chunks, speculated s) with the
+    certified ESC: the same decision and bits as the device-resident dgemm, with
+    alpha / beta, across the speculation hit / miss sequence of one handle."""
+    import torch
+
+    from paper_2511_13778_b200 import Handle
+
+    h = Handle(0)
+    m, n, k = 900, 1280, 700
+    g = torch.Generator()
+    g.manual_seed(5)
+    cfg = gpu.AdpConfig(pair_limit=gpu.PAIRS_TARGET, esc_method="certified")
+    for lo, hi, beta in ((-1.0, 1.0, 0.0), (-1.0, 1.0, 0.5), (1.0, 2.0, 0.0), (-1.0, 1.0, -2.0)):
+        Ast = torch.rand((k, m) if ta == "N" else (m, k), generator=g, dtype=torch.float64) * (hi - lo) + lo
+        Bst = torch.rand((n, k) if tb == "N" else (k, n), generator=g, dtype=torch.float64) * (hi - lo) + lo
+        Ct = torch.rand((n, m), generator=g, dtype=torch.float64)
+        lda = m if ta == "N" else k
+        ldb = k if tb == "N" else n
+        A_h, B_h, C_h = Ast.pin_memory(), Bst.pin_memory(), Ct.clone().pin_memory()
+        tr = gpu.dgemm_host(ta, tb, m, n, k, -0.75, A_h, lda, B_h, ldb, beta, C_h, m, cfg, h)
+        Cd = Ct.cuda()
+        gpu.dgemm(ta, tb, m, n, k, -0.75, Ast.cuda(), lda, Bst.cuda(), ldb, beta, Cd, m, cfg, h)
+        torch.cuda.synchronize()
+        assert tr.path == "emulated" and tr.slices == 7  # U[-1,1] certified down to s0 = 7
+        assert torch.equal(C_h.view(torch.int64), Cd.cpu().view(torch.int64))
