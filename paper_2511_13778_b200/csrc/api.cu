@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "adpb200.h"
 #include "igemm.cuh"
@@ -43,7 +45,7 @@ struct adpb200_context {
     // streamed host path: H2D stream, per-chunk events, pinned plan read-back and
     // the slice count speculated for the next call (the last decided one)
     cudaStream_t h2d = nullptr;
-    cudaEvent_t h2d_ev[kMaxStreamChunks + 2] = {};
+    cudaEvent_t h2d_ev[2 * kMaxStreamChunks + 2] = {};  // B chunks, A chunks, [2k] a_ready, [2k+1] start
     Plan* host_plan = nullptr;
     int spec_s = 7;
 };
@@ -604,9 +606,19 @@ __global__ void spec_fixup_kernel(Plan* plan, const Plan* spec) {
 // run_pipeline bit for bit: the speculation only decides what runs early.
 // copy_b(c0, c1, stream) copies internal B lines [c0, c1) to the device;
 // copy_c(c0, c1) enqueues the D2H of internal C columns [c0, c1) on h->d2h.
-template <class CopyB, class CopyC>
+// Host-buffer path, streamed in two dimensions: A in row chunks and B in column
+// chunks go over PCIe interleaved (A_0, B_0, A_1, B_1, ...) on the H2D stream;
+// when a chunk lands, its statistics and slicing run and the GEMM computes the C
+// block(s) it completes — A_i x (B columns so far) or (A rows so far) x B_j — and
+// the D2H stream copies those C blocks back while the next chunks travel. The
+// slicing and GEMMs use the speculated slice count (the handle's last decision);
+// the ESC of each (A_i, B_j) block pair accumulates into the plan, and after the
+// last chunk the real decision is compared with the speculation: a hit is done, a
+// miss recomputes everything with the decided plan (bitwise the same as the
+// device path either way). a_ready: the caller's C_in transfer (beta != 0).
+template <class CopyA, class CopyB, class CopyC>
 int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* tdev, cudaStream_t st,
-                 cudaEvent_t a_ready, CopyB copy_b, CopyC copy_c, bool* streamed) {
+                 cudaEvent_t a_ready, CopyA copy_a, CopyB copy_b, CopyC copy_c, bool* streamed) {
     *streamed = false;
     if (o.mode == ADPB200_MODE_NATIVE || P.M == 0 || P.K == 0) return ADPB200_OK;
     const int cap = plane_cap(o, 0, 0);
@@ -618,6 +630,15 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     int64_t chunk = (P.N + kMaxStreamChunks - 1) / kMaxStreamChunks;
     chunk = (chunk + nb - 1) / nb * nb;
     const int nchunks = int((P.N + chunk - 1) / chunk);
+    // row chunks of A: whole 128-row m-tiles (ADPB200_STREAM_ROWS caps the count, 1 = A first)
+    static const int max_rows = [] {
+        const char* e = getenv("ADPB200_STREAM_ROWS");
+        const int v = e ? atoi(e) : kMaxStreamChunks;
+        return v < 1 ? 1 : (v > kMaxStreamChunks ? kMaxStreamChunks : v);
+    }();
+    const int64_t mtiles = (P.M + 127) / 128;
+    const int64_t rchunk = (mtiles + max_rows - 1) / max_rows * 128;
+    const int rchunks = int((P.M + rchunk - 1) / rchunk);
     *streamed = true;
 
     const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
@@ -640,38 +661,86 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     const int64_t mn = std::min(std::min(P.tm, P.tn), P.tk);
     const bool esc_expected = (o.mode == ADPB200_MODE_AUTO || (o.mode == ADPB200_MODE_EMULATE && o.guardrails_forced)) &&
                               mn >= o.min_dim;
-    // B chunks on the H2D stream, after A (a_ready) and after everything earlier on st
-    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1];
+    // transfer order: A_0, B_0, A_1, B_1, ... (the longer list finishes alone)
+    std::vector<std::pair<int, int>> order;  // (0 = A / 1 = B, chunk)
+    for (int q = 0; q < std::max(rchunks, nchunks); ++q) {
+        if (q < rchunks) order.push_back({0, q});
+        if (q < nchunks) order.push_back({1, q});
+    }
+    auto rows_of_chunk = [&](int i, int64_t& r0, int64_t& r1) {
+        r0 = i * rchunk;
+        r1 = std::min(P.M, r0 + rchunk);
+    };
+    auto cols_of_chunk = [&](int j, int64_t& c0, int64_t& c1) {
+        c0 = j * chunk;
+        c1 = std::min(P.N, c0 + chunk);
+    };
+    cudaEvent_t ev0 = h->h2d_ev[2 * kMaxStreamChunks + 1];
     rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
     if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent");
     if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->h2d, a_ready, 0), "cudaStreamWaitEvent");
-    for (int c = 0; c < nchunks && !rc; ++c) {
-        const int64_t c0 = c * chunk, c1 = std::min(P.N, c0 + chunk);
-        rc = copy_b(c0, c1, h->h2d);
-        if (!rc) rc = cuda_check(cudaEventRecord(h->h2d_ev[c], h->h2d), "cudaEventRecord(h2d)");
+    for (const auto& it : order) {
+        if (rc) break;
+        int64_t a0, a1;
+        if (it.first == 0) {
+            rows_of_chunk(it.second, a0, a1);
+            rc = copy_a(a0, a1, h->h2d);
+            if (!rc) rc = cuda_check(cudaEventRecord(h->h2d_ev[kMaxStreamChunks + it.second], h->h2d), "cudaEventRecord");
+        } else {
+            cols_of_chunk(it.second, a0, a1);
+            rc = copy_b(a0, a1, h->h2d);
+            if (!rc) rc = cuda_check(cudaEventRecord(h->h2d_ev[it.second], h->h2d), "cudaEventRecord(h2d)");
+        }
     }
     if (rc) return rc;
-    // A: stats, speculative plan, slicing
     rc = cuda_check(cudaMemsetAsync(plan, 0, sizeof(Plan), st), "cudaMemsetAsync(plan)");
     if (!rc) rc = cuda_check(cudaMemsetAsync(spec, 0, sizeof(Plan), st), "cudaMemsetAsync(spec)");
-    if (!rc) rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent(A)");
+    if (!rc) rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent(C_in)");
     if (rc) return rc;
-    launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
     launch_set_plan(spec, s_spec, o.pair_limit, P.K, st, nl);
-    launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, spec, 0, cap, st, nl);
     GemmArgs g = product_args(h, Lw, P, spec, sb);
-    for (int c = 0; c < nchunks; ++c) {
-        const int64_t c0 = c * chunk, c1 = std::min(P.N, c0 + chunk), lines = c1 - c0;
-        rc = cuda_check(cudaStreamWaitEvent(st, h->h2d_ev[c], 0), "cudaStreamWaitEvent(B chunk)");
-        if (rc) return rc;
-        const LineView bv{P.b.ptr + c0 * P.b.ls, lines, P.K, P.b.ls, P.b.ps};
-        // chunk stats: block-major records of `lines` lines at offset c0 (line maxima stay contiguous)
-        launch_stats(bv, o.esc_block_len, bmax + c0 * t, bmin + c0 * t, bline + c0, plan->counts + 3, &plan->exc, 2, 1,
-                     st, nl);
-        if (esc_expected)
-            launch_esc(amax, amin, aline, bmax + c0 * t, bmin + c0 * t, bline + c0, P.M, lines, t, plan, &plan->esc_raw,
-                       &plan->esc_ran, st, nl);
-        launch_slice(bv, bline + c0, pb + c0 * 32, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb + c0, spec, 0, cap, st, nl);
+    int64_t rows_done = 0, cols_done = 0;  // chunks arrive in order, so "so far" is a prefix
+    for (const auto& it : order) {
+        int64_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;
+        if (it.first == 0) {
+            rows_of_chunk(it.second, r0, r1);
+            rc = cuda_check(cudaStreamWaitEvent(st, h->h2d_ev[kMaxStreamChunks + it.second], 0), "wait(A chunk)");
+            if (rc) return rc;
+            const LineView av{P.a.ptr + r0 * P.a.ls, r1 - r0, P.K, P.a.ls, P.a.ps};
+            launch_stats(av, o.esc_block_len, amax + r0 * t, amin + r0 * t, aline + r0, plan->counts, &plan->exc, 1,
+                         1, st, nl);
+            launch_slice(av, aline + r0, pa + r0 * 32, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa + r0, spec, 0, cap, st,
+                         nl);
+            for (int64_t q0 = 0; esc_expected && q0 < cols_done; q0 += chunk) {
+                const int64_t q1 = std::min(cols_done, q0 + chunk);
+                launch_esc(amax + r0 * t, amin + r0 * t, aline + r0, bmax + q0 * t, bmin + q0 * t, bline + q0, r1 - r0,
+                           q1 - q0, t, plan, &plan->esc_raw, &plan->esc_ran, st, nl);
+            }
+            rows_done = r1;
+            c0 = 0;
+            c1 = cols_done;
+        } else {
+            cols_of_chunk(it.second, c0, c1);
+            rc = cuda_check(cudaStreamWaitEvent(st, h->h2d_ev[it.second], 0), "wait(B chunk)");
+            if (rc) return rc;
+            const LineView bv{P.b.ptr + c0 * P.b.ls, c1 - c0, P.K, P.b.ls, P.b.ps};
+            // chunk stats: block-major records of the chunk's lines at offset c0 (line maxima stay contiguous)
+            launch_stats(bv, o.esc_block_len, bmax + c0 * t, bmin + c0 * t, bline + c0, plan->counts + 3, &plan->exc,
+                         2, 1, st, nl);
+            launch_slice(bv, bline + c0, pb + c0 * 32, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb + c0, spec, 0, cap, st,
+                         nl);
+            for (int64_t q0 = 0; esc_expected && q0 < rows_done; q0 += rchunk) {
+                const int64_t q1 = std::min(rows_done, q0 + rchunk);
+                launch_esc(amax + q0 * t, amin + q0 * t, aline + q0, bmax + c0 * t, bmin + c0 * t, bline + c0, q1 - q0,
+                           c1 - c0, t, plan, &plan->esc_raw, &plan->esc_ran, st, nl);
+            }
+            cols_done = c1;
+            r0 = 0;
+            r1 = rows_done;
+        }
+        if (r1 <= r0 || c1 <= c0) continue;  // the other operand has not arrived yet
+        g.mt_begin = r0 / 128;
+        g.mt_end = (r1 + 127) / 128;
         g.nt_begin = c0 / nb;
         g.nt_end = (c1 + nb - 1) / nb;
         if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
@@ -679,7 +748,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
         cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
         rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
         if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
-        if (!rc) rc = copy_c(c0, c1);
+        if (!rc) rc = copy_c(r0, r1, c0, c1);
         if (rc) return rc;
     }
     // the real decision (the trace is written here), then compare with the speculation
@@ -695,6 +764,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     if (hp2.path == kPathDone) return ADPB200_OK;
     // speculation missed: recompute with the decided plan (predicated kernels)
     g.plan = plan;
+    g.mt_begin = g.mt_end = 0;
     g.nt_begin = g.nt_end = 0;
     launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, plan, 0, cap, st, nl);
     launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, 0, cap, st, nl);
@@ -705,7 +775,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
     rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
     if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
-    if (!rc) rc = copy_c(0, P.N);
+    if (!rc) rc = copy_c(0, P.M, 0, P.N);
     return rc ? rc : cuda_check(cudaGetLastError(), "kernel launch");
 }
 
@@ -1179,11 +1249,11 @@ int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, in
     double* dB = reinterpret_cast<double*>(io + ta + sa);
     double* dC = reinterpret_cast<double*>(io + ta + sa + sb);
     double* dCin = beta != 0.0 ? reinterpret_cast<double*>(io + ta + sa + sb + sc) : dC;
-    // A (and C when beta != 0) on the H2D stream, after the work already queued on st
-    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1], a_ready = h->h2d_ev[kMaxStreamChunks];
+    // C_in (beta != 0) on the H2D stream, after the work already queued on st; A and B
+    // follow in chunks (run_streamed)
+    cudaEvent_t ev0 = h->h2d_ev[2 * kMaxStreamChunks + 1], a_ready = h->h2d_ev[2 * kMaxStreamChunks];
     if ((rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord"))) return rc;
     if ((rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent"))) return rc;
-    if ((rc = h2d_block(dA, A, arows, acols, lda, h->h2d))) return rc;
     if (beta != 0.0 && (rc = h2d_block(dCin, C, m, n, ldc, h->h2d))) return rc;
     if ((rc = cuda_check(cudaEventRecord(a_ready, h->h2d), "cudaEventRecord"))) return rc;
     Problem P{};
@@ -1201,6 +1271,17 @@ int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, in
     P.tm = m;
     P.tn = n;
     P.tk = k;
+    // internal A lines [r0, r1) = rows (op N) or columns (op T) of the stored A
+    auto copy_a = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+        if (r1 <= r0 || k == 0) return int(ADPB200_OK);
+        if (is_n(transa))
+            return cuda_check(cudaMemcpy2DAsync(dA + r0, size_t(arows) * 8, A + r0, size_t(lda) * 8,
+                                                size_t(r1 - r0) * 8, size_t(acols), cudaMemcpyHostToDevice, s),
+                              "cudaMemcpy2DAsync(H2D A rows)");
+        return cuda_check(cudaMemcpy2DAsync(dA + r0 * arows, size_t(arows) * 8, A + r0 * lda, size_t(lda) * 8,
+                                            size_t(arows) * 8, size_t(r1 - r0), cudaMemcpyHostToDevice, s),
+                          "cudaMemcpy2DAsync(H2D A rows)");
+    };
     // internal B lines [c0, c1) = columns (op N) or rows (op T) of the stored B
     auto copy_b = [&](int64_t c0, int64_t c1, cudaStream_t s) {
         if (c1 <= c0) return int(ADPB200_OK);
@@ -1212,17 +1293,19 @@ int adpb200_dgemm_host(adpb200_handle h, char transa, char transb, int64_t m, in
                                             size_t(bcols), cudaMemcpyHostToDevice, s),
                           "cudaMemcpy2DAsync(H2D B chunk)");
     };
-    auto copy_c = [&](int64_t c0, int64_t c1) {
-        if (c1 <= c0 || m == 0) return int(ADPB200_OK);
-        return cuda_check(cudaMemcpy2DAsync(C + c0 * ldc, size_t(ldc) * 8, dC + c0 * m, size_t(m) * 8, size_t(m) * 8,
-                                            size_t(c1 - c0), cudaMemcpyDeviceToHost, h->d2h),
-                          "cudaMemcpy2DAsync(D2H C chunk)");
+    // C block rows [r0, r1) x columns [c0, c1)
+    auto copy_c = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+        if (c1 <= c0 || r1 <= r0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpy2DAsync(C + c0 * ldc + r0, size_t(ldc) * 8, dC + c0 * m + r0, size_t(m) * 8,
+                                            size_t(r1 - r0) * 8, size_t(c1 - c0), cudaMemcpyDeviceToHost, h->d2h),
+                          "cudaMemcpy2DAsync(D2H C block)");
     };
     bool streamed = false;
-    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_b, copy_c, &streamed);
+    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_a, copy_b, copy_c, &streamed);
     if (rc) return rc;
     if (!streamed) {
         if ((rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent"))) return rc;
+        if ((rc = h2d_block(dA, A, arows, acols, lda, st))) return rc;
         if ((rc = h2d_block(dB, B, brows, bcols, ldb, st))) return rc;
         HostOut out{C, ldc};
         rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &out);
@@ -1258,29 +1341,37 @@ int adpb200_adp_gemm_host(adpb200_handle h, int64_t m, int64_t n, int64_t k, dou
     double* dCin = beta != 0.0 ? reinterpret_cast<double*>(io + ta + sa + sb + sc) : dC;
     // internally C^T = B^T A^T: the internal A is the user's B (all of it first),
     // the internal B-lines are the user's rows of A (streamed in row chunks)
-    cudaEvent_t ev0 = h->h2d_ev[kMaxStreamChunks + 1], a_ready = h->h2d_ev[kMaxStreamChunks];
+    cudaEvent_t ev0 = h->h2d_ev[2 * kMaxStreamChunks + 1], a_ready = h->h2d_ev[2 * kMaxStreamChunks];
     if ((rc = cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord"))) return rc;
     if ((rc = cuda_check(cudaStreamWaitEvent(h->h2d, ev0, 0), "cudaStreamWaitEvent"))) return rc;
-    if ((rc = h2d_block(dB, B, n, k, n, h->h2d))) return rc;
     if (beta != 0.0 && (rc = h2d_block(dCin, c_in, n, m, n, h->h2d))) return rc;
     if ((rc = cuda_check(cudaEventRecord(a_ready, h->h2d), "cudaEventRecord"))) return rc;
     Problem P = rowmajor_problem(m, n, k, alpha, dA, dB, beta, dCin, dC);
+    // internal A lines [r0, r1) = columns [r0, r1) of the user's B (k x n row-major)
+    auto copy_a = [&](int64_t r0, int64_t r1, cudaStream_t s) {
+        if (r1 <= r0 || k == 0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpy2DAsync(dB + r0, size_t(n) * 8, B + r0, size_t(n) * 8, size_t(r1 - r0) * 8,
+                                            size_t(k), cudaMemcpyHostToDevice, s),
+                          "cudaMemcpy2DAsync(H2D B columns)");
+    };
     auto copy_b = [&](int64_t c0, int64_t c1, cudaStream_t s) {
         if (c1 <= c0 || k == 0) return int(ADPB200_OK);
         return cuda_check(cudaMemcpyAsync(dA + c0 * k, A + c0 * k, size_t(c1 - c0) * k * 8, cudaMemcpyHostToDevice, s),
                           "cudaMemcpyAsync(H2D A rows)");
     };
-    auto copy_c = [&](int64_t c0, int64_t c1) {
-        if (c1 <= c0 || n == 0) return int(ADPB200_OK);
-        return cuda_check(cudaMemcpyAsync(out + c0 * n, dC + c0 * n, size_t(c1 - c0) * n * 8, cudaMemcpyDeviceToHost,
-                                          h->d2h),
-                          "cudaMemcpyAsync(D2H C rows)");
+    // internal C block (rows [r0, r1) = user columns) x (columns [c0, c1) = user rows)
+    auto copy_c = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) {
+        if (c1 <= c0 || r1 <= r0) return int(ADPB200_OK);
+        return cuda_check(cudaMemcpy2DAsync(out + c0 * n + r0, size_t(n) * 8, dC + c0 * n + r0, size_t(n) * 8,
+                                            size_t(r1 - r0) * 8, size_t(c1 - c0), cudaMemcpyDeviceToHost, h->d2h),
+                          "cudaMemcpy2DAsync(D2H C block)");
     };
     bool streamed = false;
-    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_b, copy_c, &streamed);
+    rc = run_streamed(h, P, o, tdev, st, a_ready, copy_a, copy_b, copy_c, &streamed);
     if (rc) return rc;
     if (!streamed) {
         if ((rc = cuda_check(cudaStreamWaitEvent(st, a_ready, 0), "cudaStreamWaitEvent"))) return rc;
+        if ((rc = h2d_block(dB, B, n, k, n, st))) return rc;
         if ((rc = h2d_block(dA, A, k, m, k, st))) return rc;
         HostOut hout{out, n};
         rc = run_pipeline(h, P, o, tdev, st, 0, 0, nullptr, 0, 0, nullptr, &hout);
