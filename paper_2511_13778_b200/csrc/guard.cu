@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
         for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
     for (int64_t tb = 0; tb < t; tb += kEscTB) {
         __syncthreads();
-#pragma unroll 1
+#pragma unroll
         for (int tt = st0; tt < kEscTB; tt += 4) {
             const int64_t gt = tb + tt;
             const bool tok = gt < t;
