@@ -67,6 +67,7 @@ struct AdpConfig {
     std::size_t chunk_len = 65536;
     int pair_limit = ADPB200_PAIRS_FULL;  // ADPB200_PAIRS_TARGET skips the pairs below the target precision
     bool guardrails_forced = false;
+    bool esc_certified = false;  // ADPB200_ESC_CERTIFIED instead of the reference's coarsened ESC
 
     adpb200_options to_c() const {
         adpb200_options o;
@@ -81,6 +82,7 @@ struct AdpConfig {
         o.chunk_len = static_cast<int64_t>(chunk_len);
         o.pair_limit = pair_limit;
         o.guardrails_forced = guardrails_forced ? 1 : 0;
+        o.esc_method = esc_certified ? ADPB200_ESC_CERTIFIED : ADPB200_ESC_COARSENED;
         return o;
     }
     void validate() const {

@@ -43,6 +43,12 @@ static int cpu_checks() {
         return fail("cost_ratio 0 accepted");
     } catch (const std::invalid_argument&) {
     }
+    // the certified-ESC extension maps onto the C options
+    AdpConfig cc;
+    cc.esc_certified = true;
+    cc.validate();
+    if (cc.to_c().esc_method != ADPB200_ESC_CERTIFIED || AdpConfig{}.to_c().esc_method != ADPB200_ESC_COARSENED)
+        return fail("esc_method mapping");
     // parse_mode (adp.cpp:116-137)
     AdpConfig p;
     if (!parse_mode("emulate:11", p) || p.mode != AdpMode::ForceEmulate || p.forced_slices != 11)
