@@ -10,6 +10,7 @@ from .adp import (  # noqa: F401
     AdpConfig,
     AdpMode,
     AdpTrace,
+    GraphedDgemm,
     Handle,
     adp_gemm,
     block_exponent_stats,

@@ -308,6 +308,34 @@ def dgemm(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A: tor
                               None if trace is None else C.c_void_p(trace.data_ptr()), _stream(dev)))
 
 
+class GraphedDgemm:
+    """One dgemm call captured in a CUDA graph: the pipeline is stream-ordered with
+    no host synchronisation, so after a warm-up call (it sizes the handle's
+    workspace and encodes the TMA descriptors) the whole call records into a graph.
+    Each replay re-reads A, B (and C when beta != 0) from the captured buffers and
+    re-takes the ADP decision on the device; it removes the per-kernel launch gaps
+    that dominate small calls. Arguments as dgemm; the tensors must stay alive."""
+
+    def __init__(self, transa: str, transb: str, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
+                 B: torch.Tensor, ldb: int, beta: float, C_: torch.Tensor, ldc: int,
+                 config: Optional[AdpConfig] = None, handle: Optional[Handle] = None):
+        dev = C_.device
+        self.handle = handle or Handle(dev.index)
+        args = (transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C_, ldc, config, self.handle)
+        self.stream = torch.cuda.Stream(dev)
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(self.stream):
+            dgemm(*args)  # warm-up: workspace + descriptors, outside the capture
+        self.stream.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            dgemm(*args)
+
+    def __call__(self) -> None:
+        """Replay on the current stream (stream-ordered, no synchronisation)."""
+        self.graph.replay()
+
+
 def dgemm_host(transa: str, transb: str, m: int, n: int, k: int, alpha: float, A: torch.Tensor, lda: int,
                B: torch.Tensor, ldb: int, beta: float, C_: torch.Tensor, ldc: int, config: Optional[AdpConfig] = None,
                handle: Optional[Handle] = None, device: int = 0) -> AdpTrace:

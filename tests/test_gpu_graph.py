@@ -33,3 +33,23 @@ def test_dgemm_graph_replay_bitwise(gpu, n, lo):
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(C.view(torch.int64), Cg.view(torch.int64))
+
+
+def test_graphed_dgemm_helper(gpu):
+    """adp.GraphedDgemm: capture once, replay; each replay follows the buffers' data."""
+    import torch
+
+    from paper_2511_13778_b200 import grading
+
+    n = 640
+    A = grading.gen_uniform_rect(n, n, 3, 1.0, 2.0)
+    B = grading.gen_uniform_rect(n, n, 4, 1.0, 2.0)
+    C, Cg = (torch.empty((n, n), dtype=torch.float64, device="cuda") for _ in range(2))
+    cfg = gpu.AdpConfig()
+    g = gpu.GraphedDgemm("N", "T", n, n, n, 0.5, A, n, B, n, 0.0, Cg, n, cfg)
+    for seed in (5, 6):
+        A.copy_(grading.gen_uniform_rect(n, n, seed, -1.0, 1.0))
+        g()
+        gpu.dgemm("N", "T", n, n, n, 0.5, A, n, B, n, 0.0, C, n, cfg)
+        torch.cuda.synchronize()
+        assert torch.equal(C.view(torch.int64), Cg.view(torch.int64))
