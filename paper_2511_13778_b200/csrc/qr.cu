@@ -82,19 +82,15 @@ __global__ void panel_load_kernel(const double* __restrict__ f, int64_t ld, int6
     }
 }
 
-// make_reflector (qr.cpp:26-47) for panel column j; tau[j] to global memory
-__global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __restrict__ P, int64_t rows, int j,
-                                                                  double* __restrict__ tau,
-                                                                  double* __restrict__ vglob) {
-    extern __shared__ double vsh[];
-    double* v = vglob ? vglob : vsh;
-    double* q2 = v + rows;  // (v[r] / amax)^2, computed in parallel, summed in order by one thread
+// make_reflector (qr.cpp:26-47) of panel column j (global `col`), whose values for
+// rows [j, rows) are already in v; q2 is a rows-long scratch; tau[j] to global memory.
+// Called by the whole CTA.
+__device__ __forceinline__ void make_reflector_cta(double* __restrict__ col, double* v, double* q2, int64_t rows,
+                                                   int j, double* __restrict__ tau) {
     const int tid = threadIdx.x, nth = blockDim.x;
     __shared__ double red_s[32];
     __shared__ double v0_s, beta_s, x0_s, tail_s;
     __shared__ int mode_s;
-    double* col = P + int64_t(j) * rows;
-    for (int64_t r = j + tid; r < rows; r += nth) v[r] = col[r];
     __syncthreads();
     // column_norm's max (qr.cpp:15): exact and order-free, reduced in parallel
     double amax = 0.0;
@@ -165,28 +161,40 @@ __global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __rest
     }
 }
 
+// make_reflector for panel column j as its own kernel (the first column of a panel, and
+// the path for columns too long for shared memory). kSmem: the column lives in shared
+// memory (a compile-time address space, so the sequential sums read it with LDS at
+// shared-memory latency), else in the global scratch vglob.
+template <bool kSmem>
+__global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __restrict__ P, int64_t rows, int j,
+                                                                  double* __restrict__ tau,
+                                                                  double* __restrict__ vglob) {
+    extern __shared__ double vsh[];
+    double* v = kSmem ? vsh : vglob;
+    double* col = P + int64_t(j) * rows;
+    for (int64_t r = j + threadIdx.x; r < rows; r += blockDim.x) v[r] = col[r];
+    make_reflector_cta(col, v, v + rows, rows, j, tau);
+}
+
 // apply_reflector (qr.cpp:51-60) of column j to panel column j + 1 + blockIdx.x
+template <bool kStaged>
 __global__ void __launch_bounds__(kPanelThreads) apply_kernel(double* __restrict__ P, int64_t rows, int j,
-                                                              const double* __restrict__ tau, int staged) {
+                                                              const double* __restrict__ tau) {
     const double tj = tau[j];
     if (tj == 0.0) return;
     extern __shared__ double sh[];
     const int tid = threadIdx.x, nth = blockDim.x;
     const double* vcol = P + int64_t(j) * rows;
     double* dst = P + int64_t(j + 1 + blockIdx.x) * rows;
-    const double* sv = vcol;
-    const double* sd = dst;
-    if (staged) {
-        double* v = sh;
-        double* d = sh + rows;
+    if (kStaged) {
         for (int64_t r = j + tid; r < rows; r += nth) {
-            v[r] = vcol[r];
-            d[r] = dst[r];
+            sh[r] = vcol[r];
+            sh[rows + r] = dst[r];
         }
         __syncthreads();
-        sv = v;
-        sd = d;
     }
+    const double* sv = kStaged ? sh : vcol;
+    const double* sd = kStaged ? sh + rows : dst;
     __shared__ double w_s, head_s;
     if (tid == 0) {
         const double dot = seq_dot(sd[j], sv, sd, j + 1, rows);
@@ -199,6 +207,49 @@ __global__ void __launch_bounds__(kPanelThreads) apply_kernel(double* __restrict
     // element-independent update; with staging the new values go straight to P
     for (int64_t r = j + 1 + tid; r < rows; r += nth) dst[r] = __dsub_rn(sd[r], __dmul_rn(w, sv[r]));
     if (tid == 0) dst[j] = head_s;
+}
+
+// apply_reflector of column j to every later column, fused with the next step: CTA 0
+// updates column j + 1 in shared memory as well and then makes its reflector
+// (make_reflector of j + 1 needs exactly that column), so a panel takes one launch per
+// column; the other CTAs' updates run meanwhile. Shared-memory (staged) path only.
+__global__ void __launch_bounds__(kPanelThreads) apply_reflect_kernel(double* __restrict__ P, int64_t rows, int j,
+                                                                      double* __restrict__ tau) {
+    const double tj = tau[j];
+    const bool next = blockIdx.x == 0;  // this CTA owns column j + 1
+    if (tj == 0.0 && !next) return;
+    extern __shared__ double sh[];
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const double* vcol = P + int64_t(j) * rows;
+    double* dst = P + int64_t(j + 1 + blockIdx.x) * rows;
+    double* sv = sh;
+    double* sd = sh + rows;
+    for (int64_t r = j + tid; r < rows; r += nth) {
+        sv[r] = vcol[r];
+        sd[r] = dst[r];
+    }
+    __syncthreads();
+    if (tj != 0.0) {
+        __shared__ double w_s, head_s;
+        if (tid == 0) {
+            const double dot = seq_dot(sd[j], sv, sd, j + 1, rows);
+            const double w = __dmul_rn(tj, dot);
+            w_s = w;
+            head_s = __dsub_rn(sd[j], w);
+        }
+        __syncthreads();
+        const double w = w_s;
+        for (int64_t r = j + 1 + tid; r < rows; r += nth) {
+            const double x = __dsub_rn(sd[r], __dmul_rn(w, sv[r]));
+            dst[r] = x;
+            if (next) sd[r] = x;
+        }
+        if (tid == 0) dst[j] = head_s;
+    }
+    if (!next) return;
+    __syncthreads();
+    // column j + 1's reflector from its updated values (sd), sv reused as the squares
+    make_reflector_cta(dst, sd, sv, rows, j + 1, tau);
 }
 
 // write the panel back to f; build_y (qr.cpp:64-71)
@@ -216,17 +267,17 @@ __global__ void panel_store_kernel(const double* __restrict__ P, double* __restr
 
 // build_t's z (qr.cpp:79-85): z(i, j) = sum_{r >= j} y(r, i) y(r, j) for i < j, y(j, j) = 1
 // first, then the tails; one CTA per j (column j staged in shared memory when it fits)
+template <bool kStaged>
 __global__ void __launch_bounds__(kPanelThreads) build_z_kernel(const double* __restrict__ P, int64_t rows, int pw,
-                                                                double* __restrict__ z, int staged) {
+                                                                double* __restrict__ z) {
     extern __shared__ double sh[];
     const int j = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
     if (j == 0) return;
-    const double* cj = P + int64_t(j) * rows;
-    if (staged) {
-        for (int64_t r = j + tid; r < rows; r += nth) sh[r] = cj[r];
+    if (kStaged) {
+        for (int64_t r = j + tid; r < rows; r += nth) sh[r] = P[int64_t(j) * rows + r];
         __syncthreads();
-        cj = sh;
     }
+    const double* cj = kStaged ? sh : P + int64_t(j) * rows;
     for (int i = tid; i < j; i += nth) {
         const double* ci = P + int64_t(i) * rows;
         const double first = __dmul_rn(ci[j], 1.0);
@@ -375,9 +426,9 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
     double* z = bz.alloc(size_t(pwmax) * pwmax);
     if (!tau || !z) return 2;
     static bool attr = [] {
-        cudaFuncSetAttribute(reflector_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
-        cudaFuncSetAttribute(apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
-        cudaFuncSetAttribute(build_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(reflector_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(apply_reflect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(build_z_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
         return true;
     }();
     (void)attr;
@@ -392,16 +443,27 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         const bool vsmem = vbytes <= kPanelSmemMax;
         panel_load_kernel<<<grid_for(rows * pw), 256, 0, st>>>(f, n, p0, rows, pw, P);
         ++*nl;
-        for (int j = 0; j < pw; ++j) {
-            reflector_kernel<<<1, threads, vsmem ? vbytes : 0, st>>>(P, rows, j, tau, vsmem ? nullptr : vg);
+        if (vsmem) {
+            // one launch per column: update the later columns, make the next reflector
+            reflector_kernel<true><<<1, threads, vbytes, st>>>(P, rows, 0, tau, nullptr);
             ++*nl;
-            if (j + 1 < pw) {
-                apply_kernel<<<unsigned(pw - j - 1), threads, vsmem ? vbytes : 0, st>>>(P, rows, j, tau, vsmem ? 1 : 0);
+            for (int j = 0; j + 1 < pw; ++j) {
+                apply_reflect_kernel<<<unsigned(pw - j - 1), threads, vbytes, st>>>(P, rows, j, tau);
                 ++*nl;
+            }
+        } else {
+            for (int j = 0; j < pw; ++j) {
+                reflector_kernel<false><<<1, threads, 0, st>>>(P, rows, j, tau, vg);
+                ++*nl;
+                if (j + 1 < pw) {
+                    apply_kernel<false><<<unsigned(pw - j - 1), threads, 0, st>>>(P, rows, j, tau);
+                    ++*nl;
+                }
             }
         }
         panel_store_kernel<<<grid_for(rows * pw), 256, 0, st>>>(P, f, n, p0, rows, pw, y, yT);
-        build_z_kernel<<<unsigned(pw), threads, vsmem ? vbytes / 2 : 0, st>>>(P, rows, pw, z, vsmem ? 1 : 0);
+        if (vsmem) build_z_kernel<true><<<unsigned(pw), threads, vbytes / 2, st>>>(P, rows, pw, z);
+        else build_z_kernel<false><<<unsigned(pw), threads, 0, st>>>(P, rows, pw, z);
         build_t_kernel<<<1, threads, 0, st>>>(tau, z, pw, t, tT);
         *nl += 3;
         copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
