@@ -286,24 +286,36 @@ __global__ void __launch_bounds__(kPanelThreads) build_z_kernel(const double* __
 }
 
 // build_t (qr.cpp:75-94): T(j,j) = tau_j, T(0:j, j) = -tau_j T(0:j,0:j) z(:, j); and T^T
+template <bool kSmem>
 __global__ void __launch_bounds__(kPanelThreads) build_t_kernel(const double* __restrict__ tau,
                                                                 const double* __restrict__ z, int pw,
                                                                 double* __restrict__ t, double* __restrict__ tT) {
+    // T (pw x pw) in shared memory when it fits, and z's column j staged per step: the
+    // short sequential dots of the recursion then read LDS instead of global memory
+    extern __shared__ double tsh[];
+    double* T = kSmem ? tsh : t;
+    double* zj = kSmem ? tsh + int64_t(pw) * pw : nullptr;
     const int tid = threadIdx.x, nth = blockDim.x;
-    for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) t[e] = 0.0;
+    for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) T[e] = 0.0;
     __syncthreads();
     for (int j = 0; j < pw; ++j) {
-        if (tid == 0) t[j * pw + j] = tau[j];
+        if (kSmem) {
+            for (int l = tid; l < j; l += nth) zj[l] = z[int64_t(l) * pw + j];
+            __syncthreads();
+        }
+        if (tid == 0) T[j * pw + j] = tau[j];
         for (int i = tid; i < j; i += nth) {
             double dot = 0.0;
-            for (int l = i; l < j; ++l) dot = __dadd_rn(dot, __dmul_rn(t[i * pw + l], z[int64_t(l) * pw + j]));
-            t[i * pw + j] = __dmul_rn(-tau[j], dot);
+            for (int l = i; l < j; ++l)
+                dot = __dadd_rn(dot, __dmul_rn(T[i * pw + l], kSmem ? zj[l] : z[int64_t(l) * pw + j]));
+            T[i * pw + j] = __dmul_rn(-tau[j], dot);
         }
         __syncthreads();
     }
     for (int64_t e = tid; e < int64_t(pw) * pw; e += nth) {
         const int64_t i = e / pw, jj = e - i * pw;
-        tT[jj * pw + i] = t[e];
+        tT[jj * pw + i] = T[e];
+        if (kSmem) t[e] = T[e];
     }
 }
 
@@ -429,6 +441,7 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         cudaFuncSetAttribute(reflector_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
         cudaFuncSetAttribute(apply_reflect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
         cudaFuncSetAttribute(build_z_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
+        cudaFuncSetAttribute(build_t_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmemMax));
         return true;
     }();
     (void)attr;
@@ -464,7 +477,9 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         panel_store_kernel<<<grid_for(rows * pw), 256, 0, st>>>(P, f, n, p0, rows, pw, y, yT);
         if (vsmem) build_z_kernel<true><<<unsigned(pw), threads, vbytes / 2, st>>>(P, rows, pw, z);
         else build_z_kernel<false><<<unsigned(pw), threads, 0, st>>>(P, rows, pw, z);
-        build_t_kernel<<<1, threads, 0, st>>>(tau, z, pw, t, tT);
+        const size_t tbytes = (size_t(pw) * pw + pw) * sizeof(double);
+        if (tbytes <= kPanelSmemMax) build_t_kernel<true><<<1, threads, tbytes, st>>>(tau, z, pw, t, tT);
+        else build_t_kernel<false><<<1, threads, 0, st>>>(tau, z, pw, t, tT);
         *nl += 3;
         copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
         ++*nl;
