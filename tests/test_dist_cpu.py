@@ -108,6 +108,11 @@ def test_dist_decision_matches_decide():
     assert dist_decision([256, 8], 8192, 8192, 8192, cc) == (0, 8, 8, 48)
     assert dist_decision([257, 8], 8192, 8192, 8192, cc)[0] == 1
     assert dist_decision([0, 8], 100, 8192, 8192, cc) == (1, 0, 0, 0)  # too small: no ESC, no certificate
+    # two certificate levels in bits 8-9 (max over ranks): v = 0 level 0 held, 1 only level 1, 2 neither
+    assert dist_decision([0, 12], 8192, 8192, 8192, cc)[1] == 7
+    assert dist_decision([1 << 8, 12], 8192, 8192, 8192, cc)[1] == 8
+    assert dist_decision([2 << 8, 12], 8192, 8192, 8192, cc)[1] == 9
+    assert dist_decision([2 << 8, 12], 8192, 8192, 8192, AdpConfig(pair_limit=PAIRS_TARGET))[1] == 9
 
 
 def _collective_worker(rank, world, port, results):
