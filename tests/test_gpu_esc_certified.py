@@ -155,3 +155,20 @@ def test_certified_streamed_dgemm_host_matches_device(gpu, ta, tb):
         torch.cuda.synchronize()
         assert tr.path == "emulated" and tr.slices == 7  # U[-1,1] certified down to s0 = 7
         assert torch.equal(C_h.view(torch.int64), Cd.cpu().view(torch.int64))
+
+
+@pytest.mark.parametrize("block_len", [16, 100, 1024])
+def test_certified_with_other_esc_block_lengths(gpu, port, block_len):
+    """The certificate composes with any esc_block_len: the device decision equals
+    the restatement applied to the reference's coarsened ESC at that block length."""
+    import torch
+
+    for name in ("u11", "wide", "zero_col"):
+        a, b = _make(name, 280, 900, 300, block_len)
+        coarse = port.esc_coarsened(a, b, block_len, 53)[0]
+        want = esc_certified(a, b, coarse, 53)
+        cfg = gpu.AdpConfig(esc_method="certified", esc_block_len=block_len)
+        got, t = gpu.adp_gemm(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), config=cfg)
+        assert t.esc_bits == want, (name, t.esc_bits, want, coarse)
+        if t.path == "emulated":
+            assert_bitwise(got.cpu().numpy(), port.emulated_gemm(a, b, t.slices), nan_equiv=False)
