@@ -213,6 +213,30 @@ GemmArgs count_args(adpb200_context* h, const Layout& Lw, const Problem& P, Plan
     return g;
 }
 
+// GEMM variants (NB) the device plan can pick for these options and this k: the s range
+// is [required_slices(target_bits, 0), max_slices] in auto mode, the forced s otherwise;
+// only those variants are launched (the rest would exit at once).
+bool variant_possible(int nb, const adpb200_options& o, int64_t K, int fixed_slices, int fixed_limit) {
+    int s_lo, s_hi, limit;
+    if (fixed_slices > 0) {
+        s_lo = s_hi = fixed_slices;
+        limit = fixed_limit;
+    } else if (o.mode == ADPB200_MODE_EMULATE) {
+        s_lo = s_hi = o.forced_slices;
+        limit = o.pair_limit;
+    } else {
+        s_lo = required_slices(o.target_bits, 0);
+        s_hi = o.max_slices;
+        limit = o.pair_limit;
+    }
+    for (int s = s_lo; s <= s_hi; ++s) {
+        Plan hp{};
+        fill_emulation_plan(hp, s, limit, K);
+        if (hp.variant == nb) return true;
+    }
+    return false;
+}
+
 constexpr int kHostChunks = 4;  // row chunks of the host-buffer path (GEMM chunk i || D2H chunk i-1); 8 measured slower
 
 // Destination of C on the host for the host-buffer entry points.
@@ -367,11 +391,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
             g.mt_begin = mtiles * c / nchunk;
             g.mt_end = hout ? mtiles * (c + 1) / nchunk : 0;
             for (int nb : variants) {
-                if (fixed_slices > 0) {  // the host knows the variant
-                    Plan hp{};
-                    fill_emulation_plan(hp, fixed_slices, fixed_limit, P.K);
-                    if (hp.variant != nb) continue;
-                }
+                if (!variant_possible(nb, o, P.K, fixed_slices, fixed_limit)) continue;
                 if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
                     return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
             }
