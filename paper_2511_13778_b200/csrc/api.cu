@@ -84,10 +84,23 @@ int cuda_check(cudaError_t e, const char* what) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Deferred rounding: the GEMM parks the folded words and a separate HBM-bound pass
+// rounds them, so short-k tiles do not wait on the epilogue's rounding (the MMA warp
+// otherwise waits ~31 % of the time at k = 1024). Needs 16 B of scratch per element.
+bool deferred_rounding(int64_t M, int64_t N, int64_t K) {
+    static const int mode = [] {  // -1 auto, 0 off, 1 on (ADPB200_DEFER_ROUND)
+        const char* e = getenv("ADPB200_DEFER_ROUND");
+        return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+    }();
+    if (mode == 0 || M <= 0 || N <= 0 || M * N > (int64_t(1) << 28)) return false;
+    // auto: short k over a large C (65536 x 1024 x 1024: +10 %; 2048^3 and 8192^3 lose 2-9 %)
+    return mode == 1 || (K <= 1536 && M * N >= (int64_t(1) << 24));
+}
+
 // Carve-up of the workspace for one call.
 struct Layout {
     size_t plan, stats_a_max, stats_a_min, line_a, stats_b_max, stats_b_min, line_b, scale_a, scale_b, planes_a,
-        planes_b, partial, scratch, rplan, total;
+        planes_b, partial, scratch, rplan, fold, total;
     int64_t blocks, pitch, slots_a, slots_b;
     int cap;
 };
@@ -120,6 +133,7 @@ Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) 
     L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
     L.scratch = take(4096);
     L.rplan = take(sizeof(Plan));
+    L.fold = deferred_rounding(M, N, K) ? take(size_t(M) * size_t(N) * 16) : 0;
     L.total = off;
     return L;
 }
@@ -377,6 +391,8 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         GemmArgs g = product_args(h, Lw, P, plan, sb);
         g.dump = dump;
         g.ndump = ndump;
+        const bool defer = !hout && !dump && deferred_rounding(P.M, P.N, P.K);
+        if (defer) g.fold_out = at<uint32_t>(h, Lw.fold);
         int variants[5] = {64, 48, 32, 16, 8};
         if (hout) {
             // host-buffer path: the (predicated) fallback first, then the GEMM in
@@ -401,6 +417,9 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                 if (rc2) return rc2;
             }
         }
+        if (defer)
+            launch_round_folded(plan, at<uint32_t>(h, Lw.fold), P.M, P.N, sa, sb, P.alpha, P.beta, P.c_in, P.ldc_in,
+                                P.c_out, P.ldc, st, nl);
         tm.end(4);
         if (hout) return cuda_check(cudaGetLastError(), "kernel launch");
     }

@@ -651,6 +651,20 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                         tc::fence_before();
                         tc::mbar_arrive(&hdr->tmem_empty);
                         if (timing) hold += clock64() - th;
+                        if (g.fold_out && lp.nchunks == 1) {
+                            // deferred rounding: park the folded words, a separate pass rounds
+                            const int64_t plane = g.M * g.N;
+#pragma unroll
+                            for (int jl = 0; jl < kCols; ++jl) {
+                                const int64_t col = col_base + jh * kCols + jl;
+                                if (!row_ok || col >= col_end) continue;
+                                uint32_t* o = g.fold_out + col * g.M + row;
+#pragma unroll
+                                for (int i = 0; i < kW; ++i) o[i * plane] = w[jl][i];
+                            }
+                            acc_phase ^= 1;
+                            continue;
+                        }
                         // phase B (TMEM already back with the MMA warp): round, scale, store
 #pragma unroll
                         for (int jl = 0; jl < kCols; ++jl) {
@@ -1008,6 +1022,45 @@ int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int 
     if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
     *nlaunch += 5;
     return rc;
+}
+
+// ---- deferred rounding of the folded words --------------------------------------
+namespace {
+__global__ void round_folded_kernel(const Plan* __restrict__ plan, const uint32_t* __restrict__ fold, int64_t M,
+                                    int64_t N, const int32_t* __restrict__ scale_a,
+                                    const int32_t* __restrict__ scale_b, double alpha, double beta,
+                                    const double* __restrict__ c_in, int64_t ldc_in, double* __restrict__ c_out,
+                                    int64_t ldc) {
+    if (plan->path != ADPB200_PATH_EMULATED || plan->nchunks != 1) return;
+    const int nb = plan->variant;
+    if (nb != 64 && nb != 48) return;
+    const int kW = nb == 64 ? 3 : 4;
+    const int exp_fix = -14 - 8 * (512 / nb - 1);  // S' = S 256^(kNDMax-1-L), as in the GEMM epilogue
+    const int64_t plane = M * N;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < plane; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t col = e / M, row = e - col * M;
+        const uint32_t w0 = fold[e], w1 = fold[plane + e], w2 = fold[2 * plane + e];
+        uint64_t S0 = uint64_t(w0) | (uint64_t(w1) << 32), S1;
+        if (kW == 3) S1 = uint64_t(int64_t(int32_t(w2)));
+        else S1 = uint64_t(w2) | (uint64_t(fold[3 * plane + e]) << 32);
+        const double vv = round_i128(__int128((unsigned __int128)S1 << 64 | S0), scale_a[row] + scale_b[col] + exp_fix);
+        double r = __dmul_rn(alpha, vv);
+        if (beta != 0.0) r = __dadd_rn(r, __dmul_rn(beta, c_in[row + col * ldc_in]));
+        c_out[row + col * ldc] = r;
+    }
+}
+}  // namespace
+
+void launch_round_folded(const Plan* plan, const uint32_t* fold, int64_t M, int64_t N, const int32_t* scale_a,
+                         const int32_t* scale_b, double alpha, double beta, const double* c_in, int64_t ldc_in,
+                         double* c_out, int64_t ldc, cudaStream_t st, uint64_t* nlaunch) {
+    const int64_t total = M * N;
+    if (total == 0) return;
+    const int64_t want = (total + 255) / 256;
+    const int grid = int(want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16);
+    round_folded_kernel<<<grid, 256, 0, st>>>(plan, fold, M, N, scale_a, scale_b, alpha, beta, c_in, ldc_in, c_out,
+                                             ldc);
+    ++*nlaunch;
 }
 
 // ---- recompose stage export (igemm.cpp:99-127) -------------------------------------
