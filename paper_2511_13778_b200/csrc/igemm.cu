@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                         tc::fence_before();
                         tc::mbar_arrive(&hdr->tmem_empty);
                         if (timing) hold += clock64() - th;
-                        if (g.fold_out && lp.nchunks == 1) {
+                        if (NB == 64 && g.fold_out && lp.nchunks == 1) {
                             // deferred rounding: park the folded words, a separate pass rounds
                             const int64_t plane = g.M * g.N;
 #pragma unroll
@@ -1033,8 +1033,8 @@ __global__ void round_folded_kernel(const Plan* __restrict__ plan, const uint32_
                                     int64_t ldc) {
     if (plan->path != ADPB200_PATH_EMULATED || plan->nchunks != 1) return;
     const int nb = plan->variant;
-    if (nb != 64 && nb != 48) return;
-    const int kW = nb == 64 ? 3 : 4;
+    if (nb != 64) return;  // NB = 48 (s 8-9) keeps the fused rounding: its tiles are long enough
+    const int kW = 3;
     const int exp_fix = -14 - 8 * (512 / nb - 1);  // S' = S 256^(kNDMax-1-L), as in the GEMM epilogue
     const int64_t plane = M * N;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < plane; e += int64_t(gridDim.x) * blockDim.x) {

@@ -32,7 +32,7 @@ struct GemmArgs {
     int64_t mt_begin, mt_end;  // 128-row m-tile range to compute (mt_end 0 = all)
     int64_t nt_begin, nt_end;  // NB-column n-tile range to compute (nt_end 0 = all)
     int32_t* zero_flag;        // certified ESC: no C; set to 1 if any (i, j) has a zero diagonal-0 count
-    uint32_t* fold_out;        // deferred rounding (NB 64/48, one k-chunk): the folded words go to
+    uint32_t* fold_out;        // deferred rounding (NB 64, one k-chunk): the folded words go to
                                // fold_out[word][col][row] (M x N per word) instead of C
     // fused all-gather -> GEMM (multi-GPU phase 7): B planes and scales read in place
     // from every rank's slab record over peer memory; rank r owns columns
@@ -58,7 +58,7 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
                  int64_t nkb, int cap, const GemmArgs& g, cudaStream_t st, uint64_t* nlaunch);
 
 // Deferred rounding: C from the folded words the GEMM left in fold (4 planes of M x N
-// uint32, column-major); predicated on the plan (variant 64 / 48, one k-chunk), like the GEMM.
+// uint32, column-major); predicated on the plan (variant 64, one k-chunk), like the GEMM.
 void launch_round_folded(const Plan* plan, const uint32_t* fold, int64_t M, int64_t N, const int32_t* scale_a,
                          const int32_t* scale_b, double alpha, double beta, const double* c_in, int64_t ldc_in,
                          double* c_out, int64_t ldc, cudaStream_t st, uint64_t* nlaunch);
