@@ -105,7 +105,7 @@ struct Layout {
     int cap;
 };
 
-Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) {
+Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap, bool fold = false) {
     Layout L{};
     L.blocks = K == 0 ? 0 : (K + block_len - 1) / block_len;
     L.pitch = (int64_t)align_up((size_t)std::max<int64_t>(K, 1), 32);
@@ -133,7 +133,7 @@ Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap) 
     L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
     L.scratch = take(4096);
     L.rplan = take(sizeof(Plan));
-    L.fold = deferred_rounding(M, N, K) ? take(size_t(M) * size_t(N) * 16) : 0;
+    L.fold = fold && deferred_rounding(M, N, K) ? take(size_t(M) * size_t(N) * 16) : 0;
     L.total = off;
     return L;
 }
@@ -315,7 +315,8 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                  cudaStream_t st, int fixed_slices, int fixed_limit, int64_t* dump, int ndump, int phase = 0,
                  int32_t* xchg = nullptr, const HostOut* hout = nullptr) {
     const int cap = plane_cap(o, fixed_slices, fixed_limit);
-    const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
+    const bool defer = !hout && !dump && deferred_rounding(P.M, P.N, P.K);  // only this path rounds apart
+    const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap, defer);
     int rc = ensure_ws(h, Lw.total, st);
     if (rc) return rc;
     uint64_t* nl = &h->launches;
@@ -391,7 +392,6 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         GemmArgs g = product_args(h, Lw, P, plan, sb);
         g.dump = dump;
         g.ndump = ndump;
-        const bool defer = !hout && !dump && deferred_rounding(P.M, P.N, P.K);
         if (defer) g.fold_out = at<uint32_t>(h, Lw.fold);
         int variants[5] = {64, 48, 32, 16, 8};
         if (hout) {
