@@ -53,6 +53,9 @@ extern "C" {
 
 /* Native-fallback flavour. */
 #define ADPB200_FALLBACK_REFERENCE 0 /* ascending-k, separate mul/add: bitwise native_gemm */
+#define ADPB200_FALLBACK_FAST 1      /* FP64 tensor cores (DMMA m8n8k4), fused multiply-adds:
+                                        |C - AB| <= gamma_k |A||B| (+ alpha/beta roundings),
+                                        not the reference's bits; opt-in */
 
 typedef struct adpb200_options {
     /* ozadp::AdpConfig (adp.hpp:18-33), same meaning and defaults */
@@ -80,9 +83,21 @@ typedef struct adpb200_options {
                                   rowmax_i + colmax_j (delta the largest with 2*delta+1 <= the
                                   ESC s0 tolerates); if so esc_bits = 2*delta+1 (an upper bound
                                   of esc_exact, esc.cpp:61-87), else the coarsened value stays.
-                                  Single-GPU entry points; the multi-GPU phases ignore it. */
-    int32_t reserved[4];
+                                  Honoured by every entry point: the multi-GPU phases run the
+                                  indicator GEMM on the local rows against the gathered column
+                                  indicators and max-reduce its verdict with the ESC. */
+    int32_t rounding;          /* ADPB200_ROUND_*: where the NB = 64 slice GEMM rounds the exact
+                                  sums to FP64 — inside its epilogue (FUSED) or in a separate
+                                  HBM pass over parked folded words (DEFERRED, 12 B of workspace
+                                  per element of C; pays off for short k over a large C). AUTO
+                                  defers for k <= 1536 and m*n >= 2^24 (env ADPB200_DEFER_ROUND
+                                  = 0/1 overrides AUTO). Bitwise the same C either way. */
+    int32_t reserved[3];
 } adpb200_options;
+
+#define ADPB200_ROUND_AUTO 0
+#define ADPB200_ROUND_FUSED 1
+#define ADPB200_ROUND_DEFERRED 2
 
 #define ADPB200_ESC_COARSENED 0
 #define ADPB200_ESC_CERTIFIED 1
@@ -102,6 +117,8 @@ typedef struct adpb200_trace {
     int64_t m, n, k;
     int32_t gemm_variant; /* columns per diagonal accumulator of the tcgen05 kernel */
     int32_t k_chunks;     /* int32 TMEM accumulation chunks along k */
+    int32_t rounding_deferred; /* 1: C was rounded by the separate pass (adpb200_options.rounding) */
+    int32_t reserved_t;
 } adpb200_trace;
 
 typedef struct adpb200_context* adpb200_handle;
@@ -344,6 +361,8 @@ int adpb200_qr_residual(adpb200_handle handle, int64_t m, int64_t n, int64_t pan
 
 /* Kernel launches issued by this handle since creation (all kernels are ours). */
 uint64_t adpb200_launch_count(adpb200_handle handle);
+/* bytes of device workspace the handle currently owns (grows on demand, never shrinks) */
+uint64_t adpb200_workspace_bytes(adpb200_handle handle);
 
 /* Stage timing with CUDA events on the caller's stream (no effect on results).
  * Stages: 0 scan+stats (K1), 1 ESC (K2), 2 decide, 3 slicing (K3),

@@ -5,7 +5,7 @@ DGEMM of arXiv 2511.13778 (reference: ozadp::adp_gemm). All arithmetic runs
 in the CUDA kernels of libadpb200.so (C ABI: include/adpb200.h); this Python
 package mirrors the reference's host interface on top of it.
 """
-from ._lib import LIB_PATH, PAIRS_FULL, PAIRS_TARGET, lib  # noqa: F401
+from ._lib import LIB_PATH, PAIRS_FULL, PAIRS_TARGET, TRACE_BYTES, lib  # noqa: F401
 from .adp import (  # noqa: F401
     AdpConfig,
     AdpMode,

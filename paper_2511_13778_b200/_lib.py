@@ -34,7 +34,8 @@ class Options(C.Structure):
         ("guardrails_forced", C.c_int32),
         ("fallback", C.c_int32),
         ("esc_method", C.c_int32),
-        ("reserved", C.c_int32 * 4),
+        ("rounding", C.c_int32),
+        ("reserved", C.c_int32 * 3),
     ]
 
 
@@ -58,6 +59,8 @@ class Trace(C.Structure):
         ("k", C.c_int64),
         ("gemm_variant", C.c_int32),
         ("k_chunks", C.c_int32),
+        ("rounding_deferred", C.c_int32),
+        ("reserved_t", C.c_int32),
     ]
 
 
@@ -87,6 +90,7 @@ def lib() -> C.CDLL:
         "adpb200_create": (C.c_int, [C.POINTER(vp), C.c_int]),
         "adpb200_destroy": (C.c_int, [vp]),
         "adpb200_launch_count": (C.c_uint64, [vp]),
+        "adpb200_workspace_bytes": (C.c_uint64, [vp]),
         "adpb200_decide_host": (C.c_int, [C.c_int, C.c_int, i64, i64, i64, C.c_int, popt, C.POINTER(i32),
                                           C.POINTER(f64)]),
         "adpb200_dgemm": (C.c_int, [vp, C.c_char, C.c_char, i64, i64, i64, f64, vp, i64, vp, i64, f64, vp, i64,
@@ -135,7 +139,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = (
     "adpb200_version", "adpb200_last_error", "adpb200_status_string", "adpb200_default_options",
-    "adpb200_validate_options", "adpb200_create", "adpb200_destroy", "adpb200_launch_count",
+    "adpb200_validate_options", "adpb200_create", "adpb200_destroy", "adpb200_launch_count", "adpb200_workspace_bytes",
     "adpb200_decide_host", "adpb200_dgemm", "adpb200_adp_gemm", "adpb200_dgemm_rows", "adpb200_dgemm_host",
     "adpb200_adp_gemm_host", "adpb200_scan", "adpb200_block_stats",
     "adpb200_esc_coarsened", "adpb200_decompose", "adpb200_slice_pair_mm", "adpb200_emulated_gemm",

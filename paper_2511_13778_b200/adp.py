@@ -42,6 +42,8 @@ class AdpMode(enum.IntEnum):
 
 
 ESC_METHODS = {"coarsened": 0, "certified": 1}
+ROUNDING_MODES = {"auto": 0, "fused": 1, "deferred": 2}
+FALLBACKS = {"reference": 0, "fast": 1}
 
 
 @dataclass
@@ -61,6 +63,11 @@ class AdpConfig:
     # "coarsened" (the reference's esc_coarsened) or "certified": the coarsened ESC
     # lowered to the s0 bound when an INT8 indicator GEMM certifies it (adpb200.h)
     esc_method: str = "coarsened"
+    # where the NB = 64 GEMM rounds: "auto", "fused" (in its epilogue) or "deferred"
+    # (a separate pass over parked folded words); bitwise the same C
+    rounding: str = "auto"
+    # native fallback flavour: "reference" (bitwise native_gemm) or "fast" (DMMA)
+    fallback: str = "reference"
 
     def to_c(self) -> _lib.Options:
         o = _lib.default_options()
@@ -75,6 +82,8 @@ class AdpConfig:
         o.pair_limit = int(self.pair_limit)
         o.guardrails_forced = 1 if self.guardrails_forced else 0
         o.esc_method = ESC_METHODS.get(self.esc_method, -1)
+        o.rounding = ROUNDING_MODES.get(self.rounding, -1)
+        o.fallback = FALLBACKS.get(self.fallback, -1)
         return o
 
     def validate(self) -> None:
@@ -101,6 +110,7 @@ class AdpTrace:
     pairs: int = 0
     gemm_variant: int = 0
     k_chunks: int = 0
+    rounding_deferred: bool = False
 
     @staticmethod
     def from_c(t: _lib.Trace) -> "AdpTrace":
@@ -114,6 +124,7 @@ class AdpTrace:
             modeled_cost_ratio=float(t.modeled_cost_ratio),
             pair_limit=None if t.pair_limit < 0 else int(t.pair_limit), pairs=int(t.pairs),
             gemm_variant=int(t.gemm_variant), k_chunks=int(t.k_chunks),
+            rounding_deferred=bool(t.rounding_deferred),
         )
 
     @property
@@ -200,6 +211,9 @@ class Handle:
 
     def launches(self) -> int:
         return int(lib().adpb200_launch_count(self.h))
+
+    def workspace_bytes(self) -> int:
+        return int(lib().adpb200_workspace_bytes(self.h))
 
     def profile_enable(self, max_calls: int) -> None:
         """Record CUDA events around each pipeline stage of the next calls."""

@@ -37,18 +37,26 @@ def _stale(target: str, deps) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libadpb200.so; with `variant`, an A/B build of the same sources with extra
+    -D defines into ab/lib_<variant>.so (objects under build/adpb200_<variant>)."""
+    build_dir, lib_out, flags = BUILD, LIB, list(FLAGS)
+    if variant:
+        build_dir = BUILD + "_" + variant
+        lib_out = os.path.join(ROOT, "ab", f"lib_{variant}.so")
+        os.makedirs(os.path.dirname(lib_out), exist_ok=True)
+        flags += ["-D" + d for d in defines]
+    os.makedirs(build_dir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(INCLUDE, "adpb200.h"))
     objs = []
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        o = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC] + FLAGS + ["-c", s, "-o", o])
+            jobs.append([NVCC] + flags + ["-c", s, "-o", o])
 
     def run(cmd):
         if verbose:
@@ -60,10 +68,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _stale(LIB, objs):
-        run([NVCC, "-shared", "-cudart", "static", "-o", LIB] + objs + ["-ldl", "-lpthread", "-lrt"])
-    return LIB
+    if force or jobs or _stale(lib_out, objs):
+        run([NVCC, "-shared", "-cudart", "static", "-o", lib_out] + objs + ["-ldl", "-lpthread", "-lrt"])
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    # python -m paper_2511_13778_b200.build [--force] [--variant NAME -DNAME=VAL ...]
+    args = sys.argv[1:]
+    var = args[args.index("--variant") + 1] if "--variant" in args else ""
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose=True, variant=var, defines=defs))

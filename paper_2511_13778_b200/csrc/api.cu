@@ -48,6 +48,7 @@ struct adpb200_context {
     cudaEvent_t h2d_ev[2 * kMaxStreamChunks + 2] = {};  // B chunks, A chunks, [2k] a_ready, [2k+1] start
     Plan* host_plan = nullptr;
     int spec_s = 7;
+    bool ws_pinned = false;  // a call was captured into a CUDA graph: the workspace may not move
 };
 
 namespace {
@@ -86,13 +87,18 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 // Deferred rounding: the GEMM parks the folded words and a separate HBM-bound pass
 // rounds them, so short-k tiles do not wait on the epilogue's rounding (the MMA warp
-// otherwise waits ~31 % of the time at k = 1024). Needs 16 B of scratch per element.
-bool deferred_rounding(int64_t M, int64_t N, int64_t K) {
-    static const int mode = [] {  // -1 auto, 0 off, 1 on (ADPB200_DEFER_ROUND)
+// otherwise waits ~31 % of the time at k = 1024). Needs 12 B of scratch per element
+// (the NB = 64 variant parks three 32-bit words of the folded sum).
+constexpr size_t kFoldBytesPerElement = 12;
+bool deferred_rounding(int64_t M, int64_t N, int64_t K, int rounding) {
+    static const int env = [] {  // -1 unset, 0 off, 1 on (ADPB200_DEFER_ROUND): refines ADPB200_ROUND_AUTO
         const char* e = getenv("ADPB200_DEFER_ROUND");
         return e ? (atoi(e) != 0 ? 1 : 0) : -1;
     }();
-    if (mode == 0 || M <= 0 || N <= 0 || M * N > (int64_t(1) << 28)) return false;
+    if (rounding == ADPB200_ROUND_FUSED || M <= 0 || N <= 0 || M * N > (int64_t(1) << 28)) return false;
+    if (rounding == ADPB200_ROUND_DEFERRED) return true;
+    const int mode = env;
+    if (mode == 0) return false;
     // auto: short k over a large C (65536 x 1024 x 1024: +10 %; 2048^3 and 8192^3 lose 2-9 %)
     return mode == 1 || (K <= 1536 && M * N >= (int64_t(1) << 24));
 }
@@ -133,13 +139,25 @@ Layout make_layout(int64_t M, int64_t N, int64_t K, int64_t block_len, int cap, 
     L.partial = take(cap ? kPartialBytesPerCta * size_t(num_sms()) : 0);
     L.scratch = take(4096);
     L.rplan = take(sizeof(Plan));
-    L.fold = fold && deferred_rounding(M, N, K) ? take(size_t(M) * size_t(N) * 16) : 0;
+    L.fold = fold ? take(size_t(M) * size_t(N) * kFoldBytesPerElement) : 0;
     L.total = off;
     return L;
 }
 
 int ensure_ws(adpb200_context* h, size_t bytes, cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cap = cudaStreamCaptureStatusNone;
+    // a captured graph holds raw pointers into the workspace: once a call has been
+    // captured on this handle the workspace must never move (a replay would touch
+    // freed memory), and a capture itself cannot allocate
+    if (cap != cudaStreamCaptureStatusNone) h->ws_pinned = true;
     if (h->ws_bytes >= bytes) return ADPB200_OK;
+    if (cap != cudaStreamCaptureStatusNone)
+        return fail(ADPB200_ERR_RUNTIME, "workspace too small inside a CUDA-graph capture: make one uncaptured "
+                                         "call with the same shape and options on this handle first");
+    if (h->ws_pinned)
+        return fail(ADPB200_ERR_RUNTIME, "this handle's workspace is referenced by a captured CUDA graph and "
+                                         "cannot grow: use a separate handle for larger calls");
     if (h->ws) {
         int rc = cuda_check(cudaFreeAsync(h->ws, st), "cudaFreeAsync(workspace)");
         if (rc) return rc;
@@ -297,7 +315,7 @@ int run_certify(adpb200_context* h, const Problem& P, const adpb200_options& o, 
                  nl, 1);
     const GemmArgs g = count_args(h, Lw, P, rplan, kw);
     if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, Lw.cap, g, st, nl))
-        return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
+        return fail(ADPB200_ERR_RUNTIME, "indicator GEMM launch failed (tensor map encoding or kernel resources)");
     if (!rows_mode) launch_certify_finish(plan, rplan, o.target_bits, st, nl);
     return ADPB200_OK;
 }
@@ -315,7 +333,10 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
                  cudaStream_t st, int fixed_slices, int fixed_limit, int64_t* dump, int ndump, int phase = 0,
                  int32_t* xchg = nullptr, const HostOut* hout = nullptr) {
     const int cap = plane_cap(o, fixed_slices, fixed_limit);
-    const bool defer = !hout && !dump && deferred_rounding(P.M, P.N, P.K);  // only this path rounds apart
+    // only this path rounds apart, and only the NB = 64 variant parks folded words: no
+    // scratch unless the plan can actually reach that variant for these options and k
+    const bool defer = !hout && !dump && cap > 0 && deferred_rounding(P.M, P.N, P.K, o.rounding) &&
+                       variant_possible(64, o, P.K, fixed_slices, fixed_limit);
     const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap, defer);
     int rc = ensure_ws(h, Lw.total, st);
     if (rc) return rc;
@@ -373,7 +394,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     // decision
     tm.begin(2);
     if (fixed_slices > 0) launch_set_plan(plan, fixed_slices, fixed_limit, P.K, st, nl);
-    else launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, P.swap_ab, trace, st, nl);
+    else launch_decide(plan, o, P.tm, P.tn, P.tk, esc_expected ? 1 : 0, P.swap_ab, trace, st, nl, defer ? 1 : 0);
     tm.end(2);
 
     if (P.M == 0 || P.N == 0) return cuda_check(cudaGetLastError(), "launch");
@@ -398,7 +419,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
             // host-buffer path: the (predicated) fallback first, then the GEMM in
             // row chunks, each chunk's C rows copied to the host on a second stream
             // while the next chunk computes
-            launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+            launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl, o.fallback);
         }
         const int64_t mtiles = (P.M + 127) / 128;
         const int nchunk = hout ? int(std::min<int64_t>(mtiles, kHostChunks)) : 1;
@@ -409,7 +430,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
             for (int nb : variants) {
                 if (!variant_possible(nb, o, P.K, fixed_slices, fixed_limit)) continue;
                 if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
-                    return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+                    return fail(ADPB200_ERR_RUNTIME, "slice GEMM launch failed (tensor map encoding or kernel resources)");
             }
             if (hout) {
                 const int64_t r0 = g.mt_begin * 128, r1 = std::min<int64_t>(g.mt_end * 128, P.M);
@@ -428,7 +449,7 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     if (!dump && (fixed_slices <= 0 || P.K == 0)) {
         const Plan* pred = P.K == 0 ? nullptr : plan;
         tm.begin(5);
-        launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, pred, st, nl);
+        launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, pred, st, nl, o.fallback);
         tm.end(5);
     }
     if (hout && P.M > 0 && P.N > 0) return hout->copy_rows(h, 0, P.M, P, st);
@@ -519,7 +540,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
             launch_slice(aw, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, nullptr, rplan, 0, 1, st, nl, 1);
             const GemmArgs g = count_args(h, Lw, P, rplan, kw);
             if (launch_igemm(64, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
-                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the indicator planes");
+                return fail(ADPB200_ERR_RUNTIME, "indicator GEMM launch failed (tensor map encoding or kernel resources)");
         }
         tm.end(1);
         launch_dist_export(plan, rplan, io.xchg, cert ? 1 : 0, st, nl);
@@ -553,7 +574,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
                                           static_cast<const int8_t* const*>(io.gathered), io.world, nr, slab_hdr(nr),
                                           io.nsl, g, st, nl);
         tm.end(4);
-        if (prc) return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the peer slab planes");
+        if (prc) return fail(ADPB200_ERR_RUNTIME, "peer GEMM launch failed (tensor map encoding or kernel resources)");
         return cuda_check(cudaGetLastError(), "dist phase 7");
     }
     if ((phase == 5 || phase == 6) && io.nsl > 0) {
@@ -591,7 +612,7 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
                 g.nt_begin = ranges[q][0];
                 g.nt_end = ranges[q][1];
                 if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, nkb, cap, g, st, nl))
-                    return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+                    return fail(ADPB200_ERR_RUNTIME, "slice GEMM launch failed (tensor map encoding or kernel resources)");
             }
         }
         tm.end(4);
@@ -613,12 +634,12 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
         tm.begin(4);
         for (int nb : {64, 48, 32, 16, 8})
             if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, nkb, cap, g, st, nl))
-                return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+                return fail(ADPB200_ERR_RUNTIME, "slice GEMM launch failed (tensor map encoding or kernel resources)");
         tm.end(4);
     } else {
         const LineView bfull{static_cast<const double*>(io.gathered), P.N, P.K, P.K, 1};
         tm.begin(5);
-        launch_native(P.a, bfull, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+        launch_native(P.a, bfull, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl, o.fallback);
         tm.end(5);
     }
     return cuda_check(cudaGetLastError(), "dist phase 4");
@@ -783,7 +804,7 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
         g.nt_begin = c0 / nb;
         g.nt_end = (c1 + nb - 1) / nb;
         if (launch_igemm(nb, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
-            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
+            return fail(ADPB200_ERR_RUNTIME, "slice GEMM launch failed (tensor map encoding or kernel resources)");
         cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
         rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
         if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
@@ -809,8 +830,8 @@ int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o,
     launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, 0, cap, st, nl);
     for (int v : {64, 48, 32, 16, 8})
         if (launch_igemm(v, pa, pb, Lw.slots_a, Lw.slots_b, Lw.pitch / 32, cap, g, st, nl))
-            return fail(ADPB200_ERR_RUNTIME, "cuTensorMapEncodeTiled failed for the slice planes");
-    launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl);
+            return fail(ADPB200_ERR_RUNTIME, "slice GEMM launch failed (tensor map encoding or kernel resources)");
+    launch_native(P.a, P.b, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl, o.fallback);
     cudaEvent_t ev = h->chunk_ev[h->chunk_next++ % 16];
     rc = cuda_check(cudaEventRecord(ev, st), "cudaEventRecord");
     if (!rc) rc = cuda_check(cudaStreamWaitEvent(h->d2h, ev, 0), "cudaStreamWaitEvent(d2h)");
@@ -889,9 +910,12 @@ int adpb200_validate_options(const adpb200_options* o) {
     if (!(o->chunk_len >= 1 && o->chunk_len * 16384 < (int64_t(1) << 31)))
         return fail(3, "GemmParams: chunk_len * 16384 must stay below 2^31");
     if (o->pair_limit < ADPB200_PAIRS_TARGET) return fail(3, "options: bad pair_limit");
-    if (o->fallback != ADPB200_FALLBACK_REFERENCE) return fail(3, "options: bad fallback");
+    if (o->fallback != ADPB200_FALLBACK_REFERENCE && o->fallback != ADPB200_FALLBACK_FAST)
+        return fail(3, "options: bad fallback");
     if (o->esc_method != ADPB200_ESC_COARSENED && o->esc_method != ADPB200_ESC_CERTIFIED)
         return fail(3, "options: bad esc_method");
+    if (o->rounding < ADPB200_ROUND_AUTO || o->rounding > ADPB200_ROUND_DEFERRED)
+        return fail(3, "options: bad rounding");
     return ADPB200_OK;
 }
 
@@ -934,6 +958,7 @@ int adpb200_destroy(adpb200_handle h) {
 }
 
 uint64_t adpb200_launch_count(adpb200_handle h) { return h ? h->launches : 0; }
+uint64_t adpb200_workspace_bytes(adpb200_handle h) { return h ? uint64_t(h->ws_bytes) : 0; }
 
 int adpb200_profile_enable(adpb200_handle h, int max_calls) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "profile: null handle");

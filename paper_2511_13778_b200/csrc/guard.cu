@@ -376,7 +376,7 @@ __global__ void esc_finish_kernel(int32_t* out, int target_bits) {
 
 // ---- the decision kernel (one thread) ---------------------------------------------
 __global__ void decide_kernel(Plan* plan, adpb200_options opt, int64_t m, int64_t n, int64_t k,
-                              int esc_expected, int swap_ab, adpb200_trace* trace) {
+                              int esc_expected, int swap_ab, adpb200_trace* trace, int defer) {
     Plan& p = *plan;
     DecideInput in;
     in.exc_a = p.exc & 1;
@@ -424,6 +424,9 @@ __global__ void decide_kernel(Plan* plan, adpb200_options opt, int64_t m, int64_
         t.k = k;
         t.gemm_variant = p.variant;
         t.k_chunks = p.nchunks;
+        // the separate rounding pass runs exactly when the NB = 64 variant works on one k-chunk
+        t.rounding_deferred = defer && d.path == ADPB200_PATH_EMULATED && p.variant == 64 && p.nchunks == 1;
+        t.reserved_t = 0;
         *trace = t;
     }
 }
@@ -617,8 +620,8 @@ void launch_dist_import(Plan* plan, const int32_t* xchg, int target_bits, int ce
 }
 
 void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
-                   int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch) {
-    decide_kernel<<<1, 1, 0, st>>>(plan, opt, m, n, k, esc_expected, swap_ab, trace);
+                   int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch, int defer) {
+    decide_kernel<<<1, 1, 0, st>>>(plan, opt, m, n, k, esc_expected, swap_ab, trace, defer);
     ++*nlaunch;
 }
 

@@ -42,7 +42,7 @@ void launch_transpose_i32(const int32_t* src, int64_t lines, int64_t blocks, int
                           uint64_t* nlaunch);
 // swap_ab: the internal operands are the user's B (A-lines) and A (B-lines).
 void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
-                   int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch);
+                   int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch, int defer = 0);
 
 // Stage exports: a fixed emulation plan (slices s, pair policy) without guardrails.
 void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t st, uint64_t* nlaunch);

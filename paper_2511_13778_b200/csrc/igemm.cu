@@ -42,6 +42,18 @@ constexpr int kMaxStages = 8;
 #define ADPB200_GROUP_M 8  // measured: 8 beats 16 (-1.5..2 %: less DRAM traffic, less power, higher clock) and 32
 #endif
 constexpr int kGroupM = ADPB200_GROUP_M;   // raster: m-tiles per group
+// Per-thread registers after the warpgroup split. The CTA's pool is what the launch
+// reserved (384 threads x 168 registers): setmaxnreg.inc blocks until the pool has
+// the registers, so the split must fit it exactly or the epilogue never starts.
+constexpr int kLaunchRegs = 168;
+constexpr int kRegsCtl = 40;
+constexpr int kRegsEpi = 232;
+static_assert(128 * kRegsCtl + 256 * kRegsEpi <= 384 * kLaunchRegs, "register split exceeds the CTA pool");
+#ifndef ADPB200_NO_REGSPLIT
+#define ADPB200_SETMAXNREG(dir, n) asm volatile("setmaxnreg." dir ".sync.aligned.u32 %0;\n" ::"n"(n))
+#else
+#define ADPB200_SETMAXNREG(dir, n) ((void)0)
+#endif
 
 template <int NB>
 struct Cfg {
@@ -492,7 +504,13 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
     tc::fence_after();
     const uint32_t tmem_base = hdr->tmem_slot;
 
+    // Register split by warpgroup: the producer / MMA / allocator warpgroup needs few
+    // registers, the two epilogue warpgroups hold 32 columns x 3 parked fold words
+    // plus a TMEM batch each (without the split the epilogue spills ~400 B/thread).
+    // Each role's branch starts with its own setmaxnreg so ptxas sees the budget
+    // dominate the role's code.
     if (warp == 0) {
+        ADPB200_SETMAXNREG("dec", kRegsCtl);
         // ===== TMA producer (converged warp, one elected lane issues) =====
         int stage = 0;
         uint32_t phase = 0;
@@ -536,9 +554,13 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
         }
     } else if (warp == 1) {
         // ===== MMA issuer (converged warp, one elected lane issues) =====
+        ADPB200_SETMAXNREG("dec", kRegsCtl);
         mma_dispatch<NB>(s, L, lp, hdr, sched, tc::smem_u32(stages), tmem_base, g.debug);
-    } else if (warp >= C::kFirstEpiWarp) {
+    } else if (warp < C::kFirstEpiWarp) {
+        ADPB200_SETMAXNREG("dec", kRegsCtl);
+    } else {
         // ===== epilogue: (lane quadrant, column group) per warp =====
+        ADPB200_SETMAXNREG("inc", kRegsEpi);
         const int ew = warp - C::kFirstEpiWarp;
         const int q = warp & 3;                        // TMEM lane quadrant (warp id % 4)
         const int jh = ew / 4;                         // column group
@@ -838,12 +860,20 @@ bool encode_plane_map(CUtensorMap* map, const int8_t* planes, int64_t slots, int
 }
 
 template <int NB>
-void set_attr_once() {
-    static bool done = false;
-    if (!done) {
+bool set_attr_once() {
+    static int ok = -1;
+    if (ok < 0) {
         cudaFuncSetAttribute(igemm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
-        done = true;
+        // the warpgroup register split assumes the launch reserves exactly kLaunchRegs per
+        // thread; refuse to launch (an error, not a hang) if the binary says otherwise
+        cudaFuncAttributes fa{};
+        ok = cudaFuncGetAttributes(&fa, igemm_kernel<NB>) == cudaSuccess && fa.numRegs == kLaunchRegs ? 1 : 0;
+#ifdef ADPB200_NO_REGSPLIT
+        ok = 1;
+#endif
+        if (!ok) fprintf(stderr, "adpb200: igemm_kernel<%d> uses %d registers, expected %d\n", NB, fa.numRegs, kLaunchRegs);
     }
+    return ok == 1;
 }
 
 // Encoded maps are cached per (planes, shape, variant): re-encoding ~90 maps
@@ -898,23 +928,23 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     a.smem_bytes = kGemmSmemBytes;
     switch (nb) {
         case 64:
-            set_attr_once<64>();
+            if (!set_attr_once<64>()) return -3;
             igemm_kernel<64><<<grid, Cfg<64>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 48:
-            set_attr_once<48>();
+            if (!set_attr_once<48>()) return -3;
             igemm_kernel<48><<<grid, Cfg<48>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 32:
-            set_attr_once<32>();
+            if (!set_attr_once<32>()) return -3;
             igemm_kernel<32><<<grid, Cfg<32>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 16:
-            set_attr_once<16>();
+            if (!set_attr_once<16>()) return -3;
             igemm_kernel<16><<<grid, Cfg<16>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 8:
-            set_attr_once<8>();
+            if (!set_attr_once<8>()) return -3;
             igemm_kernel<8><<<grid, Cfg<8>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         default:
@@ -993,7 +1023,7 @@ int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, i
     const int64_t tiles = (mt_end - g.mt_begin) * world * ((nr + NB - 1) / NB);
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
-    set_attr_once<NB>();
+    if (!set_attr_once<NB>()) return -3;
     igemm_kernel<NB><<<grid, Cfg<NB>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
     return 0;
 }
@@ -1034,15 +1064,13 @@ __global__ void round_folded_kernel(const Plan* __restrict__ plan, const uint32_
     if (plan->path != ADPB200_PATH_EMULATED || plan->nchunks != 1) return;
     const int nb = plan->variant;
     if (nb != 64) return;  // NB = 48 (s 8-9) keeps the fused rounding: its tiles are long enough
-    const int kW = 3;
     const int exp_fix = -14 - 8 * (512 / nb - 1);  // S' = S 256^(kNDMax-1-L), as in the GEMM epilogue
     const int64_t plane = M * N;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < plane; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t col = e / M, row = e - col * M;
         const uint32_t w0 = fold[e], w1 = fold[plane + e], w2 = fold[2 * plane + e];
-        uint64_t S0 = uint64_t(w0) | (uint64_t(w1) << 32), S1;
-        if (kW == 3) S1 = uint64_t(int64_t(int32_t(w2)));
-        else S1 = uint64_t(w2) | (uint64_t(fold[3 * plane + e]) << 32);
+        const uint64_t S0 = uint64_t(w0) | (uint64_t(w1) << 32);
+        const uint64_t S1 = uint64_t(int64_t(int32_t(w2)));  // |S'| < 2^88: sign-extend bit 95
         const double vv = round_i128(__int128((unsigned __int128)S1 << 64 | S0), scale_a[row] + scale_b[col] + exp_fix);
         double r = __dmul_rn(alpha, vv);
         if (beta != 0.0) r = __dadd_rn(r, __dmul_rn(beta, c_in[row + col * ldc_in]));

@@ -68,11 +68,14 @@ void launch_recompose(const int64_t* acc, int64_t m, int64_t n, int ndiag, const
                       const int32_t* col_scale, double alpha, double beta, const double* c_in, double* out,
                       cudaStream_t st, uint64_t* nlaunch);
 
-// K6: native FP64 fallback in the reference's summation order (ascending k,
-// separate multiply and add: oracle.cpp:7-28). Runs iff the plan says
-// native (or always when plan == nullptr).
+// K6: native FP64 fallback. flavour ADPB200_FALLBACK_REFERENCE: the reference's
+// summation order (ascending k, separate multiply and add: oracle.cpp:7-28), bitwise;
+// ADPB200_FALLBACK_FAST: FP64 tensor cores (DMMA). Runs iff the plan says native (or
+// always when plan == nullptr); persistent grids, so a skipped launch is one small wave.
 void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
-                   int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch);
+                   int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch,
+                   int flavour = ADPB200_FALLBACK_REFERENCE);
+int num_sms();
 
 // Grading tools (grade.cu): Dot2 double-double GEMM oracle out[i + j*ldo]
 // (+ (|A||B|)_ij when absab != nullptr), and error_report on row-major

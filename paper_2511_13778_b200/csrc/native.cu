@@ -1,21 +1,31 @@
-// K6: the native FP64 fallback (native_gemm, proj/src/oracle.cpp:7-28).
+// K6: the native FP64 fallback (native_gemm, proj/src/oracle.cpp:7-28), two flavours.
 //
-// Every output is summed in ascending k with one rounding per multiply and
-// one per add (sum = sum + a*b, no FMA — the reference build disables
-// contraction, proj/CMakeLists.txt:16-18, and proj/tests/test_oracle.cpp:54-71
-// pins it), then r = alpha*sum, and r = r + beta*c only when beta != 0. The
-// result is therefore bitwise identical to the reference's fallback (NaN
-// payloads aside: the GPU produces the canonical NaN).
+// ADPB200_FALLBACK_REFERENCE (default) — bitwise the reference:
+//   every output is summed in ascending k with one rounding per multiply and
+//   one per add (sum = sum + a*b, no FMA — the reference build disables
+//   contraction, proj/CMakeLists.txt:16-18, and proj/tests/test_oracle.cpp:54-71
+//   pins it), then r = alpha*sum, and r = r + beta*c only when beta != 0
+//   (NaN payloads aside: the GPU produces the canonical NaN). SIMT FP64:
+//   64x64 CTA tiles, 4x4 outputs per thread, k staged through shared memory
+//   16 at a time; the k loop is never split, so the summation order per
+//   output element is exactly the reference's.
 //
-// Register-tiled 64x64 CTA tiles, 4x4 outputs per thread, k staged through
-// shared memory 16 at a time; the k loop is never split, so the summation
-// order per output element is exactly the reference's.
+// ADPB200_FALLBACK_FAST — the FP64 tensor cores (DMMA, mma.sync m8n8k4.f64):
+//   128x128 CTA tiles, 8 warps of 64x32, k staged 16 at a time through a
+//   3-deep cp.async ring; fused multiply-adds in ascending k within each
+//   output, so |C - AB| <= gamma_k |A||B| (+ the alpha/beta roundings) but not
+//   the reference's bits. Opt-in (adpb200_options.fallback).
+//
+// Both kernels are persistent (grid = resident CTAs, tiles strided over it), so
+// when the device plan says "emulated" the predicated launch costs one small
+// wave that reads the plan and exits, not a full grid of tiles.
 #include "igemm.cuh"
 
 namespace adpb200 {
 
 namespace {
 
+// ---- reference order (SIMT) ---------------------------------------------------------
 constexpr int kT = 64, kKT = 16;
 
 __global__ void __launch_bounds__(256) native_kernel(LineView a, LineView b, double alpha, double beta,
@@ -26,75 +36,262 @@ __global__ void __launch_bounds__(256) native_kernel(LineView a, LineView b, dou
     __shared__ double Bs[2][kKT][kT + 1];
     const int tid = threadIdx.x;
     const int tx = tid % 16, ty = tid / 16;
-    const int64_t i0 = int64_t(blockIdx.x) * kT, j0 = int64_t(blockIdx.y) * kT;
     const int64_t K = a.len;
+    const int64_t tiles_m = (a.lines + kT - 1) / kT, tiles_n = (b.lines + kT - 1) / kT;
 
-    auto load = [&](int buf, int64_t k0) {
-        // A tile: 64 lines x 16 positions; B tile: 64 lines x 16 positions.
+    for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
+        const int64_t i0 = (tile % tiles_m) * kT, j0 = (tile / tiles_m) * kT;
+        auto load = [&](int buf, int64_t k0) {
+            // A tile: 64 lines x 16 positions; B tile: 64 lines x 16 positions.
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            int e = tid + q * 256;
-            int li, kk;
-            if (a.ls == 1) { li = e % kT; kk = e / kT; }
-            else { kk = e % kKT; li = e / kKT; }
-            int64_t gi = i0 + li, gk = k0 + kk;
-            As[buf][kk][li] = (gi < a.lines && gk < K) ? a.ptr[gi * a.ls + gk * a.ps] : 0.0;
-            int lj, kj;
-            if (b.ls == 1) { lj = e % kT; kj = e / kT; }
-            else { kj = e % kKT; lj = e / kKT; }
-            int64_t gj = j0 + lj, gk2 = k0 + kj;
-            Bs[buf][kj][lj] = (gj < b.lines && gk2 < K) ? b.ptr[gj * b.ls + gk2 * b.ps] : 0.0;
-        }
-    };
+            for (int q = 0; q < 4; ++q) {
+                int e = tid + q * 256;
+                int li, kk;
+                if (a.ls == 1) { li = e % kT; kk = e / kT; }
+                else { kk = e % kKT; li = e / kKT; }
+                int64_t gi = i0 + li, gk = k0 + kk;
+                As[buf][kk][li] = (gi < a.lines && gk < K) ? a.ptr[gi * a.ls + gk * a.ps] : 0.0;
+                int lj, kj;
+                if (b.ls == 1) { lj = e % kT; kj = e / kT; }
+                else { kj = e % kKT; lj = e / kKT; }
+                int64_t gj = j0 + lj, gk2 = k0 + kj;
+                Bs[buf][kj][lj] = (gj < b.lines && gk2 < K) ? b.ptr[gj * b.ls + gk2 * b.ps] : 0.0;
+            }
+        };
 
-    double acc[4][4];
+        double acc[4][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
 
-    const int64_t nk = (K + kKT - 1) / kKT;
-    if (nk > 0) load(0, 0);
-    __syncthreads();
-    for (int64_t t = 0; t < nk; ++t) {
-        const int buf = int(t & 1);
-        if (t + 1 < nk) load(buf ^ 1, (t + 1) * kKT);
-        const int kmax = (K - t * kKT) < kKT ? int(K - t * kKT) : kKT;
-        for (int kk = 0; kk < kmax; ++kk) {  // ascending k, never reordered
-            double av[4], bv[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) av[r] = As[buf][kk][tx + 16 * r];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) bv[c] = Bs[buf][kk][ty + 16 * c];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int c = 0; c < 4; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(av[r], bv[c]));
-        }
+        const int64_t nk = (K + kKT - 1) / kKT;
+        if (nk > 0) load(0, 0);
         __syncthreads();
+        for (int64_t t = 0; t < nk; ++t) {
+            const int buf = int(t & 1);
+            if (t + 1 < nk) load(buf ^ 1, (t + 1) * kKT);
+            const int kmax = (K - t * kKT) < kKT ? int(K - t * kKT) : kKT;
+            for (int kk = 0; kk < kmax; ++kk) {  // ascending k, never reordered
+                double av[4], bv[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) av[r] = As[buf][kk][tx + 16 * r];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bv[c] = Bs[buf][kk][ty + 16 * c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(av[r], bv[c]));
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int64_t j = j0 + ty + 16 * c;
+            if (j >= b.lines) continue;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int64_t i = i0 + tx + 16 * r;
+                if (i >= a.lines) continue;
+                double v = __dmul_rn(alpha, acc[r][c]);
+                if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c_in[i + j * ldc_in]));
+                c_out[i + j * ldc] = v;
+            }
+        }
+        __syncthreads();  // the next tile's first load reuses buffer 0
     }
+}
+
+// ---- fast flavour: DMMA ---------------------------------------------------------------
+constexpr int kDT = 128;       // CTA tile (lines of A) x (lines of B)
+#ifndef ADPB200_DMMA_DK
+#define ADPB200_DMMA_DK 16
+#endif
+#ifndef ADPB200_DMMA_STAGES
+#define ADPB200_DMMA_STAGES 3
+#endif
+constexpr int kDK = ADPB200_DMMA_DK;  // k per stage
+constexpr int kDStages = ADPB200_DMMA_STAGES;
+constexpr int kPadL = kDT + 4;  // [k][line] rows: 132 doubles (== 4 mod 16: conflict-free fragment reads)
+constexpr int kPadK = kDK + 4;  // [line][k] rows: kDK + 4 doubles (== 4 mod 16)
+constexpr int kOpDoubles = (kDK * kPadL > kDT * kPadK) ? kDK * kPadL : kDT * kPadK;  // one operand, one stage
+constexpr int kGroupTiles = 8;  // raster: CTA tiles along m per group (B tiles stay in L2)
+constexpr size_t kDmmaSmem = size_t(kDStages) * 2 * kOpDoubles * sizeof(double);
+
+__device__ __forceinline__ void cp_async8(uint32_t dst, const double* src, bool valid) {
+    // src-size 0 zero-fills (out-of-range rows / k)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// One operand's tile (128 lines x 16 k) of one stage: `line_major` layout S[k][line]
+// when the lines are contiguous in memory (ls == 1), else S[line][k].
+template <bool kLineMajor>
+struct OpTile {
+    static constexpr bool line_major = kLineMajor;
+    const double* ptr;
+    int64_t lines, len, ls, ps;
+    __device__ __forceinline__ void load(uint32_t sdst, int64_t l0, int64_t k0, int tid) const {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-        const int64_t j = j0 + ty + 16 * c;
-        if (j >= b.lines) continue;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const int64_t i = i0 + tx + 16 * r;
-            if (i >= a.lines) continue;
-            double v = __dmul_rn(alpha, acc[r][c]);
-            if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c_in[i + j * ldc_in]));
-            c_out[i + j * ldc] = v;
+        for (int q = 0; q < kDT * kDK / 256; ++q) {
+            const int e = tid + q * 256;
+            int li, kk;
+            uint32_t off;
+            if (line_major) {
+                li = e % kDT;
+                kk = e / kDT;
+                off = uint32_t(kk * kPadL + li);
+            } else {
+                kk = e % kDK;
+                li = e / kDK;
+                off = uint32_t(li * kPadK + kk);
+            }
+            const int64_t gl = l0 + li, gk = k0 + kk;
+            const bool ok = gl < lines && gk < len;
+            cp_async8(sdst + off * 8u, ok ? ptr + gl * ls + gk * ps : ptr, ok);
         }
     }
+    __device__ __forceinline__ double frag(const double* s, int line, int k) const {
+        return line_major ? s[k * kPadL + line] : s[line * kPadK + k];
+    }
+};
+
+template <bool kAL, bool kBL>
+__global__ void __launch_bounds__(256, 1) dmma_kernel(LineView a, LineView b, double alpha, double beta,
+                                                      const double* __restrict__ c_in, int64_t ldc_in,
+                                                      double* __restrict__ c_out, int64_t ldc, const Plan* plan) {
+    if (plan && plan->path != ADPB200_PATH_NATIVE) return;
+    extern __shared__ __align__(16) double dsm[];
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int wm = warp % 2, wn = warp / 2;  // warp tile: lines [64 wm, +64) of A x [32 wn, +32) of B
+    const OpTile<kAL> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
+    const OpTile<kBL> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+    const int64_t K = a.len;
+    const int64_t tiles_m = (a.lines + kDT - 1) / kDT, tiles_n = (b.lines + kDT - 1) / kDT;
+    const int64_t nk = (K + kDK - 1) / kDK;
+    const uint32_t s0 = uint32_t(__cvta_generic_to_shared(dsm));
+    auto sa = [&](int st) { return dsm + size_t(st) * 2 * kOpDoubles; };
+    auto sb = [&](int st) { return dsm + size_t(st) * 2 * kOpDoubles + kOpDoubles; };
+    auto sa_u = [&](int st) { return s0 + uint32_t(st) * 2u * kOpDoubles * 8u; };
+    auto sb_u = [&](int st) { return s0 + (uint32_t(st) * 2u + 1u) * kOpDoubles * 8u; };
+    const int fr = lane / 4, fk = lane % 4;  // fragment row (line) and k of this lane
+
+    for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
+        // grouped raster: kGroupTiles m-tiles share each B tile while it is L2-resident
+        const int64_t group = int64_t(kGroupTiles) * tiles_n;
+        const int64_t first_m = (tile / group) * kGroupTiles;
+        const int64_t gm = tiles_m - first_m < kGroupTiles ? tiles_m - first_m : kGroupTiles;
+        const int64_t local = tile % group;
+        const int64_t i0 = (first_m + local % gm) * kDT, j0 = (local / gm) * kDT;
+
+        double acc[8][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+#pragma unroll
+        for (int st = 0; st < kDStages - 1; ++st) {
+            if (st < nk) {
+                ta.load(sa_u(st), i0, int64_t(st) * kDK, tid);
+                tb.load(sb_u(st), j0, int64_t(st) * kDK, tid);
+            }
+            cp_async_commit();
+        }
+        for (int64_t t = 0; t < nk; ++t) {
+            cp_async_wait<kDStages - 2>();
+            __syncthreads();  // stage t visible to all; stage t-1 fully consumed
+            const int64_t tn = t + kDStages - 1;
+            if (tn < nk) {
+                const int st = int(tn % kDStages);
+                ta.load(sa_u(st), i0, tn * kDK, tid);
+                tb.load(sb_u(st), j0, tn * kDK, tid);
+            }
+            cp_async_commit();
+            const double* As = sa(int(t % kDStages));
+            const double* Bs = sb(int(t % kDStages));
+#pragma unroll
+            for (int kk = 0; kk < kDK; kk += 4) {
+                double af[8], bf[4];
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) af[mi] = ta.frag(As, wm * 64 + mi * 8 + fr, kk + fk);
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) bf[ni] = tb.frag(Bs, wn * 32 + ni * 8 + fr, kk + fk);
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();  // the next tile's prologue overwrites stages 0..1
+        // C fragment: line i = 8 mi + lane/4 of A, lines j = 8 ni + 2 (lane%4) + {0, 1} of B
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = j0 + wn * 32 + ni * 8 + 2 * fk + h;
+                if (j >= b.lines) continue;
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) {
+                    const int64_t i = i0 + wm * 64 + mi * 8 + fr;
+                    if (i >= a.lines) continue;
+                    double v = __dmul_rn(alpha, acc[mi][ni][h]);
+                    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c_in[i + j * ldc_in]));
+                    c_out[i + j * ldc] = v;
+                }
+            }
+    }
+}
+
+int resident_grid(const void* fn, int threads, size_t smem, int64_t tiles) {
+    static int sms = 0;
+    if (!sms) sms = num_sms();
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int64_t cap = int64_t(sms) * per_sm;
+    return int(tiles < cap ? tiles : cap);
 }
 
 }  // namespace
 
 void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
-                   int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch) {
+                   int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch,
+                   int flavour) {
     if (a.lines == 0 || b.lines == 0) return;
-    dim3 grid((unsigned)((a.lines + kT - 1) / kT), (unsigned)((b.lines + kT - 1) / kT));
-    native_kernel<<<grid, 256, 0, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+    if (flavour == ADPB200_FALLBACK_FAST) {
+        // operand layouts in shared memory follow the contiguous direction in HBM
+        using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
+                            const Plan*);
+        static const Fn fns[4] = {dmma_kernel<false, false>, dmma_kernel<false, true>, dmma_kernel<true, false>,
+                                  dmma_kernel<true, true>};
+        static bool attr = false;
+        if (!attr) {
+            for (Fn f : fns)
+                cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kDmmaSmem));
+            attr = true;
+        }
+        const Fn fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
+        const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
+        const int grid = resident_grid(reinterpret_cast<const void*>(fn), 256, kDmmaSmem, tiles);
+        fn<<<grid, 256, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+    } else {
+        const int64_t tiles = ((a.lines + kT - 1) / kT) * ((b.lines + kT - 1) / kT);
+        const int grid = resident_grid(reinterpret_cast<const void*>(native_kernel), 256, 0, tiles);
+        native_kernel<<<grid, 256, 0, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+    }
     ++*nlaunch;
 }
 

@@ -1,5 +1,5 @@
-// Round-trips a matrix file through adpb200_io.hpp (the C++ façade's copy of
-// the reference's matrix formats): io_check <in> <out> reads <in> (either
+// Round-trips a matrix file through adpb200_io.hpp (the C++ façade's reader
+// and writer of the reference's matrix formats): io_check <in> <out> reads <in> (either
 // format) and writes it to <out> (format by extension).
 #include <cstdio>
 #include <exception>

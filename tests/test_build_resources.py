@@ -1,0 +1,48 @@
+"""CPU: resource facts of the built kernels that the launch code relies on.
+
+igemm_kernel<NB> splits its register file by warpgroup with setmaxnreg
+(csrc/igemm.cu: 40 per thread for the producer/MMA/allocator warpgroup, 232 for
+the two epilogue warpgroups). setmaxnreg.inc blocks until the CTA's pool has the
+registers, and the pool is what the launch reserved: 384 threads x the kernel's
+register count. The split is sized for 168; a build that comes out different
+would hang the epilogue (launch_igemm refuses it at run time). This pins it at
+build time, together with the SASS evidence for the tensor-core paths."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+LIB = os.path.join(ROOT, "paper_2511_13778_b200", "libadpb200.so")
+
+
+def _cuobjdump(*args):
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(LIB) or not os.path.exists(exe):
+        pytest.skip("library or cuobjdump missing")
+    return subprocess.run([exe, *args, LIB], capture_output=True, text=True, check=True).stdout
+
+
+def test_igemm_register_count_matches_the_split():
+    out = _cuobjdump("--dump-resource-usage")
+    regs = {}
+    lines = out.splitlines()
+    for i, line in enumerate(lines):
+        m = re.search(r"igemm_kernel(?:I|<)L?i?(\d+)", line)
+        if m and "Function" in line:
+            r = re.search(r"REG:(\d+)", lines[i + 1] if i + 1 < len(lines) else "")
+            if r:
+                regs[int(m.group(1))] = int(r.group(1))
+    assert set(regs) == {8, 16, 32, 48, 64}, regs
+    assert all(v == 168 for v in regs.values()), regs
+
+
+def test_sass_has_tensor_core_paths():
+    sass = _cuobjdump("-sass")
+    assert "UTCIMMA" in sass          # tcgen05.mma kind::i8 (slice GEMM)
+    assert "UTMALDG" in sass          # TMA loads
+    assert "USETMAXREG" in sass       # warpgroup register split
+    assert re.search(r"\bDMMA\b", sass)  # FP64 tensor cores (fast fallback)

@@ -95,3 +95,31 @@ def test_shortest_decimal_matches_to_chars_on_random_magnitudes(ref, tmp_path):
     matrix_io.write_matrix(ours, a)
     ref.write_matrix(theirs, a)
     assert open(ours, "rb").read() == open(theirs, "rb").read()
+
+
+def test_cpp_header_rejects_malformed_files(tmp_path):
+    exe = str(tmp_path / "io_check")
+    r = subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-I",
+                        "/usr/local/cuda/include", os.path.join(ROOT, "tests", "cpp", "io_check.cpp"), "-o", exe],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    p = tmp_path / "bad.mtx"
+    cases = [(b"%%MatrixMarket matrix coordinate real general\n1 1\n1\n", "unsupported header"),
+             (b"%%MatrixMarket matrix array real general\n2 2\n1\n2\n", "not enough values"),
+             (b"%%MatrixMarket matrix array real general\n1 1\nabc\n", "bad value"),
+             (b"%%MatrixMarket matrix array real general\n% only comments\n", "missing dimensions"),
+             (b"%%MatrixMarket matrix array real general\n2 x\n", "bad dimension line"),
+             (b"ADPM\x02\x00\x00\x00", "unsupported version"),
+             (b"ADPM\x01\x00\x00\x00" + (1).to_bytes(8, "little"), "truncated header"),
+             (b"ADPM\x01\x00\x00\x00" + (1).to_bytes(8, "little") + (1).to_bytes(8, "little"), "truncated payload"),
+             (b"ADPM\x01\x00\x00\x00" + (1 << 20).to_bytes(8, "little") + (1 << 10).to_bytes(8, "little"),
+              "out of range")]
+    for body, msg in cases:
+        p.write_bytes(body)
+        r = subprocess.run([exe, str(p), str(tmp_path / "o.adpm")], capture_output=True, text=True)
+        assert r.returncode == 3 and msg in r.stderr, (body, r.stderr)
+    # CRLF, blank lines, a '+' sign and upper-case banner tokens are accepted
+    p.write_bytes(b"%%MatrixMarket MATRIX Array REAL General\r\n\r\n% c\r\n2 1\r\n+1.5\r\n-2e-3\r\n")
+    r = subprocess.run([exe, str(p), str(tmp_path / "o.mtx")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert (tmp_path / "o.mtx").read_bytes() == b"%%MatrixMarket matrix array real general\n2 1\n1.5\n-0.002\n"
