@@ -55,6 +55,16 @@ def parse():
                         "peer's planes while the GEMM of the previous rank's columns runs (phase 7 per rank). "
                         "fused / pull are not yet timed on an NVLink node")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
+    p.add_argument("--soak", type=float, default=2.0,
+                   help="seconds of untimed steps between the warm-up and the timed region, so the timed region "
+                        "runs at the power-capped steady state (value_burst: 5 steps right after the warm-up)")
+    p.add_argument("--c4-size", type=int, default=32768,
+                   help="strong_c4 side measurement: m = n = k (BASELINE config 4 is 32768; smaller only for "
+                        "plumbing checks); 0 skips it")
+    p.add_argument("--c4-dist", choices=["rows", "allgather"], default="rows",
+                   help="strong_c4 partition: rows = every rank holds B and slices it (one 8-byte stream-ordered "
+                        "max-allreduce per call, no host sync); allgather = B column slabs, slice planes "
+                        "all-gathered over NCCL")
     p.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline")
     return p.parse_args()
 
@@ -219,6 +229,59 @@ def cpu_baseline(A_host_rows, B_host, k):
 
 
 # ---------------------------------------------------------------------------------
+def strong_c4(args, adp, grading, dev, world, rank, handle, timed, dist):
+    """BASELINE config 4 (m = n = k = 32768, U[-1,1], coarsened ESC -> s = 8): the
+    row-partitioned call over the N ranks, and the same problem on one GPU (each
+    rank alone, max over ranks); speedup = single / partitioned."""
+    import torch
+
+    from paper_2511_13778_b200.dist import cols_of, dgemm_dist, dgemm_rows, rows_of
+
+    n = k = mg = args.c4_size
+    cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET)
+    flops = 2.0 * mg * n * k
+    out = {"m": mg, "n": n, "k": k, "unit": "TFLOP/s", "data": "U[-1,1], gen_uniform_rect seeds 1, 2",
+           "partition": args.c4_dist if world > 1 else "single GPU"}
+    torch.cuda.empty_cache()
+    # one GPU, the whole problem (column-major NN)
+    At = grading.gen_uniform_rect(k, mg, 1, -1.0, 1.0, dev.index)
+    Bt = grading.gen_uniform_rect(n, k, 2, -1.0, 1.0, dev.index)
+    Ct = torch.empty((n, mg), device=dev, dtype=torch.float64)
+
+    def one():
+        adp.dgemm("N", "N", mg, n, k, 1.0, At, mg, Bt, k, 0.0, Ct, mg, cfg, handle)
+
+    t1 = timed(one, 2, 1)
+    _, tr = adp.adp_gemm(At.t(), Bt.t(), config=cfg, handle=handle)  # the decision of this problem
+    out.update({"one_gpu_value": flops / (t1 * 1e-3) / 1e12, "one_gpu_ms": t1, "slices": tr.slices,
+                "esc_bits": tr.esc_bits, "pairs": tr.pairs})
+    del Ct
+    if world == 1:
+        out["value"], out["ms_per_step"], out["speedup_vs_1gpu"] = out["one_gpu_value"], t1, 1.0
+        return out
+    r0, r1 = rows_of(rank, world, mg)
+    ml = r1 - r0
+    Al = At[:, r0:r1].contiguous()                 # this rank's rows of A (column-major, lda = ml)
+    Cl = torch.empty((n, ml), device=dev, dtype=torch.float64)
+    if args.c4_dist == "rows":
+        xchg = torch.zeros(2, dtype=torch.int32, device=dev)
+
+        def part():
+            xchg.zero_()
+            dgemm_rows("N", "N", mg, ml, n, k, 1.0, Al, ml, Bt, k, 0.0, Cl, ml, cfg, handle, xchg=xchg)
+    else:
+        c0, c1 = cols_of(rank, world, n)
+        Bs = Bt[c0:c1].contiguous()
+
+        def part():
+            dgemm_dist("N", mg, ml, n, k, 1.0, Al, ml, Bs, 0.0, Cl, ml, cfg, handle)
+    del At
+    tN = timed(part, 3, 1)
+    out.update({"value": flops / (tN * 1e-3) / 1e12, "ms_per_step": tN, "speedup_vs_1gpu": t1 / tN,
+                "rows_per_rank": ml})
+    return out
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -323,9 +386,19 @@ def main():
     trace = adp.AdpTrace.from_c(_lib.Trace.from_buffer_copy(trace_buf.cpu().numpy().tobytes()))
     for _ in range(args.warmup):
         step()
+    # burst: 5 steps right after the warm-up (clocks not yet power-capped)
+    burst_ms = timed(step, 5, 0)
+    # soak to the power-capped steady state right before the timed region, with no idle gap
+    # in between (same step count on every rank); nvidia-smi starts sampling before it
     sampler = ClockSampler(dev.index)
     sampler.start()
-    time.sleep(1.0)
+    n_soak = 0
+    if args.soak > 0:
+        n_soak = max(1, int(args.soak * 1e3 / max(burst_ms, 1e-3)))
+        for _ in range(n_soak):
+            step()
+    else:
+        time.sleep(0.5)
     barrier()
     launches0 = handle.launches()
     handle.profile_enable(args.steps * (4 if world > 1 else 1))  # the dist path is 4 pipeline calls
@@ -513,8 +586,52 @@ def main():
         torch.cuda.empty_cache()
         extra["rectangular"] = rect
 
+        # ---- BASELINE config 3's fallback: one NaN in A sends the auto-mode call to the
+        # native FP64 GEMM on the device (no host sync); both flavours, beside cuBLAS ------
+        An = At.clone()
+        An.view(-1)[12345] = float("nan")
+        fb = {}
+        for flav in ("reference", "fast"):
+            fcfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET, fallback=flav)
+            trf = torch.zeros_like(trace_buf)
+            step(fcfg, An, Bt, Ct, trf)
+            torch.cuda.synchronize()
+            tf = adp.AdpTrace.from_c(_lib.Trace.from_buffer_copy(trf.cpu().numpy().tobytes()))
+            f_ms = timed(lambda: step(fcfg, An, Bt, Ct), 3, 1)
+            fb[flav] = {"value": flops_global / (f_ms * 1e-3) / 1e12, "path": tf.path, "ms_per_step": f_ms}
+        del An
+        fb["reference"]["kernel"] = "native_kernel: SIMT FP64, ascending k, no FMA (bitwise native_gemm)"
+        fb["fast"]["kernel"] = "dmma_kernel: FP64 tensor cores (DMMA m8n8k4), opt-in"
+        fb["unit"] = "TFLOP/s"
+        fb["fast_vs_cublas"] = fb["fast"]["value"] / world / extra["native_fp64"]["value"]
+        extra["fallback_tflops"] = fb
+
+    # ---- ESC (K2) against its own roofline: the DPX add+max rate (tools/dpx_peak.cu) --------
+    esc_ms = stage_ms.get("esc", 0.0)
+    if esc_ms > 0 and trace.path == "emulated":
+        blocks = (k + 255) // 256  # esc_block_len 256
+        instr = float(m) * n * blocks  # VIADDMNMX.S16x2: 2 add+max per (i, j, block), 2 j per instruction
+        esc_rf = {"bound": "dpx", "kernel": "esc_kernel (VIADDMNMX.S16x2 max-plus over exponent blocks)",
+                  "achieved": instr / (esc_ms * 1e-3), "unit": "instr/s", "instr_per_launch": instr}
+        try:
+            with open(os.path.join(ROOT, "profiles", "r02_dpx_peak.json")) as f:
+                dp = json.load(f)
+            esc_rf["peak"] = float(dp["instr_per_s"])
+            esc_rf["frac"] = esc_rf["achieved"] / esc_rf["peak"]
+            esc_rf["peak_source"] = "measured: tools/dpx_peak.cu (profiles/r02_dpx_peak.json)"
+            if load_clk:
+                esc_rf["frac_at_load_clock"] = esc_rf["achieved"] / (dp["instr_per_clk_per_sm"] * 148 * load_clk * 1e6)
+        except (OSError, KeyError, ValueError):
+            pass
+        extra["esc_roofline"] = esc_rf
+
+    # ---- BASELINE config 4 strong scaling: 32768^3 U[-1,1] row-partitioned over the N
+    # ranks, against the same problem on one GPU (every rank runs it alone, max over ranks) --
+    if not args.quick and not c4 and args.c4_size > 0:
+        extra["strong_c4"] = strong_c4(args, adp, grading, dev, world, rank, handle, timed, dist)
+
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         try:
             rows = At[:, :256].t().contiguous().cpu().numpy()        # 256 x k block of A (row-major)
             cols = Bt[:1024, :].t().contiguous().cpu().numpy()       # k x 1024 block of B (row-major)
@@ -558,6 +675,9 @@ def main():
             line["max_rel_err"] = extra["accuracy"]["max_rel_err"]
         if "native_fp64" in extra:
             line["speedup_vs_native_fp64"] = value / world / extra["native_fp64"]["value"]
+        line["value_burst"] = flops_global / (burst_ms * 1e-3) / 1e12
+        line["config"]["soak"] = (f"{n_soak} untimed steps (~{args.soak:g} s) before the timed region: value is the "
+                                  "power-capped steady state; value_burst = 5 steps right after the warm-up")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

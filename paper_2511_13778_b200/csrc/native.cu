@@ -115,6 +115,10 @@ constexpr int kDStages = ADPB200_DMMA_STAGES;
 constexpr int kPadL = kDT + 4;  // [k][line] rows: 132 doubles (== 4 mod 16: conflict-free fragment reads)
 constexpr int kPadK = kDK + 4;  // [line][k] rows: kDK + 4 doubles (== 4 mod 16)
 constexpr int kOpDoubles = (kDK * kPadL > kDT * kPadK) ? kDK * kPadL : kDT * kPadK;  // one operand, one stage
+#ifndef ADPB200_DMMA_WARPS
+#define ADPB200_DMMA_WARPS 8
+#endif
+constexpr int kDmmaWarps = ADPB200_DMMA_WARPS;
 constexpr int kGroupTiles = 8;  // raster: CTA tiles along m per group (B tiles stay in L2)
 constexpr size_t kDmmaSmem = size_t(kDStages) * 2 * kOpDoubles * sizeof(double);
 
@@ -136,15 +140,15 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // One operand's tile (128 lines x 16 k) of one stage: `line_major` layout S[k][line]
 // when the lines are contiguous in memory (ls == 1), else S[line][k].
-template <bool kLineMajor>
+template <bool kLineMajor, int kThreads>
 struct OpTile {
     static constexpr bool line_major = kLineMajor;
     const double* ptr;
     int64_t lines, len, ls, ps;
     __device__ __forceinline__ void load(uint32_t sdst, int64_t l0, int64_t k0, int tid) const {
 #pragma unroll
-        for (int q = 0; q < kDT * kDK / 256; ++q) {
-            const int e = tid + q * 256;
+        for (int q = 0; q < kDT * kDK / kThreads; ++q) {
+            const int e = tid + q * kThreads;
             int li, kk;
             uint32_t off;
             if (line_major) {
@@ -166,16 +170,22 @@ struct OpTile {
     }
 };
 
-template <bool kAL, bool kBL>
-__global__ void __launch_bounds__(256, 1) dmma_kernel(LineView a, LineView b, double alpha, double beta,
-                                                      const double* __restrict__ c_in, int64_t ldc_in,
-                                                      double* __restrict__ c_out, int64_t ldc, const Plan* plan) {
+// kWarps = 8: warp tiles of 64 x 32 (2 x 4 warps, 2 per scheduler); kWarps = 16:
+// 32 x 32 (4 x 4 warps, 4 per scheduler, half the accumulator registers each).
+template <bool kAL, bool kBL, int kWarps>
+__global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineView b, double alpha, double beta,
+                                                              const double* __restrict__ c_in, int64_t ldc_in,
+                                                              double* __restrict__ c_out, int64_t ldc,
+                                                              const Plan* plan) {
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
+    constexpr int kThreads = kWarps * 32;
+    constexpr int kWarpsM = kWarps == 8 ? 2 : 4, kWarpsN = 4;
+    constexpr int kMI = kDT / kWarpsM / 8, kNI = kDT / kWarpsN / 8;  // 8x8 fragments per warp
     extern __shared__ __align__(16) double dsm[];
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    const int wm = warp % 2, wn = warp / 2;  // warp tile: lines [64 wm, +64) of A x [32 wn, +32) of B
-    const OpTile<kAL> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
-    const OpTile<kBL> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+    const int wm = warp % kWarpsM, wn = warp / kWarpsM;  // warp tile: lines [8 kMI wm, +8 kMI) of A x [8 kNI wn, +8 kNI) of B
+    const OpTile<kAL, kThreads> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
+    const OpTile<kBL, kThreads> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
     const int64_t K = a.len;
     const int64_t tiles_m = (a.lines + kDT - 1) / kDT, tiles_n = (b.lines + kDT - 1) / kDT;
     const int64_t nk = (K + kDK - 1) / kDK;
@@ -194,11 +204,11 @@ __global__ void __launch_bounds__(256, 1) dmma_kernel(LineView a, LineView b, do
         const int64_t local = tile % group;
         const int64_t i0 = (first_m + local % gm) * kDT, j0 = (local / gm) * kDT;
 
-        double acc[8][4][2];
+        double acc[kMI][kNI][2];
 #pragma unroll
-        for (int mi = 0; mi < 8; ++mi)
+        for (int mi = 0; mi < kMI; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+            for (int ni = 0; ni < kNI; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
 #pragma unroll
         for (int st = 0; st < kDStages - 1; ++st) {
@@ -222,29 +232,29 @@ __global__ void __launch_bounds__(256, 1) dmma_kernel(LineView a, LineView b, do
             const double* Bs = sb(int(t % kDStages));
 #pragma unroll
             for (int kk = 0; kk < kDK; kk += 4) {
-                double af[8], bf[4];
+                double af[kMI], bf[kNI];
 #pragma unroll
-                for (int mi = 0; mi < 8; ++mi) af[mi] = ta.frag(As, wm * 64 + mi * 8 + fr, kk + fk);
+                for (int mi = 0; mi < kMI; ++mi) af[mi] = ta.frag(As, wm * kMI * 8 + mi * 8 + fr, kk + fk);
 #pragma unroll
-                for (int ni = 0; ni < 4; ++ni) bf[ni] = tb.frag(Bs, wn * 32 + ni * 8 + fr, kk + fk);
+                for (int ni = 0; ni < kNI; ++ni) bf[ni] = tb.frag(Bs, wn * kNI * 8 + ni * 8 + fr, kk + fk);
 #pragma unroll
-                for (int mi = 0; mi < 8; ++mi)
+                for (int mi = 0; mi < kMI; ++mi)
 #pragma unroll
-                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+                    for (int ni = 0; ni < kNI; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
             }
         }
         cp_async_wait<0>();
         __syncthreads();  // the next tile's prologue overwrites stages 0..1
         // C fragment: line i = 8 mi + lane/4 of A, lines j = 8 ni + 2 (lane%4) + {0, 1} of B
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni)
+        for (int ni = 0; ni < kNI; ++ni)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t j = j0 + wn * 32 + ni * 8 + 2 * fk + h;
+                const int64_t j = j0 + wn * kNI * 8 + ni * 8 + 2 * fk + h;
                 if (j >= b.lines) continue;
 #pragma unroll
-                for (int mi = 0; mi < 8; ++mi) {
-                    const int64_t i = i0 + wm * 64 + mi * 8 + fr;
+                for (int mi = 0; mi < kMI; ++mi) {
+                    const int64_t i = i0 + wm * kMI * 8 + mi * 8 + fr;
                     if (i >= a.lines) continue;
                     double v = __dmul_rn(alpha, acc[mi][ni][h]);
                     if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c_in[i + j * ldc_in]));
@@ -274,8 +284,8 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         // operand layouts in shared memory follow the contiguous direction in HBM
         using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
                             const Plan*);
-        static const Fn fns[4] = {dmma_kernel<false, false>, dmma_kernel<false, true>, dmma_kernel<true, false>,
-                                  dmma_kernel<true, true>};
+        static const Fn fns[4] = {dmma_kernel<false, false, kDmmaWarps>, dmma_kernel<false, true, kDmmaWarps>,
+                                  dmma_kernel<true, false, kDmmaWarps>, dmma_kernel<true, true, kDmmaWarps>};
         static bool attr = false;
         if (!attr) {
             for (Fn f : fns)
@@ -285,8 +295,8 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         }
         const Fn fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
         const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
-        const int grid = resident_grid(reinterpret_cast<const void*>(fn), 256, kDmmaSmem, tiles);
-        fn<<<grid, 256, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+        const int grid = resident_grid(reinterpret_cast<const void*>(fn), kDmmaWarps * 32, kDmmaSmem, tiles);
+        fn<<<grid, kDmmaWarps * 32, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
     } else {
         const int64_t tiles = ((a.lines + kT - 1) / kT) * ((b.lines + kT - 1) / kT);
         const int grid = resident_grid(reinterpret_cast<const void*>(native_kernel), 256, 0, tiles);

@@ -83,6 +83,31 @@ __device__ __forceinline__ typename Word<S>::T slice_word(uint64_t bits, int E) 
     return U + C;
 }
 
+// The same words for 16 elements through the FP64 pipe: U = floor(v * 2^p),
+// p = 7 + 8(S-1) - E, is one exact multiply by a power of two (|v 2^p| < 2^(8S-2)
+// cannot overflow, and p >= 0 cannot lose bits) and one round-toward--inf
+// conversion. Zeros (either sign) give U = 0 like the integer path. Taken when
+// 0 <= p <= 1023 (lines whose maximum exponent is below 8S, i.e. every line of
+// data scaled anywhere near 1) and all 16 elements are finite; otherwise the
+// caller runs slice_word.
+template <int S>
+__device__ __forceinline__ bool fast_words(const uint64_t (&bits)[16], int E, uint64_t (&X)[16]) {
+    // p >= 0: v 2^p is exact for every finite v (normal or not, no underflow), so
+    // the only per-element test is "finite": the largest exponent field < 2047
+    const int p = 7 + 8 * (S - 1) - E;
+    if (p < 0 || p > 1023) return false;
+    uint32_t exmax = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) exmax = max(exmax, uint32_t(bits[q] >> 32) & 0x7ff00000u);
+    if (exmax == 0x7ff00000u) return false;
+    const double sc = __longlong_as_double(int64_t(p + 1023) << 52);
+    const uint64_t C = slice_const<S>();
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        X[q] = uint64_t(__double2ll_rd(__dmul_rn(__longlong_as_double(int64_t(bits[q])), sc))) + C;
+    return true;
+}
+
 // byte j of X as stored in plane d = S-1-j
 template <int S>
 __device__ __forceinline__ uint32_t plane_byte(typename Word<S>::T X, int d) {
@@ -90,10 +115,10 @@ __device__ __forceinline__ uint32_t plane_byte(typename Word<S>::T X, int d) {
     return d == 0 ? b : (b ^ 0x80u);
 }
 
-// Plane d's bytes of 8 consecutive elements, packed into two words with
+// Plane d's bytes of 8 consecutive elements X[0..7], packed into two words with
 // byte permutes (d is a compile-time constant after unrolling).
 template <int S>
-__device__ __forceinline__ void pack_plane(const typename Word<S>::T (&X)[8], int d, uint32_t& lo, uint32_t& hi) {
+__device__ __forceinline__ void pack_plane(const typename Word<S>::T* X, int d, uint32_t& lo, uint32_t& hi) {
     if constexpr (S <= 8) {
         const int j = S - 1 - d;  // byte of X
         uint32_t w[8];
@@ -113,6 +138,40 @@ __device__ __forceinline__ void pack_plane(const typename Word<S>::T (&X)[8], in
         for (int q = 0; q < 4; ++q) {
             lo |= plane_byte<S>(X[q], d) << (8 * q);
             hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
+        }
+    }
+}
+
+// Every plane's bytes of 8 elements X[0..7] (S <= 8) into w[d][o], w[d][o + 1].
+// Bytes j and j + 1 (j even) of X live in the same 32-bit half, so one byte
+// permute per element pair serves two planes: t = (x_j, y_j, x_j+1, y_j+1), then
+// two permutes per plane merge the four pairs (0.5 permutes per plane byte).
+template <int S>
+__device__ __forceinline__ void pack_planes(const uint64_t* X, uint32_t (&w)[S][4], int o) {
+#pragma unroll
+    for (int j = 0; j < S; j += 2) {
+        uint32_t h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) h[q] = j < 4 ? uint32_t(X[q]) : uint32_t(X[q] >> 32);
+        const uint32_t b = uint32_t(j & 3);
+        const int d = S - 1 - j;  // plane of byte j; byte j + 1 is plane d - 1
+        if (j + 1 < S) {
+            const uint32_t sel = b | ((4 + b) << 4) | ((b + 1) << 8) | ((5 + b) << 12);
+            const uint32_t t0 = __byte_perm(h[0], h[1], sel), t1 = __byte_perm(h[2], h[3], sel);
+            const uint32_t t2 = __byte_perm(h[4], h[5], sel), t3 = __byte_perm(h[6], h[7], sel);
+            w[d][o] = __byte_perm(t0, t1, 0x5410);
+            w[d][o + 1] = __byte_perm(t2, t3, 0x5410);
+            const uint32_t f = d - 1 != 0 ? 0x80808080u : 0u;  // sub-leading digits: byte ^ 0x80
+            w[d - 1][o] = __byte_perm(t0, t1, 0x7632) ^ f;
+            w[d - 1][o + 1] = __byte_perm(t2, t3, 0x7632) ^ f;
+        } else {  // the top byte alone (odd S): the lead digit, plane 0
+            const uint32_t sel = b | ((4 + b) << 4);
+            w[d][o] = __byte_perm(__byte_perm(h[0], h[1], sel), __byte_perm(h[2], h[3], sel), 0x5410);
+            w[d][o + 1] = __byte_perm(__byte_perm(h[4], h[5], sel), __byte_perm(h[6], h[7], sel), 0x5410);
+        }
+        if (d != 0) {
+            w[d][o] ^= 0x80808080u;
+            w[d][o + 1] ^= 0x80808080u;
         }
     }
 }
@@ -176,8 +235,7 @@ struct SliceArgs {
 
 // Certified-ESC indicator bytes of 8 elements: 1 where the element is finite,
 // nonzero and its effective exponent is within delta of the line maximum.
-__device__ __forceinline__ void indicator_bytes(const uint64_t (&bits)[8], int lm, int delta, uint32_t& lo,
-                                                uint32_t& hi) {
+__device__ __forceinline__ void indicator_bytes(const uint64_t* bits, int lm, int delta, uint32_t& lo, uint32_t& hi) {
     lo = hi = 0;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -207,224 +265,337 @@ __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
     return true;
 }
 
-// ---- lines contiguous (ps == 1): a thread slices 8 consecutive positions ----------
-template <int S, bool kVec>
-__device__ __forceinline__ void rows_body(const SliceArgs& a, int nsl, int64_t groups, int64_t span) {
-    // A warp covers 4 lines x 64 positions (lane = 8 x line + group): per plane it
-    // stores two full 128-byte rows of the blocked layout (4 adjacent line slots x
-    // 32 B) and reads 4 runs of 512 B. Fewer than 4 lines: one line per warp.
-    const bool quad = a.v.lines >= 4;
-    const int64_t gw = (groups + 7) / 8;
-    const int64_t tasks = quad ? (a.v.lines + 3) / 4 * gw * 32 : a.v.lines * groups;
-    auto decode = [&](int64_t task, int64_t& line, int64_t& g) {
-        if (quad) {
-            const int64_t wt = task >> 5;
-            const int lane = int(task & 31);
-            line = (wt / gw) * 4 + (lane >> 3);
-            g = (wt % gw) * 8 + (lane & 7);
-            return line < a.v.lines && g < groups;
+// Plane d's bytes of positions p0 .. p0 + nvalid - 1 (p0 a multiple of 16, so in
+// the blocked layout they sit in one 16-byte half-row): one 128-bit store when
+// all 16 are there and the address allows it, byte stores otherwise.
+__device__ __forceinline__ void put16(const SliceArgs& a, int d, int64_t line, int64_t p0, int nvalid, uint32_t w0,
+                                      uint32_t w1, uint32_t w2, uint32_t w3) {
+    int8_t* out = a.planes + plane_off(a, d, line, p0);
+    if (nvalid >= 16 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+        *reinterpret_cast<uint4*>(out) = make_uint4(w0, w1, w2, w3);
+        return;
+    }
+    const uint64_t lo = uint64_t(w0) | (uint64_t(w1) << 32), hi = uint64_t(w2) | (uint64_t(w3) << 32);
+    for (int q = 0; q < nvalid && q < 16; ++q) out[q] = int8_t((q < 8 ? lo : hi) >> (8 * (q & 7)));
+}
+// the same for 8 positions (p0 a multiple of 8)
+__device__ __forceinline__ void put8(const SliceArgs& a, int d, int64_t line, int64_t p0, int nvalid, uint32_t lo,
+                                     uint32_t hi) {
+    int8_t* out = a.planes + plane_off(a, d, line, p0);
+    if (nvalid >= 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
+        *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+        return;
+    }
+    const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
+    for (int q = 0; q < nvalid && q < 8; ++q) out[q] = int8_t(w >> (8 * q));
+}
+
+// All planes of 16 consecutive positions of one line (nvalid of them inside the
+// plane span). S = 0: the certified-ESC indicator planes; S <= 8: one 64-bit
+// word per element, one 128-bit store per plane; S <= 16: 128-bit words, two
+// halves of 8; S = 32: the reference-form restatement per element.
+template <int S>
+__device__ __forceinline__ void emit16(const SliceArgs& a, int nsl, const uint64_t (&bits)[16], int E, int lm,
+                                       int64_t line, int64_t p0, int nvalid) {
+    if constexpr (S == 0) {
+        for (int d = 0; d < nsl; ++d) {
+            const int delta = d == 0 ? a.plan->aux : a.plan->aux2;
+            uint32_t w0, w1, w2, w3;
+            indicator_bytes(bits, lm, delta, w0, w1);
+            indicator_bytes(bits + 8, lm, delta, w2, w3);
+            put16(a, d, line, p0, nvalid, w0, w1, w2, w3);
         }
-        line = task / groups;
-        g = task - line * groups;
-        return true;
-    };
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    // the next task's 64 bytes are requested before this task is sliced and
-    // stored: two loads in flight per thread keep HBM busier
-    auto load = [&](int64_t task, uint64_t (&bits)[8]) {
-        int64_t line, g;
-        if (!decode(task, line, g)) return;
-        const int64_t p0 = g * 8;
-        const double* lp = a.v.ptr + line * a.v.ls;
-        if (kVec && p0 + 8 <= a.v.len) {
+    } else if constexpr (S <= 8) {
+        uint64_t X[16];
+        if (!fast_words<S>(bits, E, X)) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                double2 d2 = __ldg(reinterpret_cast<const double2*>(lp + p0) + q);
-                bits[2 * q] = __double_as_longlong(d2.x);
-                bits[2 * q + 1] = __double_as_longlong(d2.y);
+            for (int q = 0; q < 16; ++q) X[q] = slice_word<S>(bits[q], E);
+        }
+        uint32_t w[S][4];  // plane d: bytes of positions 0-3, 4-7, 8-11, 12-15
+#ifdef ADPB200_SLICE_PACK1
+#pragma unroll
+        for (int d = 0; d < S; ++d) {
+            pack_plane<S>(X, d, w[d][0], w[d][1]);
+            pack_plane<S>(X + 8, d, w[d][2], w[d][3]);
+        }
+#else
+        pack_planes<S>(X, w, 0);
+        pack_planes<S>(X + 8, w, 2);
+#endif
+        // plane d's 16 bytes sit at base + d * plane_stride: one address, one alignment test
+        int8_t* out = a.planes + plane_off(a, 0, line, p0);
+        const bool v16 = nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) | uintptr_t(a.plane_stride)) & 15) == 0;
+        if (v16 && nsl == S) {  // the hot path: straight-line 128-bit stores
+#pragma unroll
+            for (int d = 0; d < S; ++d) {
+                *reinterpret_cast<uint4*>(out) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+                out += a.plane_stride;
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-                bits[q] = p0 + q < a.v.len ? __double_as_longlong(__ldg(lp + p0 + q)) : 0ull;
-        }
-    };
-    int64_t task = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    uint64_t cur[8];
-    if (task < tasks) load(task, cur);
-    for (; task < tasks; task += stride) {
-        uint64_t nxt[8];
-        if (task + stride < tasks) load(task + stride, nxt);
-        int64_t line, g;
-        if (!decode(task, line, g)) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
-            continue;
-        }
-        const int lm = a.line_max[line];
-        const int E = lm == kNegSentinel ? 0 : lm + 2;
-        if (g == 0 && a.scale) a.scale[line] = E;
-        const int64_t p0 = g * 8;
-        const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
-        if constexpr (S == 0) {
-            for (int d = 0; d < nsl; ++d) {
-                uint32_t lo, hi;
-                indicator_bytes(cur, lm, d == 0 ? a.plan->aux : a.plan->aux2, lo, hi);
-                int8_t* out = a.planes + plane_off(a, d, line, p0);
-                if (kVec && nvalid == 8) {
-                    *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
+            for (int d = 0; d < S; ++d) {
+                if (d >= nsl) break;
+                if (v16) {
+                    *reinterpret_cast<uint4*>(out) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
                 } else {
-                    const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-                    for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
+                    const uint64_t lo = uint64_t(w[d][0]) | (uint64_t(w[d][1]) << 32);
+                    const uint64_t hi = uint64_t(w[d][2]) | (uint64_t(w[d][3]) << 32);
+                    for (int q = 0; q < nvalid && q < 16; ++q) out[q] = int8_t((q < 8 ? lo : hi) >> (8 * (q & 7)));
                 }
+                out += a.plane_stride;
             }
-        } else if constexpr (S <= 16) {
-            typename Word<S>::T X[8];
+        }
+    } else if constexpr (S <= 16) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(cur[q], E);
+        for (int h = 0; h < 2; ++h) {
+            if (8 * h >= nvalid) break;
+            u128 X[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[8 * h + q], E);
 #pragma unroll
             for (int d = 0; d < S; ++d) {
                 if (d >= nsl) break;
                 uint32_t lo, hi;
                 pack_plane<S>(X, d, lo, hi);
-                int8_t* out = a.planes + plane_off(a, d, line, p0);
-                if (kVec && nvalid == 8) {
-                    *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
-                } else {
-                    const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-                    for (int q = 0; q < nvalid; ++q) out[q] = int8_t(w >> (8 * q));
-                }
-            }
-        } else {
-            int8_t dig[kMaxSlices];
-            const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
-            for (int q = 0; q < nvalid; ++q) {
-                slice_digits_slow(cur[q], E, s, dig);
-                for (int d = 0; d < nsl; ++d) a.planes[plane_off(a, d, line, p0 + q)] = dig[d];
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
-    }
-}
-
-template <bool kVec>
-__global__ void __launch_bounds__(256, 3) slice_rows_kernel(SliceArgs a) {
-    int s, nsl;
-    if (!resolve(a, s, nsl)) return;
-    // blocked planes are zero-filled up to the 32-byte k-block
-    const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
-    const int64_t groups = (span + 7) / 8;
-    if (a.indicator) {
-        rows_body<0, kVec>(a, nsl, groups, span);
-        return;
-    }
-    switch (s) {
-#define ADPB200_ROWS_CASE(S) \
-    case S: rows_body<S, kVec>(a, nsl, groups, span); break;
-        ADPB200_ROWS_CASE(1) ADPB200_ROWS_CASE(2) ADPB200_ROWS_CASE(3) ADPB200_ROWS_CASE(4)
-        ADPB200_ROWS_CASE(5) ADPB200_ROWS_CASE(6) ADPB200_ROWS_CASE(7) ADPB200_ROWS_CASE(8)
-        ADPB200_ROWS_CASE(9) ADPB200_ROWS_CASE(10) ADPB200_ROWS_CASE(11) ADPB200_ROWS_CASE(12)
-        ADPB200_ROWS_CASE(13) ADPB200_ROWS_CASE(14) ADPB200_ROWS_CASE(15) ADPB200_ROWS_CASE(16)
-#undef ADPB200_ROWS_CASE
-        default: rows_body<32, kVec>(a, nsl, groups, span); break;
-    }
-}
-
-// ---- lines adjacent (ls == 1), positions strided: 64 lines x 32 positions ---------
-// The FP64 tile is transposed through shared memory (loads coalesced across
-// lines, 16.6 KiB per CTA whatever s is); each thread then slices 8
-// consecutive positions of one line exactly like the contiguous variant, so a
-// warp stores 8 lines x 32 B = one contiguous 256-byte run per plane in the
-// blocked layout.
-constexpr int kTL = 64, kTP = 32, kTPad = kTL + 1;
-
-template <int S>
-__device__ __forceinline__ void cols_body(const SliceArgs& a, int nsl, const uint64_t (&bits)[8], int E,
-                                          int64_t line, int64_t p0, int nvalid) {
-    if constexpr (S <= 16) {
-        typename Word<S>::T X[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[q], E);
-#pragma unroll
-        for (int d = 0; d < S; ++d) {
-            if (d >= nsl) break;
-            uint32_t lo, hi;
-            pack_plane<S>(X, d, lo, hi);
-            int8_t* out = a.planes + plane_off(a, d, line, p0);
-            if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0) {
-                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
-            } else {
-                const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-                for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, d, line, p0 + q)] = int8_t(w >> (8 * q));
+                put8(a, d, line, p0 + 8 * h, nvalid - 8 * h, lo, hi);
             }
         }
     } else {
         int8_t dig[kMaxSlices];
         const int s = a.slices_fixed > 0 ? a.slices_fixed : a.plan->slices;
-        for (int q = 0; q < nvalid; ++q) {
+        for (int q = 0; q < nvalid && q < 16; ++q) {
             slice_digits_slow(bits[q], E, s, dig);
             for (int d = 0; d < nsl; ++d) a.planes[plane_off(a, d, line, p0 + q)] = dig[d];
         }
     }
 }
 
-__global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
+// ---- the staged tile pipeline ------------------------------------------------------------
+// A CTA owns tiles of 4096 elements (32 KiB of FP64): rows variant (positions
+// contiguous, ps == 1) 32 lines x 128 positions, cols variant (any strides; lines
+// adjacent when ls == 1) 128 lines x one k-block of 32 positions. Tiles are
+// copied HBM -> shared memory with cp.async in fully coalesced 16-byte chunks
+// (8 B per element when the addresses do not allow 16), kStages deep, so the
+// copies of the next tiles are in flight while the current one is sliced.
+// Out-of-range elements are zero-filled by the copy (src-size 0). Each thread
+// then slices 16 consecutive positions of one line out of shared memory and
+// stores one 16-byte chunk per plane: per plane a warp writes 4 x 128 B (rows)
+// or 512 contiguous bytes (cols) of the blocked layout. Consecutive tiles walk
+// the lines first, so the CTAs in flight fill whole k-blocks.
+constexpr int kRowsLines = 32, kRowsPos = 128;  // rows tile
+constexpr int kColsLines = 128, kColsPos = 32;  // cols tile
+constexpr int kTileElems = 4096;
+#ifndef ADPB200_SLICE_STAGES
+#define ADPB200_SLICE_STAGES 2
+#endif
+constexpr int kStages = ADPB200_SLICE_STAGES;
+constexpr size_t kSliceSmem = size_t(kStages) * kTileElems * 8;
+
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp8(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// rows stage: [line 32][16-byte chunk 64], chunk c of a line stored at c ^ ((c >> 3) & 7),
+// so the 8 lanes of a quarter-warp reading chunk 8g + q (g = 0..7) hit 8 distinct bank groups
+__device__ __forceinline__ int rows_chunk(int c) { return c ^ ((c >> 3) & 7); }
+
+// Tile coordinates (line tile, position tile), walked lines first; a thread
+// advances them by gridDim.x tiles with one add and one carry (no 64-bit divisions).
+struct TileIdx {
+    int64_t lt, pt;
+};
+
+template <bool kRows, bool kVec>
+struct Tiler {
+    static constexpr int kL = kRows ? kRowsLines : kColsLines;
+    static constexpr int kP = kRows ? kRowsPos : kColsPos;
+    const SliceArgs& a;
+    int64_t nlt, npt, glt, gpt;  // tiles along lines / positions; gridDim.x as (lines, positions) step
+    __device__ __forceinline__ Tiler(const SliceArgs& a_, int64_t span) : a(a_) {
+        nlt = (a.v.lines + kL - 1) / kL;
+        npt = (span + kP - 1) / kP;
+        gpt = int64_t(gridDim.x) / nlt;
+        glt = int64_t(gridDim.x) - gpt * nlt;
+    }
+    __device__ __forceinline__ TileIdx first() const {
+        const int64_t pt = int64_t(blockIdx.x) / nlt;
+        return TileIdx{int64_t(blockIdx.x) - pt * nlt, pt};
+    }
+    __device__ __forceinline__ void step(TileIdx& t) const {
+        t.lt += glt;
+        t.pt += gpt;
+        if (t.lt >= nlt) {
+            t.lt -= nlt;
+            ++t.pt;
+        }
+    }
+    __device__ __forceinline__ bool valid(const TileIdx& t) const { return t.pt < npt; }
+    // issue the copies of tile t into the stage at shared address s
+    __device__ __forceinline__ void issue(const TileIdx& t, uint32_t s) const {
+        const int64_t l0 = t.lt * kL, p0 = t.pt * kP;
+        const int tid = threadIdx.x;
+        if (kVec) {
+            // 2048 chunks of 16 B (two elements adjacent in memory), 8 per thread:
+            // chunk column c = tid % 64 fixed, rows r = tid / 64 + 4 i
+            const int c = tid & 63, r0 = tid >> 6;
+            // (the per-chunk test is one 32-bit compare against what is left of the tile)
+            if (kRows) {  // a warp: 32 consecutive chunks (512 B) of one line
+                const int64_t pos = p0 + 2 * c;
+                const int bytes = pos < a.v.len ? (pos + 1 < a.v.len ? 16 : 8) : 0;
+                const int64_t left64 = a.v.lines - (l0 + r0);
+                const int left = left64 < 32 ? int(left64) : 32;
+                const double* src = a.v.ptr + (l0 + r0) * a.v.ls + pos;
+                const int64_t dl = 4 * a.v.ls;
+                const uint32_t dst = s + uint32_t(r0 * 64 + rows_chunk(c)) * 16u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int nb = 4 * i < left ? bytes : 0;
+                    cp16(dst + i * (4u * 64u * 16u), nb ? src : a.v.ptr, nb);
+                    src += dl;
+                }
+            } else {      // a warp: 64 adjacent lines at one position (512 contiguous bytes)
+                const int64_t line = l0 + 2 * c;
+                const int bytes = line < a.v.lines ? (line + 1 < a.v.lines ? 16 : 8) : 0;
+                const int64_t left64 = a.v.len - (p0 + r0);
+                const int left = left64 < 32 ? int(left64) : 32;
+                const double* src = a.v.ptr + line + (p0 + r0) * a.v.ps;
+                const int64_t dp = 4 * a.v.ps;
+                const uint32_t dst = s + uint32_t(r0 * kColsLines + 2 * c) * 8u;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int nb = 4 * i < left ? bytes : 0;
+                    cp16(dst + i * (4u * kColsLines * 8u), nb ? src : a.v.ptr, nb);
+                    src += dp;
+                }
+            }
+        } else {
+            // 4096 elements of 8 B, 16 per thread, any strides
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = tid + 256 * i;
+                int64_t line, pos;
+                uint32_t off;
+                if (kRows) {
+                    const int r = e >> 7, q = e & 127;
+                    line = l0 + r;
+                    pos = p0 + q;
+                    off = uint32_t(r * 64 + rows_chunk(q >> 1)) * 16u + uint32_t(q & 1) * 8u;
+                } else {
+                    const int r = e >> 7, l = e & 127;
+                    line = l0 + l;
+                    pos = p0 + r;
+                    off = uint32_t(r * kColsLines + l) * 8u;
+                }
+                const bool ok = line < a.v.lines && pos < a.v.len;
+                cp8(s + off, ok ? a.v.ptr + line * a.v.ls + pos * a.v.ps : a.v.ptr, ok ? 8 : 0);
+            }
+        }
+    }
+    // this thread's line and first position inside a tile
+    __device__ __forceinline__ void mine(int& lsub, int& psub) const {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (kRows) {
+            lsub = warp * 4 + (lane >> 3);
+            psub = (lane & 7) * 16;
+        } else {
+            lsub = warp * 16 + (lane >> 1);
+            psub = (lane & 1) * 16;
+        }
+    }
+    // its 16 elements out of a stage
+    __device__ __forceinline__ void read(const char* stage, int lsub, int psub, uint64_t (&bits)[16]) const {
+        if (kRows) {
+            const int c0 = psub >> 1;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint4 v = *reinterpret_cast<const uint4*>(stage + (lsub * 64 + rows_chunk(c0 + q)) * 16);
+                bits[2 * q] = uint64_t(v.x) | (uint64_t(v.y) << 32);
+                bits[2 * q + 1] = uint64_t(v.z) | (uint64_t(v.w) << 32);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                bits[q] = *reinterpret_cast<const uint64_t*>(stage + ((psub + q) * kColsLines + lsub) * 8);
+        }
+    }
+};
+
+template <int S, bool kRows, bool kVec>
+__device__ __forceinline__ void staged_body(const SliceArgs& a, int nsl, int64_t span, char* smem) {
+    const Tiler<kRows, kVec> T(a, span);
+    const uint32_t s0 = uint32_t(__cvta_generic_to_shared(smem));
+    int lsub, psub;
+    T.mine(lsub, psub);
+    TileIdx cur = T.first(), ahead = cur;
+#pragma unroll
+    for (int st = 0; st < kStages - 1; ++st) {
+        if (T.valid(ahead)) T.issue(ahead, s0 + uint32_t(st) * kTileElems * 8u);
+        cp_commit();
+        T.step(ahead);
+    }
+    for (int it = 0; T.valid(cur); T.step(cur), ++it) {
+        // keep kStages - 1 tiles in flight: the copy of iteration it + kStages - 1
+        if (T.valid(ahead)) T.issue(ahead, s0 + uint32_t((it + kStages - 1) % kStages) * kTileElems * 8u);
+        cp_commit();
+        T.step(ahead);
+        cp_wait<kStages - 1>();
+        __syncthreads();  // every thread's copies of this tile have landed
+        const int64_t line = cur.lt * T.kL + lsub, pos = cur.pt * T.kP + psub;
+        if (line < a.v.lines && pos < span) {
+            uint64_t bits[16];
+            T.read(smem + size_t(it % kStages) * kTileElems * 8, lsub, psub, bits);
+            const int lm = a.line_max[line];
+            const int E = lm == kNegSentinel ? 0 : lm + 2;
+            if (pos == 0 && a.scale) a.scale[line] = E;
+            const int nvalid = span - pos < 16 ? int(span - pos) : 16;
+            emit16<S>(a, nsl, bits, E, lm, line, pos, nvalid);
+        }
+        __syncthreads();  // the stage is free for the copy issued next iteration
+    }
+    cp_wait<0>();
+}
+
+template <bool kRows, bool kVec>
+__global__ void __launch_bounds__(256, 3) slice_kernel(SliceArgs a) {
     int s, nsl;
     if (!resolve(a, s, nsl)) return;
-    __shared__ uint64_t tile[kTP][kTPad];
-    const int64_t line0 = int64_t(blockIdx.x) * kTL;
-    const int64_t pos0 = int64_t(blockIdx.y) * kTP;
-    {
-        const int tl = threadIdx.x % kTL, tp = threadIdx.x / kTL;  // 4 position rows per pass
-        const int64_t line = line0 + tl;
-        uint64_t v[kTP / 4];
-#pragma unroll
-        for (int i = 0; i < kTP / 4; ++i) {
-            const int64_t pos = pos0 + tp + 4 * i;
-            v[i] = (line < a.v.lines && pos < a.v.len) ? __double_as_longlong(__ldg(a.v.ptr + line + pos * a.v.ps))
-                                                        : 0ull;
-        }
-#pragma unroll
-        for (int i = 0; i < kTP / 4; ++i) tile[tp + 4 * i][tl] = v[i];
-    }
-    __syncthreads();
-    const int ol = threadIdx.x / 4, og = threadIdx.x % 4;  // line, group of 8 positions
-    const int64_t line = line0 + ol;
-    if (line >= a.v.lines) return;
-    const int lm = a.line_max[line];
-    const int E = lm == kNegSentinel ? 0 : lm + 2;
-    if (blockIdx.y == 0 && og == 0 && a.scale) a.scale[line] = E;
+    extern __shared__ __align__(16) char smem[];
+    // blocked planes are zero-filled up to the 32-byte k-block
     const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
-    const int64_t p0 = pos0 + og * 8;
-    if (p0 >= span) return;
-    const int nvalid = span - p0 < 8 ? int(span - p0) : 8;
-    uint64_t bits[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) bits[q] = tile[og * 8 + q][ol];
     if (a.indicator) {
-        for (int d = 0; d < nsl; ++d) {
-            uint32_t lo, hi;
-            indicator_bytes(bits, lm, d == 0 ? a.plan->aux : a.plan->aux2, lo, hi);
-            const uint64_t w = uint64_t(lo) | (uint64_t(hi) << 32);
-            int8_t* out = a.planes + plane_off(a, d, line, p0);
-            if (nvalid == 8 && (reinterpret_cast<uintptr_t>(out) & 7) == 0)
-                *reinterpret_cast<uint2*>(out) = make_uint2(lo, hi);
-            else
-                for (int q = 0; q < nvalid; ++q) a.planes[plane_off(a, d, line, p0 + q)] = int8_t(w >> (8 * q));
-        }
+        staged_body<0, kRows, kVec>(a, nsl, span, smem);
         return;
     }
     switch (s) {
-#define ADPB200_COLS_CASE(S) \
-    case S: cols_body<S>(a, nsl, bits, E, line, p0, nvalid); break;
-        ADPB200_COLS_CASE(1) ADPB200_COLS_CASE(2) ADPB200_COLS_CASE(3) ADPB200_COLS_CASE(4)
-        ADPB200_COLS_CASE(5) ADPB200_COLS_CASE(6) ADPB200_COLS_CASE(7) ADPB200_COLS_CASE(8)
-        ADPB200_COLS_CASE(9) ADPB200_COLS_CASE(10) ADPB200_COLS_CASE(11) ADPB200_COLS_CASE(12)
-        ADPB200_COLS_CASE(13) ADPB200_COLS_CASE(14) ADPB200_COLS_CASE(15) ADPB200_COLS_CASE(16)
-#undef ADPB200_COLS_CASE
-        default: cols_body<32>(a, nsl, bits, E, line, p0, nvalid); break;
+#define ADPB200_SLICE_CASE(S) \
+    case S: staged_body<S, kRows, kVec>(a, nsl, span, smem); break;
+        ADPB200_SLICE_CASE(1) ADPB200_SLICE_CASE(2) ADPB200_SLICE_CASE(3) ADPB200_SLICE_CASE(4)
+        ADPB200_SLICE_CASE(5) ADPB200_SLICE_CASE(6) ADPB200_SLICE_CASE(7) ADPB200_SLICE_CASE(8)
+        ADPB200_SLICE_CASE(9) ADPB200_SLICE_CASE(10) ADPB200_SLICE_CASE(11) ADPB200_SLICE_CASE(12)
+        ADPB200_SLICE_CASE(13) ADPB200_SLICE_CASE(14) ADPB200_SLICE_CASE(15) ADPB200_SLICE_CASE(16)
+#undef ADPB200_SLICE_CASE
+        default: staged_body<32, kRows, kVec>(a, nsl, span, smem); break;
     }
+}
+
+using SliceFn = void (*)(SliceArgs);
+
+// resident CTAs per SM of a slicing kernel (the grids are persistent)
+int resident(SliceFn fn) {
+    cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(kSliceSmem));
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, kSliceSmem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return per_sm;
 }
 
 }  // namespace
@@ -432,28 +603,30 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(SliceArgs a) {
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
                   int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
                   uint64_t* nlaunch, int indicator) {
+    (void)plane_cap;
     if (v.lines == 0) return;
     SliceArgs a{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed, indicator};
-    const bool rows = v.ps == 1 || v.lines == 1 || v.len == 0;
-    if (rows) {
-        if (a.v.lines == 1) a.v.ls = 0;
-        const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
-        int64_t groups = (span + 7) / 8;
-        if (groups == 0) groups = 1;
-        int64_t tasks = v.lines * groups;
-        int64_t want = (tasks + 255) / 256;
-        int grid = (int)(want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16);
-        if (grid < 1) grid = 1;
-        const bool vec = ((reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0) && ((v.ls & 1) == 0 || v.lines == 1) &&
-                         (blocked || (((pitch & 7) == 0) && ((plane_stride & 7) == 0))) &&
-                         ((reinterpret_cast<uintptr_t>(planes) & 7) == 0);
-        if (vec) slice_rows_kernel<true><<<grid, 256, 0, st>>>(a);
-        else slice_rows_kernel<false><<<grid, 256, 0, st>>>(a);
+    const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
+    if (span == 0) return;
+    static const SliceFn fns[4] = {slice_kernel<false, false>, slice_kernel<false, true>, slice_kernel<true, false>,
+                                   slice_kernel<true, true>};
+    static int res[4] = {0, 0, 0, 0};
+    if (!res[0])
+        for (int i = 0; i < 4; ++i) res[i] = resident(fns[i]);
+    const bool aligned = (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
+    int which;
+    int64_t tiles;
+    if (v.ps == 1 || v.len == 1) {
+        if (v.lines == 1) a.v.ls = 0;
+        which = 2 + ((aligned && (a.v.ls & 1) == 0) ? 1 : 0);  // 16-byte chunks need even line starts
+        tiles = (v.lines + kRowsLines - 1) / kRowsLines * ((span + kRowsPos - 1) / kRowsPos);
     } else {
-        const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
-        dim3 grid((unsigned)((v.lines + kTL - 1) / kTL), (unsigned)((span + kTP - 1) / kTP));
-        slice_cols_kernel<<<grid, 256, 0, st>>>(a);
+        which = (aligned && v.ls == 1 && (v.ps & 1) == 0) ? 1 : 0;  // two adjacent lines per 16-byte chunk
+        tiles = (v.lines + kColsLines - 1) / kColsLines * ((span + kColsPos - 1) / kColsPos);
     }
+    const int64_t cap = int64_t(num_sms()) * res[which];
+    const int grid = int(tiles < cap ? tiles : cap);
+    fns[which]<<<grid, 256, kSliceSmem, st>>>(a);
     ++*nlaunch;
 }
 

@@ -53,7 +53,7 @@ for r in csv.reader(open(os.path.join(G, f"{tag}_launches.csv"))):
 ours = {k: v for k, v in agg.items() if not k.startswith("at::")}
 tot = sum(v[1] for v in ours.values())
 lines = ["# ncu launch list (gpu__time_duration.sum, --clock-control none): python bench.py --quick --no-cpu --steps 2 --warmup 1",
-         "# cold-cache, serialised launches - compare SHARES, not absolutes; 4 pipeline calls (trace call + warm-up + 2 timed);",
+         "# cold-cache, serialised launches - compare SHARES, not absolutes; every pipeline call of the run (trace call, warm-up, burst, timed);",
          "# uniform_kernel = the device xoshiro input generator (setup, untimed).",
          f"{'kernel':48s} {'launches':>8s} {'total_us':>12s} {'per_launch_us':>14s} {'share_of_ours':>13s}"]
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
