@@ -242,6 +242,8 @@ def strong_c4(args, adp, grading, dev, world, rank, handle, timed, dist):
     flops = 2.0 * mg * n * k
     out = {"m": mg, "n": n, "k": k, "unit": "TFLOP/s", "data": "U[-1,1], gen_uniform_rect seeds 1, 2",
            "partition": args.c4_dist if world > 1 else "single GPU"}
+    if os.environ.get("ADPB200_BENCH_SHARED_GPU") == "1":
+        out["note"] = "plumbing check: all ranks share cuda:0, so neither time is a scaling measurement"
     torch.cuda.empty_cache()
     # one GPU, the whole problem (column-major NN)
     At = grading.gen_uniform_rect(k, mg, 1, -1.0, 1.0, dev.index)

@@ -115,6 +115,9 @@ constexpr int kDStages = ADPB200_DMMA_STAGES;
 constexpr int kPadL = kDT + 4;  // [k][line] rows: 132 doubles (== 4 mod 16: conflict-free fragment reads)
 constexpr int kPadK = kDK + 4;  // [line][k] rows: kDK + 4 doubles (== 4 mod 16)
 constexpr int kOpDoubles = (kDK * kPadL > kDT * kPadK) ? kDK * kPadL : kDT * kPadK;  // one operand, one stage
+#ifndef ADPB200_DMMA_PIPE
+#define ADPB200_DMMA_PIPE 0  // measured: register double-buffered fragments 28.7 vs 29.3 TFLOP/s without
+#endif
 #ifndef ADPB200_DMMA_WARPS
 #define ADPB200_DMMA_WARPS 8
 #endif
@@ -218,18 +221,45 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
             }
             cp_async_commit();
         }
+        // stage indices tracked incrementally (no 64-bit modulo in the loop)
+        int st_cur = 0, st_next = kDStages - 1;
         for (int64_t t = 0; t < nk; ++t) {
             cp_async_wait<kDStages - 2>();
             __syncthreads();  // stage t visible to all; stage t-1 fully consumed
             const int64_t tn = t + kDStages - 1;
             if (tn < nk) {
-                const int st = int(tn % kDStages);
-                ta.load(sa_u(st), i0, tn * kDK, tid);
-                tb.load(sb_u(st), j0, tn * kDK, tid);
+                ta.load(sa_u(st_next), i0, tn * kDK, tid);
+                tb.load(sb_u(st_next), j0, tn * kDK, tid);
             }
             cp_async_commit();
-            const double* As = sa(int(t % kDStages));
-            const double* Bs = sb(int(t % kDStages));
+            const double* As = sa(st_cur);
+            const double* Bs = sb(st_cur);
+            st_cur = st_cur + 1 == kDStages ? 0 : st_cur + 1;
+            st_next = st_next + 1 == kDStages ? 0 : st_next + 1;
+#if ADPB200_DMMA_PIPE
+            // fragments of k-step kk + 4 are read while the MMAs of kk issue
+            double af[2][kMI], bf[2][kNI];
+#pragma unroll
+            for (int mi = 0; mi < kMI; ++mi) af[0][mi] = ta.frag(As, wm * kMI * 8 + mi * 8 + fr, fk);
+#pragma unroll
+            for (int ni = 0; ni < kNI; ++ni) bf[0][ni] = tb.frag(Bs, wn * kNI * 8 + ni * 8 + fr, fk);
+#pragma unroll
+            for (int kk = 0; kk < kDK; kk += 4) {
+                const int c = (kk / 4) & 1;
+                if (kk + 4 < kDK) {
+#pragma unroll
+                    for (int mi = 0; mi < kMI; ++mi)
+                        af[c ^ 1][mi] = ta.frag(As, wm * kMI * 8 + mi * 8 + fr, kk + 4 + fk);
+#pragma unroll
+                    for (int ni = 0; ni < kNI; ++ni)
+                        bf[c ^ 1][ni] = tb.frag(Bs, wn * kNI * 8 + ni * 8 + fr, kk + 4 + fk);
+                }
+#pragma unroll
+                for (int mi = 0; mi < kMI; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < kNI; ++ni) dmma(acc[mi][ni], af[c][mi], bf[c][ni]);
+            }
+#else
 #pragma unroll
             for (int kk = 0; kk < kDK; kk += 4) {
                 double af[kMI], bf[kNI];
@@ -242,6 +272,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
 #pragma unroll
                     for (int ni = 0; ni < kNI; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
             }
+#endif
         }
         cp_async_wait<0>();
         __syncthreads();  // the next tile's prologue overwrites stages 0..1
