@@ -48,7 +48,7 @@ struct Plan {
     int32_t aux;   // certified-ESC plan: indicator threshold delta of plane 0
     int32_t aux2;  //   ... of plane 1 (two-level plans)
     int32_t lvl0;  //   certificate level plane 0 stands for (0, or 1 when level 0 cannot help)
-    int32_t pad[1];
+    int32_t esc_probe_fail;  // ESC tiles whose block-0 pruning probe failed against a published maximum
 };
 
 struct DecideInput {

@@ -33,6 +33,38 @@ __device__ __forceinline__ void classify(uint64_t bits, int& nan, int& inf, int&
     e = eff_exp(bits);
 }
 
+// Exponent statistics of N elements. Fast path (three instructions per element):
+// when every element is a finite, normal nonzero number, the effective exponent is
+// the biased exponent field - 1023, so the field's max / min over the group are
+// the block's; otherwise (a zero, subnormal, Inf or NaN is present) classify() runs
+// per element, exactly as before.
+template <int N>
+__device__ __forceinline__ void stats_group(const uint64_t (&bb)[N], int& nan, int& inf, int& negz, int& bmax,
+                                            int& bmin) {
+    uint32_t mx = 0, mn = 0xffffffffu;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        const uint32_t f = uint32_t(bb[q] >> 32) & 0x7ff00000u;
+        mx = max(mx, f);
+        mn = min(mn, f);
+    }
+    if (mn != 0 && mx != 0x7ff00000u) {
+        bmax = max(bmax, int(mx >> 20) - 1023);
+        bmin = min(bmin, int(mn >> 20) - 1023);
+        return;
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+        bool fnz;
+        int e = 0;
+        classify(bb[q], nan, inf, negz, fnz, e);
+        if (fnz) {
+            bmax = max(bmax, e);
+            bmin = min(bmin, e);
+        }
+    }
+}
+
 __device__ __forceinline__ int warp_max(int v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -81,23 +113,18 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
         const double* lp = v.ptr + line * v.ls;
         int bmax = kNegSentinel, bmin = -kNegSentinel;
         int64_t pos = lo + lane;
-        // 4 independent loads in flight per lane
-        for (; pos + 96 < hi; pos += 128) {
-            uint64_t b0 = __double_as_longlong(__ldg(lp + pos));
-            uint64_t b1 = __double_as_longlong(__ldg(lp + pos + 32));
-            uint64_t b2 = __double_as_longlong(__ldg(lp + pos + 64));
-            uint64_t b3 = __double_as_longlong(__ldg(lp + pos + 96));
-            uint64_t bb[4] = {b0, b1, b2, b3};
+        // 8 (then 4) independent loads in flight per lane
+        for (; pos + 224 < hi; pos += 256) {
+            uint64_t bb[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                bool fnz;
-                int e = 0;
-                classify(bb[q], nan, inf, negz, fnz, e);
-                if (fnz) {
-                    bmax = max(bmax, e);
-                    bmin = min(bmin, e);
-                }
-            }
+            for (int q = 0; q < 8; ++q) bb[q] = __double_as_longlong(__ldg(lp + pos + 32 * q));
+            stats_group(bb, nan, inf, negz, bmax, bmin);
+        }
+        for (; pos + 96 < hi; pos += 128) {
+            uint64_t bb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) bb[q] = __double_as_longlong(__ldg(lp + pos + 32 * q));
+            stats_group(bb, nan, inf, negz, bmax, bmin);
         }
         for (; pos < hi; pos += 32) {
             bool fnz;
@@ -145,20 +172,17 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
             const int64_t hi = lo + per < b1 ? lo + per : b1;
             const double* p = v.ptr + line;
             int64_t pos = lo;
+            for (; pos + 7 < hi; pos += 8) {
+                uint64_t bb[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) bb[q] = __double_as_longlong(__ldg(p + (pos + q) * v.ps));
+                stats_group(bb, nan, inf, negz, bmax, bmin);
+            }
             for (; pos + 3 < hi; pos += 4) {
                 uint64_t bb[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) bb[q] = __double_as_longlong(__ldg(p + (pos + q) * v.ps));
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    bool fnz;
-                    int e = 0;
-                    classify(bb[q], nan, inf, negz, fnz, e);
-                    if (fnz) {
-                        bmax = max(bmax, e);
-                        bmin = min(bmin, e);
-                    }
-                }
+                stats_group(bb, nan, inf, negz, bmax, bmin);
             }
             for (; pos < hi; ++pos) {
                 bool fnz;
@@ -245,7 +269,7 @@ __device__ __forceinline__ uint32_t pack2(int lo, int hi) {
 }
 __device__ __forceinline__ int to16(int v) { return v == kNegSentinel ? kS16 : v; }
 
-__global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ amaxT,
+__global__ void __launch_bounds__(256, 4) esc_kernel(const int32_t* __restrict__ amaxT,
                                                   const int32_t* __restrict__ aminT,
                                                   const int32_t* __restrict__ aline,
                                                   const int32_t* __restrict__ bmaxT,
@@ -265,6 +289,15 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
     // all-gathered layout of the B-distributed path; nr = n: one slab): the offset of
     // column j0 + jj minus gt * nr, computed once per CTA (no division in the loops)
     __shared__ int64_t sBoff[kEscBJ];
+    __shared__ int sBound, sStop;
+#ifndef ADPB200_ESC_PRUNE
+#define ADPB200_ESC_PRUNE 1
+#endif
+    // the pruning probe's give-up flag, read under the barrier below (see kProbeGiveUp)
+    constexpr int kProbeGiveUp = 128;
+    if (threadIdx.x == 0)
+        sStop = !ADPB200_ESC_PRUNE ||
+                (plan && *reinterpret_cast<const volatile int32_t*>(&plan->esc_probe_fail) >= kProbeGiveUp);
     if (threadIdx.x < kEscBJ) {
         const int64_t gj = j0 + threadIdx.x;
         const int64_t r = gj / nr;
@@ -284,38 +317,105 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
     for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
+    auto stage_block = [&](int tt, int64_t gt) {
+        const bool tok = gt < t;
+        const int vx = a_ok && tok ? to16(pamx[gt * astride]) : kS16;
+        const int vn = a_ok && tok ? to16(pamn[gt * astride]) : kS16;
+        sAmx[tt][sl] = pack2(vx, vx);
+        sAmn[tt][sl] = pack2(vn, vn);
+        const int64_t go = gt * nr;
+        sBmx[tt][sl] = pack2(b_ok0 && tok ? to16(bmaxT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bmaxT[bo1 + go]) : kS16);
+        sBmn[tt][sl] = pack2(b_ok0 && tok ? to16(bminT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bminT[bo1 + go]) : kS16);
+    };
+    auto step = [&](int tt) {
+        const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
+        const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
+        const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
+        const uint4 b_mn = *reinterpret_cast<const uint4*>(&sBmn[tt][tx * 4]);
+        const uint32_t amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
+        const uint32_t amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
+        const uint32_t bmx[4] = {b_mx.x, b_mx.y, b_mx.z, b_mx.w};
+        const uint32_t bmn[4] = {b_mn.x, b_mn.y, b_mn.z, b_mn.w};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
+                z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
+            }
+    };
+    // spans, two j per int16x2 word: la + lb + 1 - z in [-4193, 4195] for real
+    // exponents; z <= -8000 (structurally zero dot product, or a padded row /
+    // column) is masked to -32768 so it never wins the max.
+    // max over this thread's pairs of la + lb + 1 - z, dead pairs (z <= -8000) as
+    // `dead_as` (the line maxima are re-read per call rather than held in registers
+    // across the max-plus loop)
+    auto span_max = [&](uint32_t dead_as) {
+        uint32_t lbp[4], lap[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int jj = 2 * (tx * 4 + b);
+            const int l0 = j0 + jj < n ? bline[sBoff[jj]] : 0, l1 = j0 + jj + 1 < n ? bline[sBoff[jj + 1]] : 0;
+            lbp[b] = pack2(l0 + 1, l1 + 1);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            const int64_t gi = i0 + ty * 4 + a;
+            const int la = gi < m ? aline[gi] : 0;
+            lap[a] = pack2(la, la);
+        }
+        const uint32_t lim = pack2(-8000, -8000);
+        uint32_t best = pack2(-32768, -32768);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t span = __vsub2(__vadd2(lap[a], lbp[b]), z[a][b]);
+                const uint32_t dead = __vcmples2(z[a][b], lim);  // 0xffff per half where z <= -8000
+                best = __vmaxs2(best, (span & ~dead) | (dead_as & dead));
+            }
+        return max(int(int16_t(best & 0xffffu)), int(int16_t(best >> 16)));
+    };
+    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && ran_flag) *ran_flag = 1;
+    // Tile pruning (exact). z only grows as blocks are added, so la + lb + 1 - z over
+    // the blocks seen so far bounds every final span from above -- for pairs whose z
+    // is already live (> -8000; a dead pair may still come alive, so it bounds
+    // nothing). When that bound is <= the running maximum other CTAs have already
+    // published to esc_out, no span of this tile can raise it and the tile stops:
+    // the result is the reference's max over every (i, j). Checked after block 0
+    // and after every staged round; narrow exponent ranges (every block of every
+    // line alike) stop after one block.
+    // The block-0 probe costs each CTA a serial staging + reduction latency (~17 % of
+    // the kernel when no tile can stop), so it gives up once kProbeGiveUp probes have
+    // failed against an already published maximum (plan->esc_probe_fail; probes that
+    // found nothing published yet, as in the first wave, do not count).
+    const bool probe = sStop == 0;
+    auto prunable = [&](bool count) {
+        if (threadIdx.x == 0) sBound = -32768;
+        __syncthreads();
+        const int bnd = warp_max(span_max(0x7fff7fffu));
+        if ((threadIdx.x & 31) == 0) atomicMax(&sBound, bnd);
+        __syncthreads();
+        // one thread reads the running maximum, so the whole CTA takes the same branch
+        if (threadIdx.x == 0) {
+            const int published = *reinterpret_cast<volatile int32_t*>(esc_out);
+            sStop = sBound <= published;
+            if (count && !sStop && published > 0 && plan) atomicAdd(&const_cast<Plan*>(plan)->esc_probe_fail, 1);
+        }
+        __syncthreads();
+        return sStop != 0;
+    };
+    if (probe) {
+        if (st0 == 0) stage_block(0, 0);
+        __syncthreads();
+        step(0);
+        if (prunable(true)) return;
+    }
     for (int64_t tb = 0; tb < t; tb += kEscTB) {
         __syncthreads();
 #pragma unroll
-        for (int tt = st0; tt < kEscTB; tt += 4) {
-            const int64_t gt = tb + tt;
-            const bool tok = gt < t;
-            const int vx = a_ok && tok ? to16(pamx[gt * astride]) : kS16;
-            const int vn = a_ok && tok ? to16(pamn[gt * astride]) : kS16;
-            sAmx[tt][sl] = pack2(vx, vx);
-            sAmn[tt][sl] = pack2(vn, vn);
-            const int64_t go = gt * nr;
-            sBmx[tt][sl] = pack2(b_ok0 && tok ? to16(bmaxT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bmaxT[bo1 + go]) : kS16);
-            sBmn[tt][sl] = pack2(b_ok0 && tok ? to16(bminT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bminT[bo1 + go]) : kS16);
-        }
+        for (int tt = st0; tt < kEscTB; tt += 4) stage_block(tt, tb + tt);
         __syncthreads();
-        auto step = [&](int tt) {
-            const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
-            const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
-            const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
-            const uint4 b_mn = *reinterpret_cast<const uint4*>(&sBmn[tt][tx * 4]);
-            const uint32_t amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
-            const uint32_t amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
-            const uint32_t bmx[4] = {b_mx.x, b_mx.y, b_mx.z, b_mx.w};
-            const uint32_t bmn[4] = {b_mn.x, b_mn.y, b_mn.z, b_mn.w};
-#pragma unroll
-            for (int a = 0; a < 4; ++a)
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
-                    z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
-                }
-        };
         if (t - tb >= kEscTB) {
 #pragma unroll 4
             for (int tt = 0; tt < kEscTB; ++tt) step(tt);
@@ -326,35 +426,10 @@ __global__ void __launch_bounds__(256) esc_kernel(const int32_t* __restrict__ am
 #pragma unroll 4
             for (int tt = 0; tt < tcount; ++tt) step(tt);
         }
+        if (ADPB200_ESC_PRUNE && tb + kEscTB < t && prunable(false)) return;
     }
-    // spans, two j per int16x2 word: la + lb + 1 - z in [-4193, 4195] for real
-    // exponents; z <= -8000 (structurally zero dot product, or a padded row /
-    // column) is masked to -32768 so it never wins the max.
-    uint32_t lbp[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const int jj = 2 * (tx * 4 + b);
-        const int l0 = j0 + jj < n ? bline[sBoff[jj]] : 0, l1 = j0 + jj + 1 < n ? bline[sBoff[jj + 1]] : 0;
-        lbp[b] = pack2(l0 + 1, l1 + 1);
-    }
-    const uint32_t lim = pack2(-8000, -8000);
-    uint32_t best = pack2(-32768, -32768);
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const int64_t gi = i0 + ty * 4 + a;
-        const int la = gi < m ? aline[gi] : 0;
-        const uint32_t lap = pack2(la, la);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const uint32_t span = __vsub2(__vadd2(lap, lbp[b]), z[a][b]);
-            const uint32_t dead = __vcmples2(z[a][b], lim);  // 0xffff per half where z <= -8000
-            best = __vmaxs2(best, (span & ~dead) | (0x80008000u & dead));
-        }
-    }
-    int esc = max(int(int16_t(best & 0xffffu)), int(int16_t(best >> 16)));
-    esc = warp_max(max(esc, 0));
+    int esc = warp_max(max(span_max(0x80008000u), 0));
     if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(esc_out, esc);
-    if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && ran_flag) *ran_flag = 1;
 }
 
 // [lines][blocks] -> [blocks][lines] (stage export of esc_coarsened, which

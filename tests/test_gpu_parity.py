@@ -104,6 +104,29 @@ def test_esc_sparse_rows(gpu, port):
     assert gpu.esc_coarsened(a, b, 64) == port.esc_coarsened(a, b, 64)
 
 
+@pytest.mark.parametrize("where", ["first", "late", "none"])
+@pytest.mark.parametrize("block_len", [256, 32])
+def test_esc_tile_pruning_keeps_the_maximum(gpu, port, where, block_len):
+    """The ESC kernel stops a tile once an upper bound of its spans (from the blocks
+    seen so far) cannot exceed the maximum other tiles already published. Narrow
+    exponents everywhere (U(1,2): every tile prunes after one block) with one
+    (row, column) pair whose span is 40+1: a single large element in different
+    blocks of an otherwise tiny row of A and column of B, in the first tile or in
+    a late one, and with block_len 32 so that tile sees several staged rounds."""
+    m, n, k = 1100, 1300, 2304
+    a = port.gen_uniform_rect(m, k, 1, 1.0, 2.0)
+    b = port.gen_uniform_rect(k, n, 2, 1.0, 2.0)
+    if where != "none":
+        i, j = (3, 5) if where == "first" else (m - 7, n - 11)
+        a[i, :] *= 2.0 ** -40
+        a[i, 5 * block_len + 3] = 1.5   # the row's only large element, in block 5
+        b[:, j] *= 2.0 ** -40
+        b[3 * block_len + 1, j] = 1.25  # the column's, in block 3
+    got = gpu.esc_coarsened(a, b, block_len)
+    assert got == port.esc_coarsened(a, b, block_len)
+    assert got[0] == (41 if where != "none" else 1)
+
+
 # ---- K3: slicing -----------------------------------------------------------------------------
 @pytest.mark.parametrize("slices", [1, 2, 4, 7, 8, 9, 12, 16, 17, 18, 32])
 @pytest.mark.parametrize("orient", [0, 1])
