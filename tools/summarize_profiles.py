@@ -101,7 +101,7 @@ for d, u in raw(os.path.join(G, f"{tag}_guard.ncu-rep")):
                 "frac_of_6551_GBps": round(byt / (t_us * 1e-6) / 1e9 / 6551, 3)}
 rd, wr = val(ig, igu, "dram__bytes_read.sum"), val(ig, igu, "dram__bytes_write.sum")
 summ = {
-    "round": 1, "tag": tag,
+    "round": 2, "tag": tag,
     "source": "ncu --set full --clock-control none (tools/profile_round.sh): igemm_kernel<64> = second call of "
               "tools/one_call.py (8192^3, U(1,2), s = 7, 34 pairs); guard kernels = second call",
     "igemm_kernel": {
