@@ -20,6 +20,7 @@
 // when the device plan says "emulated" the predicated launch costs one small
 // wave that reads the plan and exits, not a full grid of tiles.
 #include "igemm.cuh"
+#include "tc.cuh"
 
 namespace adpb200 {
 
@@ -295,6 +296,136 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
     }
 }
 
+// ---- fast flavour, warp-specialised: producers and consumers on mbarriers ---------------
+// 4 producer warps issue the cp.async copies of a stage and signal its `full`
+// mbarrier when they land (cp.async.mbarrier.arrive.noinc); 8 consumer warps (the
+// same 64 x 32 DMMA tiles) wait on `full`, compute, and release the stage on
+// `empty`. No CTA-wide barrier in the k loop, so a scheduler's two consumer warps
+// are never held back by the slowest warp of another scheduler, and the copy
+// issue work leaves the consumer warps. Registers: setmaxnreg 56 / 224.
+#ifndef ADPB200_DMMA_WS_STAGES
+#define ADPB200_DMMA_WS_STAGES 4
+#endif
+constexpr int kWsStages = ADPB200_DMMA_WS_STAGES;
+constexpr int kWsProd = 4, kWsCons = 8, kWsThreads = (kWsProd + kWsCons) * 32;
+constexpr size_t kWsHeader = 128;  // 2 * kWsStages mbarriers
+constexpr size_t kDmmaWsSmem = kWsHeader + size_t(kWsStages) * 2 * kOpDoubles * sizeof(double);
+static_assert(2 * kWsStages * 8 <= kWsHeader, "mbarrier header");
+
+template <bool kAL, bool kBL>
+__global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, LineView b, double alpha, double beta,
+                                                                const double* __restrict__ c_in, int64_t ldc_in,
+                                                                double* __restrict__ c_out, int64_t ldc,
+                                                                const Plan* plan) {
+    if (plan && plan->path != ADPB200_PATH_NATIVE) return;
+    extern __shared__ __align__(128) unsigned char dws[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(dws);
+    uint64_t* empty = full + kWsStages;
+    double* ops = reinterpret_cast<double*>(dws + kWsHeader);
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    if (tid == 0) {
+        for (int st = 0; st < kWsStages; ++st) {
+            tc::mbar_init(&full[st], kWsProd * 32);
+            tc::mbar_init(&empty[st], kWsCons);
+        }
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    const int64_t K = a.len;
+    const int64_t tiles_m = (a.lines + kDT - 1) / kDT, tiles_n = (b.lines + kDT - 1) / kDT;
+    const int64_t nk = (K + kDK - 1) / kDK;
+    auto coords = [&](int64_t tile, int64_t& i0, int64_t& j0) {
+        const int64_t group = int64_t(kGroupTiles) * tiles_n;
+        const int64_t first_m = (tile / group) * kGroupTiles;
+        const int64_t gm = tiles_m - first_m < kGroupTiles ? tiles_m - first_m : kGroupTiles;
+        const int64_t local = tile % group;
+        i0 = (first_m + local % gm) * kDT;
+        j0 = (local / gm) * kDT;
+    };
+    if (warp < kWsProd) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::);
+        const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
+        const OpTile<kBL, kWsProd * 32> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+        const uint32_t s0 = tc::smem_u32(ops);
+        int st = 0;
+        uint32_t ph = 0;
+        for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
+            int64_t i0, j0;
+            coords(tile, i0, j0);
+            for (int64_t t = 0; t < nk; ++t) {
+                tc::mbar_wait(&empty[st], ph ^ 1);
+                const uint32_t sa = s0 + uint32_t(st) * 2u * kOpDoubles * 8u;
+                ta.load(sa, i0, t * kDK, tid);
+                tb.load(sa + kOpDoubles * 8u, j0, t * kDK, tid);
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(&full[st]))
+                             : "memory");
+                if (++st == kWsStages) {
+                    st = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::);
+    const int cw = warp - kWsProd;
+    const int wm = cw % 2, wn = cw / 2;  // warp tile: lines [64 wm, +64) of A x [32 wn, +32) of B
+    const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
+    const OpTile<kBL, kWsProd * 32> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+    const int fr = lane / 4, fk = lane % 4;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
+        int64_t i0, j0;
+        coords(tile, i0, j0);
+        double acc[8][4][2];
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int64_t t = 0; t < nk; ++t) {
+            tc::mbar_wait(&full[st], ph);
+            const double* As = ops + size_t(st) * 2 * kOpDoubles;
+            const double* Bs = As + kOpDoubles;
+#pragma unroll
+            for (int kk = 0; kk < kDK; kk += 4) {
+                double af[8], bf[4];
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) af[mi] = ta.frag(As, wm * 64 + mi * 8 + fr, kk + fk);
+#pragma unroll
+                for (int ni = 0; ni < 4; ++ni) bf[ni] = tb.frag(Bs, wn * 32 + ni * 8 + fr, kk + fk);
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+                    for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[st]);
+            if (++st == kWsStages) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        // C fragment: line i = 8 mi + lane/4 of A, lines j = 8 ni + 2 (lane%4) + {0, 1} of B
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = j0 + wn * 32 + ni * 8 + 2 * fk + h;
+                if (j >= b.lines) continue;
+#pragma unroll
+                for (int mi = 0; mi < 8; ++mi) {
+                    const int64_t i = i0 + wm * 64 + mi * 8 + fr;
+                    if (i >= a.lines) continue;
+                    double v = __dmul_rn(alpha, acc[mi][ni][h]);
+                    if (beta != 0.0) v = __dadd_rn(v, __dmul_rn(beta, c_in[i + j * ldc_in]));
+                    c_out[i + j * ldc] = v;
+                }
+            }
+    }
+}
+
 int resident_grid(const void* fn, int threads, size_t smem, int64_t tiles) {
     static int sms = 0;
     if (!sms) sms = num_sms();
@@ -311,7 +442,26 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
                    int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch,
                    int flavour) {
     if (a.lines == 0 || b.lines == 0) return;
-    if (flavour == ADPB200_FALLBACK_FAST) {
+#ifndef ADPB200_DMMA_WS
+#define ADPB200_DMMA_WS 1
+#endif
+    if (flavour == ADPB200_FALLBACK_FAST && ADPB200_DMMA_WS) {
+        using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
+                            const Plan*);
+        static const Fn fns[4] = {dmma_ws_kernel<false, false>, dmma_ws_kernel<false, true>,
+                                  dmma_ws_kernel<true, false>, dmma_ws_kernel<true, true>};
+        static bool attr = false;
+        if (!attr) {
+            for (Fn f : fns)
+                cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kDmmaWsSmem));
+            attr = true;
+        }
+        const Fn fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
+        const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
+        const int grid = resident_grid(reinterpret_cast<const void*>(fn), kWsThreads, kDmmaWsSmem, tiles);
+        fn<<<grid, kWsThreads, kDmmaWsSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+    } else if (flavour == ADPB200_FALLBACK_FAST) {
         // operand layouts in shared memory follow the contiguous direction in HBM
         using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
                             const Plan*);
