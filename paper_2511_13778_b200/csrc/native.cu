@@ -27,71 +27,103 @@ namespace adpb200 {
 namespace {
 
 // ---- reference order (SIMT) ---------------------------------------------------------
-constexpr int kT = 64, kKT = 16;
+// 128 x 128 CTA tiles, 16 x 16 threads with 8 x 8 outputs each (rows tx + 16 r, columns
+// ty + 16 c): per k, 8 + 8 shared-memory reads feed 64 multiply-add pairs, so the FP64
+// pipe (one DMUL and one DADD per term, no FMA), not shared memory, bounds the loop.
+// k is staged 16 at a time through a 2-deep cp.async ring (zero-filled out of range);
+// a full stage runs fully unrolled, the ragged last one term by term — always
+// ascending k.
+constexpr int kT = 128, kKT = 16, kTP = kT + 1;
+constexpr size_t kNativeSmem = size_t(2) * 2 * kKT * kTP * sizeof(double);
 
-__global__ void __launch_bounds__(256) native_kernel(LineView a, LineView b, double alpha, double beta,
-                                                     const double* __restrict__ c_in, int64_t ldc_in,
-                                                     double* __restrict__ c_out, int64_t ldc, const Plan* plan) {
+__device__ __forceinline__ void cp_async8z(uint32_t dst, const double* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
+}
+
+__global__ void __launch_bounds__(256, 1) native_kernel(LineView a, LineView b, double alpha, double beta,
+                                                        const double* __restrict__ c_in, int64_t ldc_in,
+                                                        double* __restrict__ c_out, int64_t ldc, const Plan* plan) {
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
-    __shared__ double As[2][kKT][kT + 1];
-    __shared__ double Bs[2][kKT][kT + 1];
+    extern __shared__ __align__(16) double nsm[];
+    // [buf][operand][k][line]
+    auto tileA = [&](int buf) { return nsm + size_t(buf) * 2 * kKT * kTP; };
+    auto tileB = [&](int buf) { return nsm + (size_t(buf) * 2 + 1) * kKT * kTP; };
     const int tid = threadIdx.x;
     const int tx = tid % 16, ty = tid / 16;
     const int64_t K = a.len;
     const int64_t tiles_m = (a.lines + kT - 1) / kT, tiles_n = (b.lines + kT - 1) / kT;
+    const int64_t nk = (K + kKT - 1) / kKT;
 
     for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
         const int64_t i0 = (tile % tiles_m) * kT, j0 = (tile / tiles_m) * kT;
         auto load = [&](int buf, int64_t k0) {
-            // A tile: 64 lines x 16 positions; B tile: 64 lines x 16 positions.
+            // 128 lines x 16 positions per operand, 8 elements per thread; lines innermost
+            // when they are adjacent in memory, positions innermost otherwise
+            const uint32_t sa = uint32_t(__cvta_generic_to_shared(tileA(buf)));
+            const uint32_t sb = uint32_t(__cvta_generic_to_shared(tileB(buf)));
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                int e = tid + q * 256;
+            for (int q = 0; q < kT * kKT / 256; ++q) {
+                const int e = tid + q * 256;
                 int li, kk;
                 if (a.ls == 1) { li = e % kT; kk = e / kT; }
                 else { kk = e % kKT; li = e / kKT; }
-                int64_t gi = i0 + li, gk = k0 + kk;
-                As[buf][kk][li] = (gi < a.lines && gk < K) ? a.ptr[gi * a.ls + gk * a.ps] : 0.0;
+                const int64_t gi = i0 + li, gk = k0 + kk;
+                const bool oka = gi < a.lines && gk < K;
+                cp_async8z(sa + uint32_t(kk * kTP + li) * 8u, oka ? a.ptr + gi * a.ls + gk * a.ps : a.ptr, oka);
                 int lj, kj;
                 if (b.ls == 1) { lj = e % kT; kj = e / kT; }
                 else { kj = e % kKT; lj = e / kKT; }
-                int64_t gj = j0 + lj, gk2 = k0 + kj;
-                Bs[buf][kj][lj] = (gj < b.lines && gk2 < K) ? b.ptr[gj * b.ls + gk2 * b.ps] : 0.0;
+                const int64_t gj = j0 + lj, gk2 = k0 + kj;
+                const bool okb = gj < b.lines && gk2 < K;
+                cp_async8z(sb + uint32_t(kj * kTP + lj) * 8u, okb ? b.ptr + gj * b.ls + gk2 * b.ps : b.ptr, okb);
             }
+            asm volatile("cp.async.commit_group;\n" ::);
         };
 
-        double acc[4][4];
+        double acc[8][8];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+            for (int c = 0; c < 8; ++c) acc[r][c] = 0.0;
 
-        const int64_t nk = (K + kKT - 1) / kKT;
         if (nk > 0) load(0, 0);
-        __syncthreads();
         for (int64_t t = 0; t < nk; ++t) {
             const int buf = int(t & 1);
-            if (t + 1 < nk) load(buf ^ 1, (t + 1) * kKT);
-            const int kmax = (K - t * kKT) < kKT ? int(K - t * kKT) : kKT;
-            for (int kk = 0; kk < kmax; ++kk) {  // ascending k, never reordered
-                double av[4], bv[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) av[r] = As[buf][kk][tx + 16 * r];
-#pragma unroll
-                for (int c = 0; c < 4; ++c) bv[c] = Bs[buf][kk][ty + 16 * c];
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(av[r], bv[c]));
+            if (t + 1 < nk) {
+                load(buf ^ 1, (t + 1) * kKT);
+                asm volatile("cp.async.wait_group 1;\n" ::);
+            } else {
+                asm volatile("cp.async.wait_group 0;\n" ::);
             }
-            __syncthreads();
+            __syncthreads();  // stage t landed for every thread
+            const double* As = tileA(buf);
+            const double* Bs = tileB(buf);
+            auto term = [&](int kk) {  // one k: ascending, never reordered
+                double av[8], bv[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) av[r] = As[kk * kTP + tx + 16 * r];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) bv[c] = Bs[kk * kTP + ty + 16 * c];
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc[r][c] = __dadd_rn(acc[r][c], __dmul_rn(av[r], bv[c]));
+            };
+            const int kmax = (K - t * kKT) < kKT ? int(K - t * kKT) : kKT;
+            if (kmax == kKT) {
+#pragma unroll
+                for (int kk = 0; kk < kKT; ++kk) term(kk);
+            } else {
+                for (int kk = 0; kk < kmax; ++kk) term(kk);
+            }
+            __syncthreads();  // stage t consumed before the copy into its buffer is issued
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 8; ++c) {
             const int64_t j = j0 + ty + 16 * c;
             if (j >= b.lines) continue;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < 8; ++r) {
                 const int64_t i = i0 + tx + 16 * r;
                 if (i >= a.lines) continue;
                 double v = __dmul_rn(alpha, acc[r][c]);
@@ -99,7 +131,6 @@ __global__ void __launch_bounds__(256) native_kernel(LineView a, LineView b, dou
                 c_out[i + j * ldc] = v;
             }
         }
-        __syncthreads();  // the next tile's first load reuses buffer 0
     }
 }
 
@@ -479,9 +510,15 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), kDmmaWarps * 32, kDmmaSmem, tiles);
         fn<<<grid, kDmmaWarps * 32, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
     } else {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(native_kernel),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNativeSmem));
+            attr = true;
+        }
         const int64_t tiles = ((a.lines + kT - 1) / kT) * ((b.lines + kT - 1) / kT);
-        const int grid = resident_grid(reinterpret_cast<const void*>(native_kernel), 256, 0, tiles);
-        native_kernel<<<grid, 256, 0, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+        const int grid = resident_grid(reinterpret_cast<const void*>(native_kernel), 256, kNativeSmem, tiles);
+        native_kernel<<<grid, 256, kNativeSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
     }
     ++*nlaunch;
 }
