@@ -49,11 +49,13 @@ def parse():
                    help="ESC method of the timed calls: the reference's coarsened ESC (default) or the "
                         "certified ESC option (single-GPU paths)")
     p.add_argument("--dist", choices=["fused", "pull", "allgather"], default="allgather",
-                   help="N > 1: allgather (default) = NCCL all-gather of the B planes overlapped with the "
+                   help="N > 1: allgather (default: each plane byte crosses NVLink once, NCCL; one 8-byte host "
+                        "read per call sizes it) = NCCL all-gather of the B planes overlapped with the "
                         "own-column GEMM (phases 5/6); fused = the GEMM reads every rank's B planes in place "
-                        "over NVLink (CUDA IPC peer mappings, phase 7); pull = the copy engines pull each "
-                        "peer's planes while the GEMM of the previous rank's columns runs (phase 7 per rank). "
-                        "fused / pull are not yet timed on an NVLink node")
+                        "over NVLink (CUDA IPC peer mappings, phase 7), ordered by stream-side flags with no "
+                        "host read or barrier; pull = the copy engines pull each peer's planes while the GEMM "
+                        "of the previous rank's columns runs (phase 7 per rank). fused / pull are not yet timed "
+                        "on an NVLink node")
     p.add_argument("--quick", action="store_true", help="skip the side measurements")
     p.add_argument("--soak", type=float, default=2.0,
                    help="seconds of untimed steps between the warm-up and the timed region, so the timed region "

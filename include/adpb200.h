@@ -228,9 +228,31 @@ int adpb200_dgemm_rows(adpb200_handle handle, int phase, int64_t m_global, char 
  *            after a pull of that rank's record into local memory
  *            (adpb200_copy_async on a copy stream), pipelines the transfer of
  *            rank r+1's planes with the GEMM of rank r's columns.
+ *            nsl = 0 (host-sync-free form): the plane count and the path stay on
+ *            the device. Every GEMM variant and the native fallback are launched
+ *            predicated on the plan; the fallback reads B's FP64 columns from the
+ *            ranks' slab buffers, where phase 8 put them.
+ *   phase 8  (fused form, right after phase 3) on the native fallback only (device
+ *            decided): copy this rank's FP64 B slab into `slab`.
+ * Host-sync-free fused sequence per call (no host read, no host barrier): wait
+ * until every peer's "consumed" flag of this slab buffer reaches epoch-1, phase 3,
+ * phase 8, write the own "ready" flag = epoch, wait until every peer's "ready" flag
+ * reaches epoch, phase 7 with nsl = 0, write the own "consumed" flag = epoch —
+ * the flags are the last bytes of each slab buffer (adpb200_dist_flag_offset),
+ * written and waited on by the streams themselves (adpb200_stream_write_flag /
+ * adpb200_stream_wait_geq, CUDA stream memory operations, also across processes
+ * on IPC mappings), epoch = 1, 2, ... per buffer.
  * Same decision and slice count on every rank: the assembled C is
  * bit-identical to the single-GPU adpb200_dgemm('N'/transa, 'N'). */
 int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* opt, int64_t out[4]);
+/* Byte offset of a slab buffer's flag (which = 0 ready, 1 consumed) for a buffer of
+ * slab_bytes (= adpb200_dist_sizes out[3]). */
+int64_t adpb200_dist_flag_offset(int64_t slab_bytes, int which);
+/* Stream-ordered 32-bit flags (CUDA stream memory operations): the stream waits until
+ * *flag >= value; the stream writes *flag = value after its prior work. flag may be
+ * an IPC / peer mapping. */
+int adpb200_stream_wait_geq(const void* flag, uint32_t value, void* stream);
+int adpb200_stream_write_flag(void* flag, uint32_t value, void* stream);
 /* Slab buffers for phase 7, shared between the ranks' processes over CUDA IPC
  * (NVLink peer mappings): alloc exports a cudaMalloc'd buffer's 64-byte handle,
  * open maps a peer's handle (lazy peer access), close / free release them. */

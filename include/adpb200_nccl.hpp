@@ -37,6 +37,7 @@ struct PeerSlabs {
     bool pull = false;           // copy engines pull each peer's record under the GEMM (phase 7 per rank)
     void* own[2] = {nullptr, nullptr};
     std::vector<void*> ptrs[2];  // entry r: rank r's buffer in this process
+    uint32_t epoch[2] = {0, 0};  // uses of each buffer so far (the in-place path's flag values)
 };
 
 inline int peer_slabs_create(PeerSlabs& ps, ncclComm_t comm, int rank, int world, int device, int64_t n, int64_t k,
@@ -79,8 +80,12 @@ inline void peer_slabs_destroy(PeerSlabs& ps) {
 }
 
 // Returns an adpb200 status (0 ok, 2 runtime incl. CUDA/NCCL failures, 3 contract).
-// peers (optional, from peer_slabs_create for this n, k): the fused phase 7 —
-// no plane all-gather; after a barrier every rank's GEMM reads the planes in place.
+// peers (optional, from peer_slabs_create for this n, k): the fused phase 7 — no
+// plane all-gather. In place (default): no host read and no host barrier — the
+// streams order the ranks through the slab buffers' ready / consumed flags (CUDA
+// stream memory operations on the IPC mappings) and the device plan decides between
+// the GEMM and the native fallback (phase 8 / phase 7 with nsl = 0). Pulled
+// (peers->pull): one 8-byte host read sizes the copies, then a barrier.
 inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int world, char transa, int64_t m_global,
                            int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda,
                            const double* B_slab, double beta, double* C, int64_t ldc, const adpb200_options* opt,
@@ -101,7 +106,9 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
         return adpb200_dgemm_dist(h, p, m_global, world, rank, transa, m, n, k, alpha, A, lda, B_slab, beta, C, ldc,
                                   opt, trace_dev, bl, ba, xchg, slab, g, nsl, st);
     };
-    const std::vector<void*>* pp = peers ? &peers->ptrs[peers->calls++ % 2] : nullptr;
+    const int buf = peers ? peers->calls++ % 2 : 0;
+    const std::vector<void*>* pp = peers ? &peers->ptrs[buf] : nullptr;
+    const bool in_place = pp && !peers->pull;
     rc = cu(cudaMallocAsync(&bl, size_t(nrec) * 4, st));
     if (!rc) rc = cu(cudaMallocAsync(&ba, size_t(nrec) * 4 * world, st));
     if (!rc) rc = cu(cudaMallocAsync(&xchg, 8, st));
@@ -114,6 +121,27 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
     // 2: ESC of the local rows against every column; max-allreduce {exceptional, esc}
     if (!rc) rc = phase(2, nullptr, 0);
     if (!rc) rc = nc(ncclAllReduce(xchg, xchg, 2, ncclInt32, ncclMax, comm, st));
+    if (in_place) {
+        // host-sync-free fused path: slice into this buffer only after every peer has
+        // finished reading it (its previous use), publish it, wait for every peer's
+        // slab, run the device-decided phase 7, then release this call's slabs
+        const uint32_t e = ++peers->epoch[buf];
+        const int64_t off_ready = adpb200_dist_flag_offset(cap_bytes, 0);
+        const int64_t off_used = adpb200_dist_flag_offset(cap_bytes, 1);
+        for (int r = 0; r < world && !rc; ++r)
+            if (r != rank) rc = adpb200_stream_wait_geq(static_cast<char*>((*pp)[r]) + off_used, e - 1, st);
+        if (!rc) rc = phase(3, nullptr, 0);
+        if (!rc) rc = phase(8, nullptr, 0);
+        if (!rc) rc = adpb200_stream_write_flag(slab + off_ready, e, st);
+        for (int r = 0; r < world && !rc; ++r)
+            if (r != rank) rc = adpb200_stream_wait_geq(static_cast<char*>((*pp)[r]) + off_ready, e, st);
+        if (!rc) rc = phase(7, pp->data(), 0);
+        if (!rc) rc = adpb200_stream_write_flag(slab + off_used, e, st);
+        if (bl) cudaFreeAsync(bl, st);
+        if (ba) cudaFreeAsync(ba, st);
+        if (xchg) cudaFreeAsync(xchg, st);
+        return rc;
+    }
     // 3: decision, slicing; the host learns how many planes travel
     if (!rc) rc = phase(3, nullptr, 0);
     if (!rc) rc = cu(cudaMemcpyAsync(xh, xchg, 8, cudaMemcpyDeviceToHost, st));
@@ -121,11 +149,10 @@ inline int dgemm_dist_nccl(adpb200_handle h, ncclComm_t comm, int rank, int worl
     if (!rc) rc = adpb200_dist_decision(opt, xh, m_global, n, k, dec);
     const int nsl = dec[2];
     if (!rc && nsl > 0 && pp) {
-        // every rank's slab is sliced (the host sync above) once this barrier passes
+        // pulled: every rank's slab is sliced (the host sync above) once this barrier passes
         rc = nc(ncclAllReduce(xchg, xchg, 1, ncclInt32, ncclMax, comm, st));
         if (!rc) rc = cu(cudaStreamSynchronize(st));
-        if (!rc && !peers->pull) rc = phase(7, pp->data(), nsl);
-        if (!rc && peers->pull) {
+        if (!rc) {
             // own columns first, then rank by rank: the copy engines pull rank r's record
             // into local memory on a side stream while the GEMM of the previous rank runs
             const int64_t rec = hdr + int64_t(nsl) * plane_bytes;

@@ -119,6 +119,9 @@ def lib() -> C.CDLL:
         "adpb200_ipc_close": (C.c_int, [vp]),
         "adpb200_ipc_free": (C.c_int, [vp]),
         "adpb200_copy_async": (C.c_int, [vp, vp, i64, vp]),
+        "adpb200_dist_flag_offset": (i64, [i64, C.c_int]),
+        "adpb200_stream_wait_geq": (C.c_int, [vp, C.c_uint32, vp]),
+        "adpb200_stream_write_flag": (C.c_int, [vp, C.c_uint32, vp]),
         "adpb200_geqrf_blocked": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, popt, vp]),
         "adpb200_qr_materialize_q": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp]),
         "adpb200_qr_residual": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, vp]),
@@ -146,6 +149,7 @@ EXPORTED = (
     "adpb200_native_gemm", "adpb200_profile_enable", "adpb200_profile_read", "adpb200_recompose", "adpb200_esc_exact",
     "adpb200_dist_sizes", "adpb200_dist_decision", "adpb200_dgemm_dist", "adpb200_ipc_alloc",
     "adpb200_ipc_open", "adpb200_ipc_close", "adpb200_ipc_free", "adpb200_copy_async",
+    "adpb200_dist_flag_offset", "adpb200_stream_wait_geq", "adpb200_stream_write_flag",
     "adpb200_geqrf_blocked", "adpb200_qr_materialize_q", "adpb200_qr_residual",
     "adpb200_dd_gemm", "adpb200_error_report", "adpb200_gen_uniform_rect", "adpb200_gen_test2",
 )

@@ -477,6 +477,16 @@ struct DistIO {
 
 int64_t slab_hdr(int64_t nr) { return (int64_t)align_up(size_t(nr) * 4, 1024); }
 
+// Fused multi-GPU path, native fallback: the rank's FP64 B slab (k x nr, compact) is
+// copied into its shared slab buffer, where every peer's native GEMM reads it. Runs
+// only when the device plan says native (no host decision in the fused path).
+__global__ void copy_if_native_kernel(const Plan* plan, const double* __restrict__ src, double* __restrict__ dst,
+                                      int64_t count) {
+    if (plan->path != ADPB200_PATH_NATIVE) return;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
 int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace, cudaStream_t st,
              int phase, const DistIO& io) {
     const int cap = plane_cap(o, 0, 0);
@@ -565,16 +575,37 @@ int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adp
     // tiles that only need this rank's own B columns (phase 5, `gathered` = own slab
     // record), the other tiles follow once the records are in (phase 6)
     if (phase >= 4 && P.M == 0) return ADPB200_OK;  // no rows on this rank: nothing to compute
+    if (phase == 8) {
+        // fused path, after phase 3: on the native fallback (device-decided) the FP64 B
+        // slab goes into this rank's shared slab buffer for the peers' native GEMMs
+        const int64_t count = nr * P.K;
+        copy_if_native_kernel<<<num_sms() * 4, 256, 0, st>>>(plan, P.b.ptr, reinterpret_cast<double*>(io.slab), count);
+        ++*nl;
+        return cuda_check(cudaGetLastError(), "dist phase 8");
+    }
     if (phase == 7) {
         // fused all-gather -> GEMM: the GEMM's TMA reads every rank's slab record in
-        // place (peer memory over NVLink), tile by tile; no gathered copy, no NCCL
+        // place (peer memory over NVLink), tile by tile; no gathered copy, no NCCL.
+        // nsl = 0: the decision stays on the device — every GEMM variant and the native
+        // fallback (B's FP64 columns from the peers' buffers, phase 8) are launched
+        // predicated on the plan, so no host read precedes this launch.
         const GemmArgs g = product_args(h, Lw, P, plan, nullptr);
+        const int8_t* const* slabs = static_cast<const int8_t* const*>(io.gathered);
         tm.begin(4);
-        const int prc = launch_igemm_peer(at<int8_t>(h, Lw.planes_a), Lw.slots_a, Lw.pitch / 32, cap,
-                                          static_cast<const int8_t* const*>(io.gathered), io.world, nr, slab_hdr(nr),
-                                          io.nsl, g, st, nl);
+        const int prc = launch_igemm_peer(at<int8_t>(h, Lw.planes_a), Lw.slots_a, Lw.pitch / 32, cap, slabs, io.world,
+                                          nr, slab_hdr(nr), io.nsl, g, st, nl);
         tm.end(4);
         if (prc) return fail(ADPB200_ERR_RUNTIME, "peer GEMM launch failed (tensor map encoding or kernel resources)");
+        if (io.nsl == 0) {
+            PeerB pb{};
+            pb.nr = nr;
+            pb.world = io.world;
+            for (int r = 0; r < io.world; ++r) pb.p[r] = reinterpret_cast<const double*>(slabs[r]);
+            const LineView bpeer{nullptr, P.N, P.K, P.K, 1};
+            tm.begin(5);
+            launch_native(P.a, bpeer, P.alpha, P.beta, P.c_in, P.ldc_in, P.c_out, P.ldc, plan, st, nl, o.fallback, &pb);
+            tm.end(5);
+        }
         return cuda_check(cudaGetLastError(), "dist phase 7");
     }
     if ((phase == 5 || phase == 6) && io.nsl > 0) {
@@ -1106,8 +1137,48 @@ int adpb200_dist_sizes(int64_t n, int64_t k, int world, const adpb200_options* o
     out[0] = 2 * t * nr + nr + int64_t(cplanes) * nr * ((kw + 31) / 32 * 32) / 4;
     out[1] = slab_hdr(nr);
     out[2] = pitch * nr;
-    out[3] = out[1] + int64_t(plane_cap(o, 0, 0)) * out[2];
+    // a slab buffer holds the record (header + cap planes) or, on the fused path's native
+    // fallback, the FP64 slab; its last kDistFlagBytes are the fused path's ready /
+    // consumed flags (adpb200_dist_flag_offset)
+    out[3] = std::max(out[1] + int64_t(plane_cap(o, 0, 0)) * out[2], nr * k * 8) + kDistFlagBytes;
     return ADPB200_OK;
+}
+
+int64_t adpb200_dist_flag_offset(int64_t slab_bytes, int which) {
+    // which = 0: "ready" (this rank's slab of the current call is sliced), 1: "consumed"
+    // (this rank's GEMM has finished reading every peer's slab of that call)
+    return slab_bytes - kDistFlagBytes + (which ? 128 : 0);
+}
+
+namespace {
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+void* driver_sym(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        return p;
+    return nullptr;
+}
+}  // namespace
+
+int adpb200_stream_wait_geq(const void* flag, uint32_t value, void* stream) {
+    static StreamWaitValue32Fn fn = reinterpret_cast<StreamWaitValue32Fn>(driver_sym("cuStreamWaitValue32"));
+    if (!fn) return fail(ADPB200_ERR_RUNTIME, "cuStreamWaitValue32 unavailable");
+    if (!flag) return fail(3, "stream_wait_geq: null flag");
+    const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                          CU_STREAM_WAIT_VALUE_GEQ);
+    return r == CUDA_SUCCESS ? ADPB200_OK : fail(ADPB200_ERR_RUNTIME, "cuStreamWaitValue32 failed");
+}
+
+int adpb200_stream_write_flag(void* flag, uint32_t value, void* stream) {
+    static StreamWriteValue32Fn fn = reinterpret_cast<StreamWriteValue32Fn>(driver_sym("cuStreamWriteValue32"));
+    if (!fn) return fail(ADPB200_ERR_RUNTIME, "cuStreamWriteValue32 unavailable");
+    if (!flag) return fail(3, "stream_write_flag: null flag");
+    // default flags: the write is ordered after (and made visible after) the stream's prior work
+    const CUresult r = fn(static_cast<CUstream>(stream), reinterpret_cast<CUdeviceptr>(flag), value,
+                          CU_STREAM_WRITE_VALUE_DEFAULT);
+    return r == CUDA_SUCCESS ? ADPB200_OK : fail(ADPB200_ERR_RUNTIME, "cuStreamWriteValue32 failed");
 }
 
 int adpb200_ipc_alloc(int device, int64_t bytes, void** ptr, uint8_t handle[64]) {
@@ -1116,6 +1187,13 @@ int adpb200_ipc_alloc(int device, int64_t bytes, void** ptr, uint8_t handle[64])
     int rc = cuda_check(cudaSetDevice(device), "cudaSetDevice");
     if (!rc) rc = cuda_check(cudaMalloc(ptr, size_t(bytes)), "cudaMalloc(ipc)");
     if (rc) return rc;
+    // zeroed once: the fused path's flags start at epoch 0
+    rc = cuda_check(cudaMemset(*ptr, 0, size_t(bytes)), "cudaMemset(ipc)");
+    if (rc) {
+        cudaFree(*ptr);
+        *ptr = nullptr;
+        return rc;
+    }
     cudaIpcMemHandle_t hd;
     rc = cuda_check(cudaIpcGetMemHandle(&hd, *ptr), "cudaIpcGetMemHandle");
     if (rc) {
@@ -1182,9 +1260,10 @@ int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world,
                        int32_t* bstats_local, const int32_t* bstats_all, int32_t* xchg, int8_t* slab,
                        const void* gathered, int nsl, void* stream) {
     if (!h) return fail(ADPB200_ERR_RUNTIME, "dgemm_dist: null handle");
-    if (phase < 1 || phase > 7) return fail(3, "dgemm_dist: phase must be 1..7");
-    if (phase == 7 && (world > kMaxPeers || nsl < 1))
-        return fail(3, "dgemm_dist: phase 7 needs world <= 8 and nsl >= 1 (emulated path)");
+    if (phase < 1 || phase > 8) return fail(3, "dgemm_dist: phase must be 1..8");
+    if (phase == 7 && (world > kMaxPeers || nsl < 0))
+        return fail(3, "dgemm_dist: phase 7 needs world <= 8 and nsl >= 0 (0: decided on the device)");
+    if (phase == 8 && !slab) return fail(3, "dgemm_dist: phase 8 needs the slab buffer");
     if (rank < 0 || rank >= world) return fail(3, "dgemm_dist: rank out of range");
     adpb200_options o;
     if (opt) o = *opt;
@@ -1199,9 +1278,9 @@ int adpb200_dgemm_dist(adpb200_handle h, int phase, int64_t m_global, int world,
     if (ldc < std::max<int64_t>(1, m)) return fail(3, "dgemm: ldc too small");
     if (beta != 0.0 && !C) return fail(3, "dgemm_dist: beta != 0 needs C");
     if ((phase == 1 && !bstats_local) || (phase == 2 && (!bstats_all || !xchg)) ||
-        (phase == 3 && (!xchg || !slab || !bstats_local)) || (phase >= 4 && !gathered))
+        (phase == 3 && (!xchg || !slab || !bstats_local)) || (phase >= 4 && phase <= 7 && !gathered))
         return fail(3, "dgemm_dist: missing exchange buffer for this phase");
-    if (phase >= 4 && (nsl < 0 || nsl > plane_cap(o, 0, 0))) return fail(3, "dgemm_dist: bad nsl");
+    if (phase >= 4 && phase <= 7 && (nsl < 0 || nsl > plane_cap(o, 0, 0))) return fail(3, "dgemm_dist: bad nsl");
     Problem P{};
     P.M = m;
     P.N = n;

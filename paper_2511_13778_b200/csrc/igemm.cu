@@ -312,7 +312,7 @@ constexpr int kMaxBox = 18;
 struct PlaneMaps {
     CUtensorMap a[kMaxBox];
     CUtensorMap b[kMaxBox];
-    CUtensorMap bp[kMaxPeers];  // fused peer mode: rank r's slab planes, box of nsl slices
+    CUtensorMap bp[kMaxPeers];  // fused peer mode: rank r's slab planes, box of one slice
 };
 
 struct alignas(16) SmemSched {
@@ -528,11 +528,20 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                     // pre-swizzled blocked planes viewed as (128 B = 4 lines, line/4, k-block,
                     // slice): a stage is one linear box per operand, 128-byte requests
                     if (g.peer_world > 0) {
-                        // B straight from the owning rank's slab record (NVLink peer memory)
+                        // B straight from the owning rank's slab record (NVLink peer memory), one
+                        // box per plane: the peer maps are encoded without the plane count, which
+                        // only the device plan knows (no host round trip before this launch)
                         const int r = int(nt / peer_tpr);
-                        tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
-                        tc::tma_load_4d(sb, &maps.bp[r], &hdr->full[stage], 0, int((nt - r * peer_tpr) * (NB / 4)),
-                                        int(kb), 0);
+                        const int prow = int((nt - r * peer_tpr) * (NB / 4));
+                        if (boxed) {
+                            tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
+                        } else {
+                            for (int d = 0; d < nsl; ++d)
+                                tc::tma_load_4d(sa + d * (kBM * kKB), map_a, &hdr->full[stage], 0,
+                                                int(mt * (kBM / 4)), int(kb), d);
+                        }
+                        for (int d = 0; d < nsl; ++d)
+                            tc::tma_load_4d(sb + d * (NB * kKB), &maps.bp[r], &hdr->full[stage], 0, prow, int(kb), d);
                     } else if (boxed) {
                         tc::tma_load_4d(sa, map_a, &hdr->full[stage], 0, int(mt * (kBM / 4)), int(kb), 0);
                         tc::tma_load_4d(sb, map_b, &hdr->full[stage], 0, int(nt * (NB / 4)), int(kb), 0);
@@ -977,24 +986,24 @@ struct PeerCacheEntry {
     const int8_t* pa = nullptr;
     const int8_t* peers[kMaxPeers] = {};
     int64_t slots_a = -1, nkb = -1, nr = -1, hdr = -1;
-    int cap = -1, world = -1, nsl = -1;
+    int cap = -1, world = -1;
     int ranks[kMaxPeers] = {};
     PlaneMaps maps;
 };
 
 template <int NB>
 int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap,
-                   const int8_t* const* peer_slabs, const int* ranks, int world, int64_t nr, int64_t hdr, int nsl,
+                   const int8_t* const* peer_slabs, const int* ranks, int world, int64_t nr, int64_t hdr,
                    const GemmArgs& g, cudaStream_t st) {
     bool hit = e.pa == planes_a && e.slots_a == slots_a && e.nkb == nkb && e.cap == cap && e.world == world &&
-               e.nr == nr && e.hdr == hdr && e.nsl == nsl;
+               e.nr == nr && e.hdr == hdr;
     for (int r = 0; hit && r < world; ++r) hit = e.peers[r] == peer_slabs[r] && e.ranks[r] == ranks[r];
     if (!hit) {
         const int nbox = cap < kMaxBox ? cap : kMaxBox;
         for (int i = 0; i < kMaxBox; ++i)
             if (!encode_plane_map(&e.maps.a[i], planes_a, slots_a, nkb, cap, kBM, i < nbox ? i + 1 : 1)) return -1;
         for (int r = 0; r < world; ++r)
-            if (!encode_plane_map(&e.maps.bp[r], peer_slabs[r] + hdr, nr, nkb, cap, NB, nsl)) return -1;
+            if (!encode_plane_map(&e.maps.bp[r], peer_slabs[r] + hdr, nr, nkb, cap, NB, 1)) return -1;
         e.pa = planes_a;
         e.slots_a = slots_a;
         e.nkb = nkb;
@@ -1002,7 +1011,6 @@ int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, i
         e.world = world;
         e.nr = nr;
         e.hdr = hdr;
-        e.nsl = nsl;
         for (int r = 0; r < world; ++r) {
             e.peers[r] = peer_slabs[r];
             e.ranks[r] = ranks[r];
@@ -1032,7 +1040,9 @@ int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, i
 int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int cap, const int8_t* const* peer_slabs,
                       int world, int64_t nr, int64_t hdr, int nsl, const GemmArgs& g, cudaStream_t st,
                       uint64_t* nlaunch) {
-    if (world < 1 || world > kMaxPeers || nsl < 1 || nsl > cap || nsl > kMaxBox || nr % 8 != 0) return -2;
+    // nsl: the plane count the caller expects (checked against the capacity), or 0 when
+    // only the device plan knows it; the kernel always takes it from the plan
+    if (world < 1 || world > kMaxPeers || nsl < 0 || nsl > cap || nr % 8 != 0) return -2;
     // the ranks whose columns this launch computes (null entries are skipped)
     const int8_t* act[kMaxPeers];
     int ranks[kMaxPeers];
@@ -1045,11 +1055,11 @@ int launch_igemm_peer(const int8_t* planes_a, int64_t slots_a, int64_t nkb, int 
     if (na == 0) return 0;
     static thread_local PeerCacheEntry cache[5];
     int rc = 0;
-    if (!rc) rc = launch_peer_nb<64>(cache[0], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<48>(cache[1], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<32>(cache[2], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<16>(cache[3], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
-    if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, nsl, g, st);
+    if (!rc) rc = launch_peer_nb<64>(cache[0], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, g, st);
+    if (!rc) rc = launch_peer_nb<48>(cache[1], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, g, st);
+    if (!rc) rc = launch_peer_nb<32>(cache[2], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, g, st);
+    if (!rc) rc = launch_peer_nb<16>(cache[3], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, g, st);
+    if (!rc) rc = launch_peer_nb<8>(cache[4], planes_a, slots_a, nkb, cap, act, ranks, na, nr, hdr, g, st);
     *nlaunch += 5;
     return rc;
 }

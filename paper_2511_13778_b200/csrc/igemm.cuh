@@ -13,6 +13,7 @@ constexpr size_t kPartialBytesPerCta = 131072;
 // Internal problem: C(i, j) = sum_l A(i, l) B(l, j), i < M (A-lines), j < N
 // (B-lines), both operands sliced K-major into planes [slice][line][pitch].
 constexpr int kMaxPeers = 8;  // ranks whose slab records one fused GEMM can read
+constexpr int64_t kDistFlagBytes = 256;  // fused path's ready / consumed flags at the end of a slab buffer
 
 struct GemmArgs {
     const Plan* plan;
@@ -72,9 +73,23 @@ void launch_recompose(const int64_t* acc, int64_t m, int64_t n, int ndiag, const
 // summation order (ascending k, separate multiply and add: oracle.cpp:7-28), bitwise;
 // ADPB200_FALLBACK_FAST: FP64 tensor cores (DMMA). Runs iff the plan says native (or
 // always when plan == nullptr); persistent grids, so a skipped launch is one small wave.
+// B spread over the ranks' slab buffers (fused multi-GPU fallback): column j lives in
+// p[j / nr] at column j % nr, each slab compact column-major (k x nr, leading dimension k).
+struct PeerB {
+    const double* p[kMaxPeers];
+    int64_t nr;
+    int world;  // 0: B is the LineView's own pointer
+    __device__ __forceinline__ const double* at(int64_t j, int64_t kpos, int64_t ls, int64_t ps) const {
+        const int64_t r = j / nr;
+        return p[r] + (j - r * nr) * ls + kpos * ps;
+    }
+};
+
+// pb (optional): B's columns read from the ranks' slabs instead of b.ptr (b.ls / b.ps
+// then describe one slab).
 void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
                    int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch,
-                   int flavour = ADPB200_FALLBACK_REFERENCE);
+                   int flavour = ADPB200_FALLBACK_REFERENCE, const PeerB* pb = nullptr);
 int num_sms();
 
 // Grading tools (grade.cu): Dot2 double-double GEMM oracle out[i + j*ldo]

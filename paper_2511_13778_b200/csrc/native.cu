@@ -40,9 +40,11 @@ __device__ __forceinline__ void cp_async8z(uint32_t dst, const double* src, bool
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(valid ? 8 : 0));
 }
 
+template <bool kPeer>
 __global__ void __launch_bounds__(256, 1) native_kernel(LineView a, LineView b, double alpha, double beta,
                                                         const double* __restrict__ c_in, int64_t ldc_in,
-                                                        double* __restrict__ c_out, int64_t ldc, const Plan* plan) {
+                                                        double* __restrict__ c_out, int64_t ldc, const Plan* plan,
+                                                        PeerB pb) {
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
     extern __shared__ __align__(16) double nsm[];
     // [buf][operand][k][line]
@@ -75,7 +77,8 @@ __global__ void __launch_bounds__(256, 1) native_kernel(LineView a, LineView b, 
                 else { kj = e % kKT; lj = e / kKT; }
                 const int64_t gj = j0 + lj, gk2 = k0 + kj;
                 const bool okb = gj < b.lines && gk2 < K;
-                cp_async8z(sb + uint32_t(kj * kTP + lj) * 8u, okb ? b.ptr + gj * b.ls + gk2 * b.ps : b.ptr, okb);
+                const double* pbe = kPeer ? pb.at(gj, gk2, b.ls, b.ps) : b.ptr + gj * b.ls + gk2 * b.ps;
+                cp_async8z(sb + uint32_t(kj * kTP + lj) * 8u, okb ? pbe : b.ptr, okb);
             }
             asm volatile("cp.async.commit_group;\n" ::);
         };
@@ -175,11 +178,12 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 // One operand's tile (128 lines x 16 k) of one stage: `line_major` layout S[k][line]
 // when the lines are contiguous in memory (ls == 1), else S[line][k].
-template <bool kLineMajor, int kThreads>
+template <bool kLineMajor, int kThreads, bool kPeer = false>
 struct OpTile {
     static constexpr bool line_major = kLineMajor;
     const double* ptr;
     int64_t lines, len, ls, ps;
+    PeerB pb;  // kPeer: element (line, k) in the ranks' slabs
     __device__ __forceinline__ void load(uint32_t sdst, int64_t l0, int64_t k0, int tid) const {
 #pragma unroll
         for (int q = 0; q < kDT * kDK / kThreads; ++q) {
@@ -197,7 +201,8 @@ struct OpTile {
             }
             const int64_t gl = l0 + li, gk = k0 + kk;
             const bool ok = gl < lines && gk < len;
-            cp_async8(sdst + off * 8u, ok ? ptr + gl * ls + gk * ps : ptr, ok);
+            const double* e_ptr = kPeer ? pb.at(gl, gk, ls, ps) : ptr + gl * ls + gk * ps;
+            cp_async8(sdst + off * 8u, ok ? e_ptr : ptr, ok);
         }
     }
     __device__ __forceinline__ double frag(const double* s, int line, int k) const {
@@ -219,8 +224,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
     extern __shared__ __align__(16) double dsm[];
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int wm = warp % kWarpsM, wn = warp / kWarpsM;  // warp tile: lines [8 kMI wm, +8 kMI) of A x [8 kNI wn, +8 kNI) of B
-    const OpTile<kAL, kThreads> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
-    const OpTile<kBL, kThreads> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+    const OpTile<kAL, kThreads> ta{a.ptr, a.lines, a.len, a.ls, a.ps, PeerB{}};
+    const OpTile<kBL, kThreads> tb{b.ptr, b.lines, b.len, b.ls, b.ps, PeerB{}};
     const int64_t K = a.len;
     const int64_t tiles_m = (a.lines + kDT - 1) / kDT, tiles_n = (b.lines + kDT - 1) / kDT;
     const int64_t nk = (K + kDK - 1) / kDK;
@@ -343,11 +348,11 @@ constexpr size_t kWsHeader = 128;  // 2 * kWsStages mbarriers
 constexpr size_t kDmmaWsSmem = kWsHeader + size_t(kWsStages) * 2 * kOpDoubles * sizeof(double);
 static_assert(2 * kWsStages * 8 <= kWsHeader, "mbarrier header");
 
-template <bool kAL, bool kBL>
+template <bool kAL, bool kBL, bool kPeer>
 __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, LineView b, double alpha, double beta,
                                                                 const double* __restrict__ c_in, int64_t ldc_in,
                                                                 double* __restrict__ c_out, int64_t ldc,
-                                                                const Plan* plan) {
+                                                                const Plan* plan, PeerB pb) {
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
     extern __shared__ __align__(128) unsigned char dws[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dws);
@@ -375,8 +380,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
     };
     if (warp < kWsProd) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::);
-        const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
-        const OpTile<kBL, kWsProd * 32> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+        const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps, pb};
+        const OpTile<kBL, kWsProd * 32, kPeer> tb{b.ptr, b.lines, b.len, b.ls, b.ps, pb};
         const uint32_t s0 = tc::smem_u32(ops);
         int st = 0;
         uint32_t ph = 0;
@@ -402,8 +407,8 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::);
     const int cw = warp - kWsProd;
     const int wm = cw % 2, wn = cw / 2;  // warp tile: lines [64 wm, +64) of A x [32 wn, +32) of B
-    const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps};
-    const OpTile<kBL, kWsProd * 32> tb{b.ptr, b.lines, b.len, b.ls, b.ps};
+    const OpTile<kAL, kWsProd * 32> ta{a.ptr, a.lines, a.len, a.ls, a.ps, pb};
+    const OpTile<kBL, kWsProd * 32, kPeer> tb{b.ptr, b.lines, b.len, b.ls, b.ps, pb};
     const int fr = lane / 4, fk = lane % 4;
     int st = 0;
     uint32_t ph = 0;
@@ -471,16 +476,21 @@ int resident_grid(const void* fn, int threads, size_t smem, int64_t tiles) {
 
 void launch_native(const LineView& a, const LineView& b, double alpha, double beta, const double* c_in,
                    int64_t ldc_in, double* c_out, int64_t ldc, const Plan* plan, cudaStream_t st, uint64_t* nlaunch,
-                   int flavour) {
+                   int flavour, const PeerB* peer) {
     if (a.lines == 0 || b.lines == 0) return;
+    const bool use_peer = peer && peer->world > 0;
+    const PeerB pb = use_peer ? *peer : PeerB{};
+    using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t, const Plan*,
+                        PeerB);
 #ifndef ADPB200_DMMA_WS
 #define ADPB200_DMMA_WS 1
 #endif
-    if (flavour == ADPB200_FALLBACK_FAST && ADPB200_DMMA_WS) {
-        using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
-                            const Plan*);
-        static const Fn fns[4] = {dmma_ws_kernel<false, false>, dmma_ws_kernel<false, true>,
-                                  dmma_ws_kernel<true, false>, dmma_ws_kernel<true, true>};
+    if (flavour == ADPB200_FALLBACK_FAST && (ADPB200_DMMA_WS || use_peer)) {
+        // [peer][A lines adjacent][B lines adjacent]
+        static const Fn fns[8] = {dmma_ws_kernel<false, false, false>, dmma_ws_kernel<false, true, false>,
+                                  dmma_ws_kernel<true, false, false>,  dmma_ws_kernel<true, true, false>,
+                                  dmma_ws_kernel<false, false, true>,  dmma_ws_kernel<false, true, true>,
+                                  dmma_ws_kernel<true, false, true>,   dmma_ws_kernel<true, true, true>};
         static bool attr = false;
         if (!attr) {
             for (Fn f : fns)
@@ -488,37 +498,40 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
                                      int(kDmmaWsSmem));
             attr = true;
         }
-        const Fn fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
+        const Fn fn = fns[(use_peer ? 4 : 0) + (a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
         const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), kWsThreads, kDmmaWsSmem, tiles);
-        fn<<<grid, kWsThreads, kDmmaWsSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+        fn<<<grid, kWsThreads, kDmmaWsSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
     } else if (flavour == ADPB200_FALLBACK_FAST) {
         // operand layouts in shared memory follow the contiguous direction in HBM
-        using Fn = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
-                            const Plan*);
-        static const Fn fns[4] = {dmma_kernel<false, false, kDmmaWarps>, dmma_kernel<false, true, kDmmaWarps>,
-                                  dmma_kernel<true, false, kDmmaWarps>, dmma_kernel<true, true, kDmmaWarps>};
+        using Fn0 = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
+                             const Plan*);
+        static const Fn0 fns[4] = {dmma_kernel<false, false, kDmmaWarps>, dmma_kernel<false, true, kDmmaWarps>,
+                                   dmma_kernel<true, false, kDmmaWarps>, dmma_kernel<true, true, kDmmaWarps>};
         static bool attr = false;
         if (!attr) {
-            for (Fn f : fns)
+            for (Fn0 f : fns)
                 cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(kDmmaSmem));
             attr = true;
         }
-        const Fn fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
+        const Fn0 fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
         const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), kDmmaWarps * 32, kDmmaSmem, tiles);
         fn<<<grid, kDmmaWarps * 32, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
     } else {
+        static const Fn fns[2] = {native_kernel<false>, native_kernel<true>};
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(reinterpret_cast<const void*>(native_kernel),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(kNativeSmem));
+            for (Fn f : fns)
+                cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kNativeSmem));
             attr = true;
         }
+        const Fn fn = fns[use_peer ? 1 : 0];
         const int64_t tiles = ((a.lines + kT - 1) / kT) * ((b.lines + kT - 1) / kT);
-        const int grid = resident_grid(reinterpret_cast<const void*>(native_kernel), 256, kNativeSmem, tiles);
-        native_kernel<<<grid, 256, kNativeSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+        const int grid = resident_grid(reinterpret_cast<const void*>(fn), 256, kNativeSmem, tiles);
+        fn<<<grid, 256, kNativeSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
     }
     ++*nlaunch;
 }

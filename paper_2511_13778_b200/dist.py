@@ -101,11 +101,47 @@ def dist_decision(xchg_host, m_global: int, n: int, k: int, config: Optional[Adp
     return tuple(int(v) for v in out)
 
 
+class LazyDecision:
+    """(path, slices, nsl) of a dist call whose host never read the decision (the
+    fused in-place path): computed from the reduced exchange block on first access,
+    which synchronises with the device then."""
+
+    def __init__(self, xchg: torch.Tensor, m_global: int, n: int, k: int, config: AdpConfig):
+        self._args = (xchg, m_global, n, k, config)
+        self._value = None
+
+    def value(self) -> Tuple[int, int, int]:
+        if self._value is None:
+            xchg, m_global, n, k, config = self._args
+            self._value = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)[:3]
+        return self._value
+
+    def __getitem__(self, i):
+        return self.value()[i]
+
+    def __iter__(self):
+        return iter(self.value())
+
+    def __len__(self):
+        return 3
+
+    def __eq__(self, other):
+        return tuple(self.value()) == tuple(other)
+
+    def __repr__(self):
+        return f"LazyDecision{tuple(self.value())}"
+
+
+def flag_ptr(slab_ptr: int, slab_bytes: int, which: int) -> int:
+    """Address of a slab buffer's fused-path flag (which = 0 ready, 1 consumed)."""
+    return int(slab_ptr) + int(lib().adpb200_dist_flag_offset(slab_bytes, which))
+
+
 def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
                      A: torch.Tensor, lda: int, B_slab: torch.Tensor, beta: float, C_: torch.Tensor, ldc: int,
                      config: Optional[AdpConfig] = None, handle: Optional[Handle] = None,
                      trace: Optional[torch.Tensor] = None, rank: int = 0, overlap: bool = True,
-                     slab_ptrs: Optional[Sequence[int]] = None, pull: bool = False):
+                     slab_ptrs: Optional[Sequence[int]] = None, pull: bool = False, epoch: int = 1):
     """The B-distributed ADP DGEMM of one rank as a generator of collective
     requests, so that the same orchestration runs under torch.distributed
     (dgemm_dist) and under a single-process multi-rank driver (the tests):
@@ -119,19 +155,27 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     need only this rank's own B columns compute (phases 5 and 6).
 
     With slab_ptrs (every rank's slab buffer as mapped in this process, entry
-    `rank` its own: PeerSlabs over CUDA IPC, or plain buffers of one device in
-    the tests) there is no plane all-gather: after a barrier the fused phase 7
-    GEMM reads the B planes of every rank in place over peer memory
+    `rank` its own: PeerSlabs over CUDA IPC, or zeroed buffers of one device in
+    the tests) there is no plane all-gather: the fused phase 7 GEMM reads the B
+    planes of every rank in place over peer memory, with no host read and no
+    host barrier — the streams order the ranks through each buffer's ready /
+    consumed flags (`epoch` = this buffer's use count, 1, 2, ...; see
+    adpb200.h) and the device plan picks the GEMM or the native fallback:
+        ("device_barrier",)        a no-op for real ranks (the flags order them);
+                                   the virtual-rank driver enqueues every rank's
+                                   phase 3 before any rank's wait
+    With pull=True the copy engines pull each peer's record into local memory
+    on a side stream while the GEMM of the previous rank's columns runs (one
+    phase-7 launch per rank, own columns first; after one 8-byte host read and
         ("barrier",)               every rank past its phase 3 (slab sliced)
-    and with pull=True the copy engines pull each peer's record into local
-    memory on a side stream while the GEMM of the previous rank's columns runs
-    (one phase-7 launch per rank, own columns first): the transfer overlaps the
-    math rank by rank and the GEMM reads local, L2-cached planes.
+    ): the transfer overlaps the math rank by rank and the GEMM reads local,
+    L2-cached planes.
 
     Rank owns rows of op(A) / C (column-major local block, ldc) and the B
     column slab B_slab (k x n/world column-major, compact: a (n/world, k)
-    row-major torch tensor). Stream-ordered except for one 8-byte host read of
-    the reduced decision input (it sizes the plane all-gather)."""
+    row-major torch tensor). Stream-ordered except, on the all-gather and pull
+    paths, one 8-byte host read of the reduced decision input (it sizes the
+    transfer). Returns (path, slices, nsl) — lazily on the in-place fused path."""
     config = config or AdpConfig()
     dev = C_.device
     handle = handle or Handle.default(dev.index)
@@ -155,14 +199,29 @@ def dgemm_dist_steps(world: int, transa: str, m_global: int, m: int, n: int, k: 
     yield ("all_gather", ba, bl)
     phase(2)
     yield ("all_reduce_max", xchg)
+    if fused and not pull:
+        # in place, host-sync free: slice into this buffer once every peer has finished
+        # reading its previous use, publish it, wait for every peer's, GEMM (or native
+        # fallback) on the device's decision, release
+        ldev = lib()
+        for r in range(world):
+            if r != rank:
+                check(ldev.adpb200_stream_wait_geq(C.c_void_p(flag_ptr(slab_ptrs[r], cap_bytes, 1)), epoch - 1, st))
+        phase(3)
+        phase(8)
+        check(ldev.adpb200_stream_write_flag(C.c_void_p(flag_ptr(slab_ptrs[rank], cap_bytes, 0)), epoch, st))
+        yield ("device_barrier",)
+        for r in range(world):
+            if r != rank:
+                check(ldev.adpb200_stream_wait_geq(C.c_void_p(flag_ptr(slab_ptrs[r], cap_bytes, 0)), epoch, st))
+        ptrs = (C.c_void_p * world)(*[int(p) for p in slab_ptrs])
+        phase(7, C.cast(ptrs, C.c_void_p), 0)
+        check(ldev.adpb200_stream_write_flag(C.c_void_p(flag_ptr(slab_ptrs[rank], cap_bytes, 1)), epoch, st))
+        return LazyDecision(xchg, m_global, n, k, config)
     phase(3)
     path, s, nsl, _ = dist_decision(xchg.cpu().tolist(), m_global, n, k, config)  # (syncs: slab sliced)
-    if nsl > 0 and fused:
+    if nsl > 0 and fused:  # pulled
         yield ("barrier",)
-        if not pull:
-            ptrs = (C.c_void_p * world)(*[int(p) for p in slab_ptrs])
-            phase(7, C.cast(ptrs, C.c_void_p), nsl)
-            return (path, s, nsl)
         rec = hdr + nsl * plane_bytes
         staging = torch.empty(rec * world, dtype=torch.int8, device=dev)
         cur = torch.cuda.current_stream(dev)
@@ -215,8 +274,9 @@ def dgemm_dist(transa: str, m_global: int, m: int, n: int, k: int, alpha: float,
     the copy engines pull them rank by rank while the GEMM runs on local copies)."""
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
+    slab_ptrs, epoch = peers.next_with_epoch() if peers is not None else (None, 1)
     gen = dgemm_dist_steps(world, transa, m_global, m, n, k, alpha, A, lda, B_slab, beta, C_, ldc, config, handle,
-                           trace, rank=rank, slab_ptrs=peers.next() if peers is not None else None, pull=pull)
+                           trace, rank=rank, slab_ptrs=slab_ptrs, pull=pull, epoch=epoch)
     return drive_collectives(gen, world, group)
 
 
@@ -279,9 +339,14 @@ class PeerSlabs:
         return [x for x, _ in got]
 
     def next(self):
-        p = self.ptrs[self.calls % 2]
+        return self.next_with_epoch()[0]
+
+    def next_with_epoch(self):
+        """(pointer list, epoch) for the next call: buffers alternate, and the epoch
+        counts the uses of that buffer (the value its flags take, 1, 2, ...)."""
+        b = self.calls % 2
         self.calls += 1
-        return p
+        return self.ptrs[b], self.calls // 2 + (self.calls % 2)
 
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
@@ -325,6 +390,8 @@ def drive_collectives(gen, world: int, group=None):
             elif req[0] == "barrier":
                 if world > 1:
                     dist.barrier(group=group)
+            elif req[0] == "device_barrier":
+                pass  # the streams' flags order the ranks
             else:
                 raise ValueError(f"unknown collective request {req[0]!r}")
             req = next(gen)

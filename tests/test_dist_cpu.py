@@ -82,8 +82,10 @@ def test_dist_sizes():
     nrec, hdr, plane, cap = dist_sizes(8192, 8192, 8)
     nr, t = 1024, 32
     assert nrec == 2 * t * nr + nr and hdr == 4096 and plane == 8192 * nr
-    assert cap == hdr + 18 * plane  # auto mode: max_slices planes
-    assert dist_sizes(8192, 100, 8, AdpConfig(mode=1, forced_slices=7))[3] == 1024 * 4 + 7 * 128 * 1024
+    # auto mode: max_slices planes (or the FP64 slab, whichever is larger) + the fused path's flags
+    assert cap == max(hdr + 18 * plane, nr * 8192 * 8) + 256
+    assert dist_sizes(8192, 100, 8, AdpConfig(mode=1, forced_slices=7))[3] == 1024 * 4 + 7 * 128 * 1024 + 256
+    assert dist_sizes(8192, 100, 8, AdpConfig(mode=1, forced_slices=5))[3] == 1024 * 100 * 8 + 256
     with pytest.raises(ValueError):
         dist_sizes(100, 100, 8)
 

@@ -21,7 +21,7 @@ def run_virtual(gens):
     while True:
         kind = reqs[0][0]
         assert all(r[0] == kind for r in reqs), "ranks diverged"
-        if kind in ("wait", "barrier"):
+        if kind in ("wait", "barrier", "device_barrier"):
             pass
         elif kind in ("all_gather", "all_gather_async"):
             cat = torch.cat([r[2].reshape(-1) for r in reqs])
@@ -73,7 +73,8 @@ def dist_case(gpu, world, m, n, k, cfg, transa="N", alpha=1.0, beta=0.0, poison=
         from paper_2511_13778_b200.dist import dist_sizes
 
         cap_bytes = dist_sizes(n, k, world, cfg)[3]
-        slabs = [torch.empty(cap_bytes, dtype=torch.int8, device="cuda") for _ in range(world)]
+        # zeroed: the in-place path's ready / consumed flags at each buffer's end start at 0
+        slabs = [torch.zeros(cap_bytes, dtype=torch.int8, device="cuda") for _ in range(world)]
         slab_ptrs = [t.data_ptr() for t in slabs]
     for r in range(world):
         r0, r1 = rows_of(r, world, m)
@@ -192,7 +193,18 @@ def test_dist_fused_peer_gemm(gpu, world, m, n, k, cfgname):
         assert all(r == res[0] for r in res)
         assert res[0][0] == 0
         assert_bitwise(got.cpu().numpy(), ref.cpu().numpy(), nan_equiv=False)
-    # NaN in one slab: the fused path is not taken (native fallback gathers FP64 B)
-    got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 3), fused=True)
-    assert all(r[0] == 1 for r in res)
-    assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
+    # NaN in one slab: native fallback everywhere — in place (device-decided), each rank's
+    # native GEMM reads the FP64 slabs the peers copied into their buffers (phase 8); pulled,
+    # the host sees the decision and all-gathers FP64 B
+    for pull in (False, True):
+        got, ref, res = dist_case(gpu, world, m, n, k, cfg, poison=(n // world + 1, 3), fused=True, pull=pull)
+        assert all(r[0] == 1 for r in res)
+        assert_bitwise(got.cpu().numpy(), ref.cpu().numpy())
+    for flavour in ("fast",):  # the DMMA flavour reads the peers' slabs too (within its bound)
+        fcfg = gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET, fallback=flavour)
+        got, ref, res = dist_case(gpu, world, m, n, k, fcfg, poison=(n // world + 1, 3), fused=True)
+        assert all(r[0] == 1 for r in res)
+        g, rf = got.cpu().numpy(), ref.cpu().numpy()
+        fin = np.isfinite(rf)
+        assert np.array_equal(np.isnan(g), np.isnan(rf))
+        assert np.allclose(g[fin], rf[fin], rtol=1e-12, atol=1e-12)
