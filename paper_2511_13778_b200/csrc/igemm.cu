@@ -645,7 +645,13 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
                         // and the exponent below absorbs the factor (|S'| < 2^88 for NB 64,
                         // < 2^104 for NB 48).
                         constexpr int kW = NB == 64 ? 3 : 4;
-                        constexpr int kB = NB == 64 ? 4 : 2;  // columns per TMEM load batch (measured best)
+#ifndef ADPB200_KB48
+#define ADPB200_KB48 2
+#endif
+#ifndef ADPB200_KB64
+#define ADPB200_KB64 4
+#endif
+                        constexpr int kB = NB == 64 ? ADPB200_KB64 : ADPB200_KB48;  // columns per TMEM load batch
                         uint32_t w[kCols][kW];
 #pragma unroll
                         for (int b = 0; b < kCols / kB; ++b) {
