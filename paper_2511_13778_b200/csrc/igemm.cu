@@ -45,10 +45,10 @@ constexpr int kGroupM = ADPB200_GROUP_M;   // raster: m-tiles per group
 // Per-thread registers after the warpgroup split. The CTA's pool is what the launch
 // reserved (384 threads x 168 registers): setmaxnreg.inc blocks until the pool has
 // the registers, so the split must fit it exactly or the epilogue never starts.
-constexpr int kLaunchRegs = 168;
 constexpr int kRegsCtl = 40;
-constexpr int kRegsEpi = 232;
-static_assert(128 * kRegsCtl + 256 * kRegsEpi <= 384 * kLaunchRegs, "register split exceeds the CTA pool");
+#ifndef ADPB200_EPI48
+#define ADPB200_EPI48 12
+#endif
 #ifndef ADPB200_NO_REGSPLIT
 #define ADPB200_SETMAXNREG(dir, n) asm volatile("setmaxnreg." dir ".sync.aligned.u32 %0;\n" ::"n"(n))
 #else
@@ -63,10 +63,19 @@ struct Cfg {
     // registers) drains TMEM 2x slower; 16 epilogue warps cap registers at 96.)
     static constexpr int kFirstEpiWarp = 4;
     static constexpr int kAllocWarp = 2;
-    static constexpr int kEpiWarps = 8;
+    // NB = 48: 3 warps per quadrant (16 columns each) — with 10 diagonals per column the
+    // epilogue's fold, done while it holds TMEM, was the short-k bottleneck at 2 x 24
+    static constexpr int kEpiWarps = NB == 48 ? ADPB200_EPI48 : 8;
     static constexpr int kEpiThreads = kEpiWarps * 32;
     static constexpr int kThreads = kFirstEpiWarp * 32 + kEpiThreads;
     static constexpr int kColGroups = kEpiWarps / 4;
+    // the launch reserves kLaunchRegs per thread (65536 / kThreads, multiple of 8); the
+    // control warps give theirs up (setmaxnreg.dec kRegsCtl), the epilogue takes the rest
+    static constexpr int kLaunchRegs = kThreads == 384 ? 168 : 128;
+    static constexpr int kRegsEpi = kThreads == 384 ? 232 : 152;
+    static_assert(128 * kRegsCtl + kEpiThreads * kRegsEpi <= kThreads * kLaunchRegs,
+                  "register split exceeds the CTA pool");
+    static_assert(NB % kColGroups == 0, "columns per epilogue warp");
     static constexpr int kNDMax = 512 / NB;                    // diagonals that fit in TMEM
     // exact fold limbs: |S| < 2^(8L + 31 + 8) with L <= kNDMax - 1
     static constexpr int kNL = NB >= 48 ? 2 : (NB == 32 ? 3 : (NB == 16 ? 5 : 9));
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
         ADPB200_SETMAXNREG("dec", kRegsCtl);
     } else {
         // ===== epilogue: (lane quadrant, column group) per warp =====
-        ADPB200_SETMAXNREG("inc", kRegsEpi);
+        ADPB200_SETMAXNREG("inc", C::kRegsEpi);
         const int ew = warp - C::kFirstEpiWarp;
         const int q = warp & 3;                        // TMEM lane quadrant (warp id % 4)
         const int jh = ew / 4;                         // column group
@@ -882,11 +891,13 @@ bool set_attr_once() {
         // the warpgroup register split assumes the launch reserves exactly kLaunchRegs per
         // thread; refuse to launch (an error, not a hang) if the binary says otherwise
         cudaFuncAttributes fa{};
-        ok = cudaFuncGetAttributes(&fa, igemm_kernel<NB>) == cudaSuccess && fa.numRegs == kLaunchRegs ? 1 : 0;
+        ok = cudaFuncGetAttributes(&fa, igemm_kernel<NB>) == cudaSuccess && fa.numRegs == Cfg<NB>::kLaunchRegs ? 1 : 0;
 #ifdef ADPB200_NO_REGSPLIT
         ok = 1;
 #endif
-        if (!ok) fprintf(stderr, "adpb200: igemm_kernel<%d> uses %d registers, expected %d\n", NB, fa.numRegs, kLaunchRegs);
+        if (!ok)
+            fprintf(stderr, "adpb200: igemm_kernel<%d> uses %d registers, expected %d\n", NB, fa.numRegs,
+                    Cfg<NB>::kLaunchRegs);
     }
     return ok == 1;
 }

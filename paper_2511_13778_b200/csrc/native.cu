@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
 }
 
 // ---- fast flavour, warp-specialised: producers and consumers on mbarriers ---------------
-// 4 producer warps issue the cp.async copies of a stage and signal its `full`
-// mbarrier when they land (cp.async.mbarrier.arrive.noinc); 8 consumer warps (the
+// 4 producer warps issue the cp.async copies of a stage and publish it on its `full`
+// mbarrier once they have landed (wait_group + a release arrive); 8 consumer warps (the
 // same 64 x 32 DMMA tiles) wait on `full`, compute, and release the stage on
 // `empty`. No CTA-wide barrier in the k loop, so a scheduler's two consumer warps
 // are never held back by the slowest warp of another scheduler, and the copy
@@ -346,7 +346,7 @@ constexpr int kWsStages = ADPB200_DMMA_WS_STAGES;
 constexpr int kWsProd = 4, kWsCons = 8, kWsThreads = (kWsProd + kWsCons) * 32;
 constexpr size_t kWsHeader = 128;  // 2 * kWsStages mbarriers
 constexpr size_t kDmmaWsSmem = kWsHeader + size_t(kWsStages) * 2 * kOpDoubles * sizeof(double);
-static_assert(2 * kWsStages * 8 <= kWsHeader, "mbarrier header");
+static_assert(2 * kWsStages * 8 <= kWsHeader && kWsStages >= 3, "mbarrier header; kLag = stages - 2 >= 1");
 
 template <bool kAL, bool kBL, bool kPeer>
 __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, LineView b, double alpha, double beta,
@@ -385,6 +385,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
         const uint32_t s0 = tc::smem_u32(ops);
         int st = 0;
         uint32_t ph = 0;
+        // A stage is published kLag stages after its copies were issued: the thread waits
+        // for that commit group (cp.async.wait_group) and arrives on `full` with release
+        // semantics, so the consumers' acquire-wait orders their reads after the copies.
+        // kLag + 1 stages stay in flight per producer thread (kLag < kWsStages).
+        constexpr int kLag = kWsStages - 2;
+        int sig = 0;         // next stage to publish
+        int64_t owed = 0;    // issued, not yet published
         for (int64_t tile = blockIdx.x; tile < tiles_m * tiles_n; tile += gridDim.x) {
             int64_t i0, j0;
             coords(tile, i0, j0);
@@ -393,8 +400,13 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
                 const uint32_t sa = s0 + uint32_t(st) * 2u * kOpDoubles * 8u;
                 ta.load(sa, i0, t * kDK, tid);
                 tb.load(sa + kOpDoubles * 8u, j0, t * kDK, tid);
-                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(&full[st]))
-                             : "memory");
+                asm volatile("cp.async.commit_group;\n" ::: "memory");
+                if (++owed > kLag) {
+                    asm volatile("cp.async.wait_group %0;\n" ::"n"(kLag) : "memory");
+                    tc::mbar_arrive(&full[sig]);
+                    sig = sig + 1 == kWsStages ? 0 : sig + 1;
+                    --owed;
+                }
                 if (++st == kWsStages) {
                     st = 0;
                     ph ^= 1;
@@ -402,6 +414,10 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
             }
         }
         asm volatile("cp.async.wait_all;\n" ::: "memory");
+        for (; owed > 0; --owed) {
+            tc::mbar_arrive(&full[sig]);
+            sig = sig + 1 == kWsStages ? 0 : sig + 1;
+        }
         return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::);

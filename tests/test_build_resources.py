@@ -1,12 +1,14 @@
 """CPU: resource facts of the built kernels that the launch code relies on.
 
 igemm_kernel<NB> splits its register file by warpgroup with setmaxnreg
-(csrc/igemm.cu: 40 per thread for the producer/MMA/allocator warpgroup, 232 for
-the two epilogue warpgroups). setmaxnreg.inc blocks until the CTA's pool has the
-registers, and the pool is what the launch reserved: 384 threads x the kernel's
-register count. The split is sized for 168; a build that comes out different
-would hang the epilogue (launch_igemm refuses it at run time). This pins it at
-build time, together with the SASS evidence for the tensor-core paths."""
+(csrc/igemm.cu: 40 per thread for the producer/MMA/allocator warpgroup, the rest
+for the epilogue warpgroups). setmaxnreg.inc blocks until the CTA's pool has the
+registers, and the pool is what the launch reserved: the CTA's threads x the
+kernel's register count. The split is sized for 168 with 384 threads (232 per
+epilogue thread) and for 128 with 512 threads (NB = 48: 3 epilogue warps per
+TMEM quadrant, 152 per epilogue thread); a build that comes out different would
+hang the epilogue (launch_igemm refuses it at run time). This pins it at build
+time, together with the SASS evidence for the tensor-core paths."""
 import os
 import re
 import shutil
@@ -37,7 +39,8 @@ def test_igemm_register_count_matches_the_split():
             if r:
                 regs[int(m.group(1))] = int(r.group(1))
     assert set(regs) == {8, 16, 32, 48, 64}, regs
-    assert all(v == 168 for v in regs.values()), regs
+    want = {8: 168, 16: 168, 32: 168, 48: 128, 64: 168}
+    assert regs == want, regs
 
 
 def test_sass_has_tensor_core_paths():

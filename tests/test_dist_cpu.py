@@ -149,3 +149,29 @@ def test_drive_collectives_gloo():
         assert ba == list(range(6)) + [10 + i for i in range(6)]
         assert x == [1, 7]
         assert g == [1] * 8 + [2] * 8
+
+
+def test_peer_slabs_epochs_alternate_buffers():
+    """PeerSlabs.next_with_epoch: buffers alternate per call and the epoch counts the
+    uses of the chosen buffer (the fused path's flag values)."""
+    from paper_2511_13778_b200.dist import PeerSlabs
+
+    ps = object.__new__(PeerSlabs)  # no IPC: only the call bookkeeping
+    ps.ptrs, ps.calls = [["b0"], ["b1"]], 0
+    got = [ps.next_with_epoch() for _ in range(5)]
+    assert [p[0] for p, _ in got] == ["b0", "b1", "b0", "b1", "b0"]
+    assert [e for _, e in got] == [1, 1, 2, 2, 3]
+
+
+def test_flag_offsets_and_lazy_decision():
+    import torch
+
+    from paper_2511_13778_b200 import AdpConfig
+    from paper_2511_13778_b200.dist import LazyDecision, dist_decision, dist_sizes, flag_ptr
+
+    cap = dist_sizes(1024, 512, 4)[3]
+    assert flag_ptr(1000, cap, 0) == 1000 + cap - 256 and flag_ptr(1000, cap, 1) == 1000 + cap - 128
+    xchg = torch.tensor([0, 3], dtype=torch.int32)  # no exception, esc 3
+    lazy = LazyDecision(xchg, 4096, 1024, 512, AdpConfig())
+    want = dist_decision([0, 3], 4096, 1024, 512, AdpConfig())[:3]
+    assert tuple(lazy) == want and lazy == want and lazy[0] == want[0] and len(lazy) == 3

@@ -208,3 +208,51 @@ def test_dist_fused_peer_gemm(gpu, world, m, n, k, cfgname):
         fin = np.isfinite(rf)
         assert np.array_equal(np.isnan(g), np.isnan(rf))
         assert np.allclose(g[fin], rf[fin], rtol=1e-12, atol=1e-12)
+
+
+def test_dist_fused_in_place_reuses_buffers_across_calls(gpu):
+    """The host-sync-free fused path over several calls: two slab buffers alternate
+    (epochs 1, 1, 2, 2), every call's slicing waits on the peers' "consumed" flag of
+    the buffer's previous use and its GEMM on their "ready" flags. Each call changes
+    the operands (and the third one poisons B, so the native fallback reads the peers'
+    FP64 slabs); every assembled C must equal one GPU's."""
+    from paper_2511_13778_b200 import Handle
+    from paper_2511_13778_b200.dist import cols_of, dgemm_dist_steps, dist_sizes, rows_of
+
+    world, m, n, k = 3, 700, 3 * 128, 900
+    cfg = gpu.AdpConfig(min_dim=8, pair_limit=gpu.PAIRS_TARGET)
+    cap = dist_sizes(n, k, world, cfg)[3]
+    bufs = [[torch.zeros(cap, dtype=torch.int8, device="cuda") for _ in range(world)] for _ in range(2)]
+    handles = [Handle(0) for _ in range(world)]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(77)
+    for call in range(4):
+        Ast = torch.rand((k, m), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
+        Bt = torch.rand((n, k), generator=g, device="cuda", dtype=torch.float64) * 2 - 1
+        if call == 2:
+            Bt[n // world + 5, 17] = float("nan")
+        ref = torch.zeros((n, m), device="cuda", dtype=torch.float64)
+        gpu.dgemm("N", "N", m, n, k, 1.0, Ast, m, Bt, k, 0.0, ref, m, cfg)
+        slab_ptrs = [t.data_ptr() for t in bufs[call % 2]]
+        gens, blocks = [], []
+        for r in range(world):
+            r0, r1 = rows_of(r, world, m)
+            c0, c1 = cols_of(r, world, n)
+            Cb = torch.zeros((n, r1 - r0), device="cuda", dtype=torch.float64)
+            blocks.append(Cb)
+            gens.append(dgemm_dist_steps(world, "N", m, r1 - r0, n, k, 1.0, Ast[:, r0:r1].contiguous(), r1 - r0,
+                                         Bt[c0:c1].contiguous(), 0.0, Cb, r1 - r0, cfg, handles[r], rank=r,
+                                         slab_ptrs=slab_ptrs, epoch=call // 2 + 1))
+        res = run_virtual(gens)
+        torch.cuda.synchronize()
+        assert all(x[0] == (1 if call == 2 else 0) for x in res)
+        assert_bitwise(torch.cat(blocks, dim=1).cpu().numpy(), ref.cpu().numpy())
+    # the flags record the last epoch of each buffer
+    from paper_2511_13778_b200.dist import flag_ptr
+
+    for b in range(2):
+        for r in range(world):
+            t = bufs[b][r]
+            for which in (0, 1):
+                off = flag_ptr(t.data_ptr(), cap, which) - t.data_ptr()
+                assert int(t[off:off + 4].view(torch.int32).item()) == 2
