@@ -150,9 +150,6 @@ constexpr int kDStages = ADPB200_DMMA_STAGES;
 constexpr int kPadL = kDT + 4;  // [k][line] rows: 132 doubles (== 4 mod 16: conflict-free fragment reads)
 constexpr int kPadK = kDK + 4;  // [line][k] rows: kDK + 4 doubles (== 4 mod 16)
 constexpr int kOpDoubles = (kDK * kPadL > kDT * kPadK) ? kDK * kPadL : kDT * kPadK;  // one operand, one stage
-#ifndef ADPB200_DMMA_PIPE
-#define ADPB200_DMMA_PIPE 0  // measured: register double-buffered fragments 28.7 vs 29.3 TFLOP/s without
-#endif
 #ifndef ADPB200_DMMA_WARPS
 #define ADPB200_DMMA_WARPS 8
 #endif
@@ -273,30 +270,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
             const double* Bs = sb(st_cur);
             st_cur = st_cur + 1 == kDStages ? 0 : st_cur + 1;
             st_next = st_next + 1 == kDStages ? 0 : st_next + 1;
-#if ADPB200_DMMA_PIPE
-            // fragments of k-step kk + 4 are read while the MMAs of kk issue
-            double af[2][kMI], bf[2][kNI];
-#pragma unroll
-            for (int mi = 0; mi < kMI; ++mi) af[0][mi] = ta.frag(As, wm * kMI * 8 + mi * 8 + fr, fk);
-#pragma unroll
-            for (int ni = 0; ni < kNI; ++ni) bf[0][ni] = tb.frag(Bs, wn * kNI * 8 + ni * 8 + fr, fk);
-#pragma unroll
-            for (int kk = 0; kk < kDK; kk += 4) {
-                const int c = (kk / 4) & 1;
-                if (kk + 4 < kDK) {
-#pragma unroll
-                    for (int mi = 0; mi < kMI; ++mi)
-                        af[c ^ 1][mi] = ta.frag(As, wm * kMI * 8 + mi * 8 + fr, kk + 4 + fk);
-#pragma unroll
-                    for (int ni = 0; ni < kNI; ++ni)
-                        bf[c ^ 1][ni] = tb.frag(Bs, wn * kNI * 8 + ni * 8 + fr, kk + 4 + fk);
-                }
-#pragma unroll
-                for (int mi = 0; mi < kMI; ++mi)
-#pragma unroll
-                    for (int ni = 0; ni < kNI; ++ni) dmma(acc[mi][ni], af[c][mi], bf[c][ni]);
-            }
-#else
 #pragma unroll
             for (int kk = 0; kk < kDK; kk += 4) {
                 double af[kMI], bf[kNI];
@@ -309,7 +282,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
 #pragma unroll
                     for (int ni = 0; ni < kNI; ++ni) dmma(acc[mi][ni], af[mi], bf[ni]);
             }
-#endif
         }
         cp_async_wait<0>();
         __syncthreads();  // the next tile's prologue overwrites stages 0..1

@@ -312,16 +312,8 @@ __device__ __forceinline__ void emit16(const SliceArgs& a, int nsl, const uint64
             for (int q = 0; q < 16; ++q) X[q] = slice_word<S>(bits[q], E);
         }
         uint32_t w[S][4];  // plane d: bytes of positions 0-3, 4-7, 8-11, 12-15
-#ifdef ADPB200_SLICE_PACK1
-#pragma unroll
-        for (int d = 0; d < S; ++d) {
-            pack_plane<S>(X, d, w[d][0], w[d][1]);
-            pack_plane<S>(X + 8, d, w[d][2], w[d][3]);
-        }
-#else
         pack_planes<S>(X, w, 0);
         pack_planes<S>(X + 8, w, 2);
-#endif
         // plane d's 16 bytes sit at base + d * plane_stride: one address, one alignment test
         int8_t* out = a.planes + plane_off(a, 0, line, p0);
         const bool v16 = nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) | uintptr_t(a.plane_stride)) & 15) == 0;
