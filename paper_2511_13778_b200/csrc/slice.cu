@@ -108,38 +108,34 @@ __device__ __forceinline__ bool fast_words(const uint64_t (&bits)[16], int E, ui
     return true;
 }
 
-// byte j of X as stored in plane d = S-1-j
+// S in 9..16, 8 elements, through the FP64 pipe as well: with f = |v| 2^(p-64) (exact,
+// p >= 64), H = floor(f), r = f - H (exact for f >= 0) and L = floor(r 2^64) (r 2^64 is
+// exact), |v| 2^p = H 2^64 + L + frac; U = H:L for v >= 0, and for v < 0 floor gives
+// -(H:L) when frac = 0, else -(H:L) - 1 = ~(H:L). Taken when 64 <= p <= 1087 and all 8
+// elements are finite; otherwise the caller runs slice_word.
 template <int S>
-__device__ __forceinline__ uint32_t plane_byte(typename Word<S>::T X, int d) {
-    const uint32_t b = uint32_t(X >> (8 * (S - 1 - d))) & 0xffu;
-    return d == 0 ? b : (b ^ 0x80u);
-}
-
-// Plane d's bytes of 8 consecutive elements X[0..7], packed into two words with
-// byte permutes (d is a compile-time constant after unrolling).
-template <int S>
-__device__ __forceinline__ void pack_plane(const typename Word<S>::T* X, int d, uint32_t& lo, uint32_t& hi) {
-    if constexpr (S <= 8) {
-        const int j = S - 1 - d;  // byte of X
-        uint32_t w[8];
+__device__ __forceinline__ bool fast_words_w(const uint64_t* bits, int E, uint32_t (&W)[8][4]) {
+    const int p = 7 + 8 * (S - 1) - E;
+    if (p < 64 || p > 64 + 1023) return false;
+    uint32_t exmax = 0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) w[q] = j < 4 ? uint32_t(X[q]) : uint32_t(X[q] >> 32);
-        const uint32_t b = uint32_t(j & 3);
-        const uint32_t sel = b | ((4 + b) << 4);  // byte b of x -> byte 0, byte b of y -> byte 1
-        lo = __byte_perm(__byte_perm(w[0], w[1], sel), __byte_perm(w[2], w[3], sel), 0x5410);
-        hi = __byte_perm(__byte_perm(w[4], w[5], sel), __byte_perm(w[6], w[7], sel), 0x5410);
-        if (d != 0) {
-            lo ^= 0x80808080u;
-            hi ^= 0x80808080u;
-        }
-    } else {
-        lo = hi = 0;
+    for (int q = 0; q < 8; ++q) exmax = max(exmax, uint32_t(bits[q] >> 32) & 0x7ff00000u);
+    if (exmax == 0x7ff00000u) return false;
+    const double sc = __longlong_as_double(int64_t(p - 64 + 1023) << 52);
+    const u128 C = slice_const<S>();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            lo |= plane_byte<S>(X[q], d) << (8 * q);
-            hi |= plane_byte<S>(X[q + 4], d) << (8 * q);
-        }
+    for (int q = 0; q < 8; ++q) {
+        const double f = __dmul_rn(__longlong_as_double(int64_t(bits[q] & 0x7fffffffffffffffull)), sc);
+        const double hd = floor(f);
+        const double ld = __dmul_rn(__dsub_rn(f, hd), 18446744073709551616.0);  // r 2^64
+        const double lf = floor(ld);
+        u128 U = (u128(uint64_t(hd)) << 64) | u128(uint64_t(lf));
+        if (bits[q] >> 63) U = lf != ld ? ~U : u128(0) - U;
+        const u128 X = U + C;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) W[q][i] = uint32_t(X >> (32 * i));
     }
+    return true;
 }
 
 // Every plane's bytes of 8 elements X[0..7] (S <= 8) into w[d][o], w[d][o + 1].
@@ -172,6 +168,37 @@ __device__ __forceinline__ void pack_planes(const uint64_t* X, uint32_t (&w)[S][
         if (d != 0) {
             w[d][o] ^= 0x80808080u;
             w[d][o + 1] ^= 0x80808080u;
+        }
+    }
+}
+
+// The same for S in 9..16 from four 32-bit words per element (byte j of X in word j/4).
+template <int S>
+__device__ __forceinline__ void pack_planes_w(const uint32_t (&W)[8][4], uint32_t (&w)[S][2]) {
+#pragma unroll
+    for (int j = 0; j < S; j += 2) {
+        uint32_t h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) h[q] = W[q][j >> 2];
+        const uint32_t b = uint32_t(j & 3);
+        const int d = S - 1 - j;
+        if (j + 1 < S) {
+            const uint32_t sel = b | ((4 + b) << 4) | ((b + 1) << 8) | ((5 + b) << 12);
+            const uint32_t t0 = __byte_perm(h[0], h[1], sel), t1 = __byte_perm(h[2], h[3], sel);
+            const uint32_t t2 = __byte_perm(h[4], h[5], sel), t3 = __byte_perm(h[6], h[7], sel);
+            const uint32_t f = d - 1 != 0 ? 0x80808080u : 0u;
+            w[d][0] = __byte_perm(t0, t1, 0x5410) ^ (d != 0 ? 0x80808080u : 0u);
+            w[d][1] = __byte_perm(t2, t3, 0x5410) ^ (d != 0 ? 0x80808080u : 0u);
+            w[d - 1][0] = __byte_perm(t0, t1, 0x7632) ^ f;
+            w[d - 1][1] = __byte_perm(t2, t3, 0x7632) ^ f;
+        } else {
+            const uint32_t sel = b | ((4 + b) << 4);
+            w[d][0] = __byte_perm(__byte_perm(h[0], h[1], sel), __byte_perm(h[2], h[3], sel), 0x5410);
+            w[d][1] = __byte_perm(__byte_perm(h[4], h[5], sel), __byte_perm(h[6], h[7], sel), 0x5410);
+            if (d != 0) {
+                w[d][0] ^= 0x80808080u;
+                w[d][1] ^= 0x80808080u;
+            }
         }
     }
 }
@@ -338,19 +365,69 @@ __device__ __forceinline__ void emit16(const SliceArgs& a, int nsl, const uint64
             }
         }
     } else if constexpr (S <= 16) {
+        // two halves of 8 elements: 128-bit words, split into four 32-bit words each and
+        // gathered into the planes with the same paired byte permutes as S <= 8; one
+        // 16-byte store per plane once both halves are packed
+        auto half_words = [&](int h, uint32_t (&wh)[S][2]) {
+            uint32_t W[8][4];
+            if (!fast_words_w<S>(bits + 8 * h, E, W)) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const u128 X = slice_word<S>(bits[8 * h + q], E);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) W[q][i] = uint32_t(X >> (32 * i));
+                }
+            }
+            pack_planes_w<S>(W, wh);
+        };
+        int8_t* out = a.planes + plane_off(a, 0, line, p0);
+        if constexpr (S > 12) {
+            // (more planes than registers for both halves: 8-byte stores per half)
+            const bool v8 = ((reinterpret_cast<uintptr_t>(out) | uintptr_t(a.plane_stride)) & 7) == 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (8 * h >= nvalid) break;
+                uint32_t wh[S][2];
+                half_words(h, wh);
+                const int nv = nvalid - 8 * h;
+                int8_t* o = out + 8 * h;
+#pragma unroll
+                for (int d = 0; d < S; ++d) {
+                    if (d >= nsl) break;
+                    if (v8 && nv >= 8) {
+                        *reinterpret_cast<uint2*>(o) = make_uint2(wh[d][0], wh[d][1]);
+                    } else {
+                        const uint64_t x = uint64_t(wh[d][0]) | (uint64_t(wh[d][1]) << 32);
+                        for (int q = 0; q < nv && q < 8; ++q) o[q] = int8_t(x >> (8 * q));
+                    }
+                    o += a.plane_stride;
+                }
+            }
+            return;
+        }
+        uint32_t w[S][4];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-            if (8 * h >= nvalid) break;
-            u128 X[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) X[q] = slice_word<S>(bits[8 * h + q], E);
+            uint32_t wh[S][2];
+            half_words(h, wh);
 #pragma unroll
             for (int d = 0; d < S; ++d) {
-                if (d >= nsl) break;
-                uint32_t lo, hi;
-                pack_plane<S>(X, d, lo, hi);
-                put8(a, d, line, p0 + 8 * h, nvalid - 8 * h, lo, hi);
+                w[d][2 * h] = wh[d][0];
+                w[d][2 * h + 1] = wh[d][1];
             }
+        }
+        const bool v16 = nvalid >= 16 && ((reinterpret_cast<uintptr_t>(out) | uintptr_t(a.plane_stride)) & 15) == 0;
+#pragma unroll
+        for (int d = 0; d < S; ++d) {
+            if (d >= nsl) break;
+            if (v16) {
+                *reinterpret_cast<uint4*>(out) = make_uint4(w[d][0], w[d][1], w[d][2], w[d][3]);
+            } else {
+                const uint64_t lo = uint64_t(w[d][0]) | (uint64_t(w[d][1]) << 32);
+                const uint64_t hi = uint64_t(w[d][2]) | (uint64_t(w[d][3]) << 32);
+                for (int q = 0; q < nvalid && q < 16; ++q) out[q] = int8_t((q < 8 ? lo : hi) >> (8 * (q & 7)));
+            }
+            out += a.plane_stride;
         }
     } else {
         int8_t dig[kMaxSlices];
