@@ -284,7 +284,11 @@ __global__ void __launch_bounds__(256, 4) esc_kernel(const int32_t* __restrict__
     __shared__ __align__(16) uint32_t sBmx[kEscTB][kEscBJ / 2];
     __shared__ __align__(16) uint32_t sBmn[kEscTB][kEscBJ / 2];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    const int64_t i0 = int64_t(blockIdx.y) * kEscBI, j0 = int64_t(blockIdx.x) * kEscBJ;
+    // A CTA owns one 128-column j tile and walks the 64-row i tiles it.y, it.y + grid.y, ...
+    // (persistent in i: the B side — offsets, and for t <= kEscTB the staged B stats —
+    // is set up once per CTA, which is what short k, e.g. C5b's t = 4, spends its time on)
+    const int64_t j0 = int64_t(blockIdx.x) * kEscBJ;
+    const int64_t tiles_m = (m + kEscBI - 1) / kEscBI;
     // B stats of column slabs of nr lines, one record of `rec` int32 per slab (the
     // all-gathered layout of the B-distributed path; nr = n: one slab): the offset of
     // column j0 + jj minus gt * nr, computed once per CTA (no division in the loops)
@@ -304,132 +308,152 @@ __global__ void __launch_bounds__(256, 4) esc_kernel(const int32_t* __restrict__
         sBoff[threadIdx.x] = r * rec + (gj - r * nr);
     }
     __syncthreads();
+    const bool probe = sStop == 0;
     // staging roles, fixed per thread: one A line (or one B column pair), every 4th block
     const int sl = threadIdx.x % 64, st0 = threadIdx.x / 64;
-    const int64_t ga = i0 + sl;
-    const bool a_ok = ga < m;
-    const int32_t* pamx = amaxT + ga;
-    const int32_t* pamn = aminT + ga;
     const bool b_ok0 = j0 + 2 * sl < n, b_ok1 = j0 + 2 * sl + 1 < n;
     const int64_t bo0 = sBoff[2 * sl], bo1 = sBoff[2 * sl + 1];
-    uint32_t z[4][4];  // [i][j pair]
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
-    auto stage_block = [&](int tt, int64_t gt) {
+    const bool b_resident = t <= kEscTB;  // one staged round holds every block of B
+    bool b_staged = false;
+    auto stage_b = [&](int tt, int64_t gt) {
         const bool tok = gt < t;
-        const int vx = a_ok && tok ? to16(pamx[gt * astride]) : kS16;
-        const int vn = a_ok && tok ? to16(pamn[gt * astride]) : kS16;
-        sAmx[tt][sl] = pack2(vx, vx);
-        sAmn[tt][sl] = pack2(vn, vn);
         const int64_t go = gt * nr;
         sBmx[tt][sl] = pack2(b_ok0 && tok ? to16(bmaxT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bmaxT[bo1 + go]) : kS16);
         sBmn[tt][sl] = pack2(b_ok0 && tok ? to16(bminT[bo0 + go]) : kS16, b_ok1 && tok ? to16(bminT[bo1 + go]) : kS16);
     };
-    auto step = [&](int tt) {
-        const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
-        const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
-        const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
-        const uint4 b_mn = *reinterpret_cast<const uint4*>(&sBmn[tt][tx * 4]);
-        const uint32_t amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
-        const uint32_t amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
-        const uint32_t bmx[4] = {b_mx.x, b_mx.y, b_mx.z, b_mx.w};
-        const uint32_t bmn[4] = {b_mn.x, b_mn.y, b_mn.z, b_mn.w};
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
-                z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
-            }
-    };
-    // spans, two j per int16x2 word: la + lb + 1 - z in [-4193, 4195] for real
-    // exponents; z <= -8000 (structurally zero dot product, or a padded row /
-    // column) is masked to -32768 so it never wins the max.
-    // max over this thread's pairs of la + lb + 1 - z, dead pairs (z <= -8000) as
-    // `dead_as` (the line maxima are re-read per call rather than held in registers
-    // across the max-plus loop)
-    auto span_max = [&](uint32_t dead_as) {
-        uint32_t lbp[4], lap[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int jj = 2 * (tx * 4 + b);
-            const int l0 = j0 + jj < n ? bline[sBoff[jj]] : 0, l1 = j0 + jj + 1 < n ? bline[sBoff[jj + 1]] : 0;
-            lbp[b] = pack2(l0 + 1, l1 + 1);
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int64_t gi = i0 + ty * 4 + a;
-            const int la = gi < m ? aline[gi] : 0;
-            lap[a] = pack2(la, la);
-        }
-        const uint32_t lim = pack2(-8000, -8000);
-        uint32_t best = pack2(-32768, -32768);
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const uint32_t span = __vsub2(__vadd2(lap[a], lbp[b]), z[a][b]);
-                const uint32_t dead = __vcmples2(z[a][b], lim);  // 0xffff per half where z <= -8000
-                best = __vmaxs2(best, (span & ~dead) | (dead_as & dead));
-            }
-        return max(int(int16_t(best & 0xffffu)), int(int16_t(best >> 16)));
-    };
     if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && ran_flag) *ran_flag = 1;
-    // Tile pruning (exact). z only grows as blocks are added, so la + lb + 1 - z over
-    // the blocks seen so far bounds every final span from above -- for pairs whose z
-    // is already live (> -8000; a dead pair may still come alive, so it bounds
-    // nothing). When that bound is <= the running maximum other CTAs have already
-    // published to esc_out, no span of this tile can raise it and the tile stops:
-    // the result is the reference's max over every (i, j). Checked after block 0
-    // and after every staged round; narrow exponent ranges (every block of every
-    // line alike) stop after one block.
-    // The block-0 probe costs each CTA a serial staging + reduction latency (~17 % of
-    // the kernel when no tile can stop), so it gives up once kProbeGiveUp probes have
-    // failed against an already published maximum (plan->esc_probe_fail; probes that
-    // found nothing published yet, as in the first wave, do not count).
-    const bool probe = sStop == 0;
-    auto prunable = [&](bool count) {
-        if (threadIdx.x == 0) sBound = -32768;
-        __syncthreads();
-        const int bnd = warp_max(span_max(0x7fff7fffu));
-        if ((threadIdx.x & 31) == 0) atomicMax(&sBound, bnd);
-        __syncthreads();
-        // one thread reads the running maximum, so the whole CTA takes the same branch
-        if (threadIdx.x == 0) {
-            const int published = *reinterpret_cast<volatile int32_t*>(esc_out);
-            sStop = sBound <= published;
-            if (count && !sStop && published > 0 && plan) atomicAdd(&const_cast<Plan*>(plan)->esc_probe_fail, 1);
-        }
-        __syncthreads();
-        return sStop != 0;
-    };
-    if (probe) {
-        if (st0 == 0) stage_block(0, 0);
-        __syncthreads();
-        step(0);
-        if (prunable(true)) return;
-    }
-    for (int64_t tb = 0; tb < t; tb += kEscTB) {
-        __syncthreads();
+    for (int64_t it = blockIdx.y; it < tiles_m; it += gridDim.y) {
+        const int64_t i0 = it * kEscBI;
+        const int64_t ga = i0 + sl;
+        const bool a_ok = ga < m;
+        const int32_t* pamx = amaxT + ga;
+        const int32_t* pamn = aminT + ga;
+        uint32_t z[4][4];  // [i][j pair]
 #pragma unroll
-        for (int tt = st0; tt < kEscTB; tt += 4) stage_block(tt, tb + tt);
-        __syncthreads();
-        if (t - tb >= kEscTB) {
-#pragma unroll 4
-            for (int tt = 0; tt < kEscTB; ++tt) step(tt);
-        } else {
-            // only the staged blocks (short k, e.g. 4 blocks at k = 1024, would
-            // otherwise spend 7/8 of the max-plus on sentinel padding)
-            const int tcount = int(t - tb);
-#pragma unroll 4
-            for (int tt = 0; tt < tcount; ++tt) step(tt);
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) z[a][b] = 0x80008000u;
+        auto stage_a = [&](int tt, int64_t gt) {
+            const bool tok = gt < t;
+            const int vx = a_ok && tok ? to16(pamx[gt * astride]) : kS16;
+            const int vn = a_ok && tok ? to16(pamn[gt * astride]) : kS16;
+            sAmx[tt][sl] = pack2(vx, vx);
+            sAmn[tt][sl] = pack2(vn, vn);
+        };
+        auto step = [&](int tt) {
+            const uint4 a_mx = *reinterpret_cast<const uint4*>(&sAmx[tt][ty * 4]);
+            const uint4 a_mn = *reinterpret_cast<const uint4*>(&sAmn[tt][ty * 4]);
+            const uint4 b_mx = *reinterpret_cast<const uint4*>(&sBmx[tt][tx * 4]);
+            const uint4 b_mn = *reinterpret_cast<const uint4*>(&sBmn[tt][tx * 4]);
+            const uint32_t amx[4] = {a_mx.x, a_mx.y, a_mx.z, a_mx.w};
+            const uint32_t amn[4] = {a_mn.x, a_mn.y, a_mn.z, a_mn.w};
+            const uint32_t bmx[4] = {b_mx.x, b_mx.y, b_mx.z, b_mx.w};
+            const uint32_t bmn[4] = {b_mn.x, b_mn.y, b_mn.z, b_mn.w};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    z[a][b] = __viaddmax_s16x2(amx[a], bmn[b], z[a][b]);
+                    z[a][b] = __viaddmax_s16x2(amn[a], bmx[b], z[a][b]);
+                }
+        };
+        // spans, two j per int16x2 word: la + lb + 1 - z in [-4193, 4195] for real
+        // exponents; z <= -8000 (structurally zero dot product, or a padded row /
+        // column) is masked to -32768 so it never wins the max.
+        // max over this thread's pairs of la + lb + 1 - z, dead pairs (z <= -8000) as
+        // `dead_as` (the line maxima are re-read per call rather than held in registers
+        // across the max-plus loop)
+        auto span_max = [&](uint32_t dead_as) {
+            uint32_t lbp[4], lap[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int jj = 2 * (tx * 4 + b);
+                const int l0 = j0 + jj < n ? bline[sBoff[jj]] : 0, l1 = j0 + jj + 1 < n ? bline[sBoff[jj + 1]] : 0;
+                lbp[b] = pack2(l0 + 1, l1 + 1);
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int64_t gi = i0 + ty * 4 + a;
+                const int la = gi < m ? aline[gi] : 0;
+                lap[a] = pack2(la, la);
+            }
+            const uint32_t lim = pack2(-8000, -8000);
+            uint32_t best = pack2(-32768, -32768);
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t span = __vsub2(__vadd2(lap[a], lbp[b]), z[a][b]);
+                    const uint32_t dead = __vcmples2(z[a][b], lim);  // 0xffff per half where z <= -8000
+                    best = __vmaxs2(best, (span & ~dead) | (dead_as & dead));
+                }
+            return max(int(int16_t(best & 0xffffu)), int(int16_t(best >> 16)));
+        };
+        // Tile pruning (exact). z only grows as blocks are added, so la + lb + 1 - z over
+        // the blocks seen so far bounds every final span from above -- for pairs whose z
+        // is already live (> -8000; a dead pair may still come alive, so it bounds
+        // nothing). When that bound is <= the running maximum already published to
+        // esc_out (by other tiles), no span of this tile can raise it and the tile stops:
+        // the result is the reference's max over every (i, j). Checked after block 0
+        // and after every staged round; narrow exponent ranges (every block of every
+        // line alike) stop after one block.
+        // The block-0 probe costs each tile a serial staging + reduction latency (~17 % of
+        // the kernel when no tile can stop), so it gives up once kProbeGiveUp probes have
+        // failed against an already published maximum (plan->esc_probe_fail; probes that
+        // found nothing published yet, as in the first wave, do not count).
+        auto prunable = [&](bool count) {
+            if (threadIdx.x == 0) sBound = -32768;
+            __syncthreads();
+            const int bnd = warp_max(span_max(0x7fff7fffu));
+            if ((threadIdx.x & 31) == 0) atomicMax(&sBound, bnd);
+            __syncthreads();
+            // one thread reads the running maximum, so the whole CTA takes the same branch
+            if (threadIdx.x == 0) {
+                const int published = *reinterpret_cast<volatile int32_t*>(esc_out);
+                sStop = sBound <= published;
+                if (count && !sStop && published > 0 && plan)
+                    atomicAdd(&const_cast<Plan*>(plan)->esc_probe_fail, 1);
+            }
+            __syncthreads();
+            return sStop != 0;
+        };
+        bool pruned = false;
+        if (probe) {
+            __syncthreads();  // the previous tile's reads of the stage are done
+            if (st0 == 0) {
+                stage_a(0, 0);
+                if (!b_resident || !b_staged) stage_b(0, 0);
+            }
+            __syncthreads();
+            step(0);
+            pruned = prunable(true);
         }
-        if (ADPB200_ESC_PRUNE && tb + kEscTB < t && prunable(false)) return;
+        for (int64_t tb = 0; tb < t && !pruned; tb += kEscTB) {
+            // only the blocks that exist are staged and stepped (short k, e.g. 4 blocks at
+            // k = 1024, would otherwise spend 7/8 of the max-plus on sentinel padding)
+            const int tcount = t - tb < kEscTB ? int(t - tb) : kEscTB;
+            __syncthreads();
+            for (int tt = st0; tt < tcount; tt += 4) {
+                stage_a(tt, tb + tt);
+                if (!b_resident || !b_staged) stage_b(tt, tb + tt);
+            }
+            __syncthreads();
+            b_staged = true;
+            if (tcount == kEscTB) {
+#pragma unroll 4
+                for (int tt = 0; tt < kEscTB; ++tt) step(tt);
+            } else {
+#pragma unroll 4
+                for (int tt = 0; tt < tcount; ++tt) step(tt);
+            }
+            if (ADPB200_ESC_PRUNE && tb + kEscTB < t && prunable(false)) pruned = true;
+        }
+        if (!pruned) {
+            // publish this tile's maximum now, so the CTAs' later tiles prune against it
+            const int esc = warp_max(max(span_max(0x80008000u), 0));
+            if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(esc_out, esc);
+        }
     }
-    int esc = warp_max(max(span_max(0x80008000u), 0));
-    if ((threadIdx.x & 31) == 0 && esc > 0) atomicMax(esc_out, esc);
 }
 
 // [lines][blocks] -> [blocks][lines] (stage export of esc_coarsened, which
@@ -574,7 +598,13 @@ void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, 
     if (m == 0 || n == 0) return;
     if (b_nr <= 0) b_nr = n;
     if (a_stride <= 0) a_stride = m;
-    dim3 grid((unsigned)((n + kEscBJ - 1) / kEscBJ), (unsigned)((m + kEscBI - 1) / kEscBI));
+    // short k (every block staged in one round, B resident): persistent in i, about two
+    // waves of CTAs (4 resident per SM) each walking i tiles; longer k: one CTA per tile,
+    // which balances the irregular work tile pruning leaves better than a static walk
+    const int64_t gx = (n + kEscBJ - 1) / kEscBJ, tiles_m = (m + kEscBI - 1) / kEscBI;
+    int64_t gy = t <= kEscTB ? int64_t(num_sms()) * 8 / gx : tiles_m;
+    gy = gy < 1 ? 1 : (gy > tiles_m ? tiles_m : gy);
+    dim3 grid((unsigned)gx, (unsigned)(gy < 65535 ? gy : 65535));
     esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, a_stride, plan,
                                      esc_out, ran_flag);
     ++*nlaunch;
