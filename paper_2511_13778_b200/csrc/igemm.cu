@@ -46,8 +46,8 @@ constexpr int kGroupM = ADPB200_GROUP_M;   // raster: m-tiles per group
 // reserved (384 threads x 168 registers): setmaxnreg.inc blocks until the pool has
 // the registers, so the split must fit it exactly or the epilogue never starts.
 constexpr int kRegsCtl = 40;
-#ifndef ADPB200_EPI48
-#define ADPB200_EPI48 12
+#ifndef ADPB200_EPI12_MAXK
+#define ADPB200_EPI12_MAXK 2048  // k up to which the NB = 48 GEMM runs 12 epilogue warps (0: never)
 #endif
 #ifndef ADPB200_NO_REGSPLIT
 #define ADPB200_SETMAXNREG(dir, n) asm volatile("setmaxnreg." dir ".sync.aligned.u32 %0;\n" ::"n"(n))
@@ -55,7 +55,7 @@ constexpr int kRegsCtl = 40;
 #define ADPB200_SETMAXNREG(dir, n) ((void)0)
 #endif
 
-template <int NB>
+template <int NB, int EW = 8>
 struct Cfg {
     // warp roles: warps 0-3 = TMA producer, MMA issuer, TMEM allocator, spare; then
     // 8 epilogue warps, 2 per TMEM lane quadrant (warp id % 4), NB/2 columns each.
@@ -63,9 +63,12 @@ struct Cfg {
     // registers) drains TMEM 2x slower; 16 epilogue warps cap registers at 96.)
     static constexpr int kFirstEpiWarp = 4;
     static constexpr int kAllocWarp = 2;
-    // NB = 48: 3 warps per quadrant (16 columns each) — with 10 diagonals per column the
-    // epilogue's fold, done while it holds TMEM, was the short-k bottleneck at 2 x 24
-    static constexpr int kEpiWarps = NB == 48 ? ADPB200_EPI48 : 8;
+    // EW = 12 (NB = 48, short k): 3 warps per quadrant (16 columns each) — with 10
+    // diagonals per column the epilogue's fold, done while it holds TMEM, was the short-k
+    // bottleneck at 2 x 24. launch_igemm picks it for k <= ADPB200_EPI12_MAXK only: over
+    // long k the 512-thread CTA ran the power-capped SMs ~30 % slower (32768^3: 970 vs
+    // 1450 MHz at the same 990 W).
+    static constexpr int kEpiWarps = EW;
     static constexpr int kEpiThreads = kEpiWarps * 32;
     static constexpr int kThreads = kFirstEpiWarp * 32 + kEpiThreads;
     static constexpr int kColGroups = kEpiWarps / 4;
@@ -448,10 +451,10 @@ __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemH
     mma_role<NB, 0, 0>(lp, hdr, sched, stage0, tmem_base, debug);
 }
 
-template <int NB>
-__global__ void __launch_bounds__(Cfg<NB>::kThreads, 1)
+template <int NB, int EW = 8>
+__global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
     igemm_kernel(const __grid_constant__ PlaneMaps maps, GemmArgs g) {
-    using C = Cfg<NB>;
+    using C = Cfg<NB, EW>;
     const Plan* plan = g.plan;
     if (plan->path != ADPB200_PATH_EMULATED || plan->variant != NB) return;
     const int s = plan->slices, L = plan->L, nsl = plan->nsl;
@@ -883,21 +886,24 @@ bool encode_plane_map(CUtensorMap* map, const int8_t* planes, int64_t slots, int
     return r == CUDA_SUCCESS;
 }
 
-template <int NB>
+template <int NB, int EW = 8>
 bool set_attr_once() {
     static int ok = -1;
     if (ok < 0) {
-        cudaFuncSetAttribute(igemm_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
+        cudaFuncSetAttribute(igemm_kernel<NB, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, kGemmSmemBytes);
         // the warpgroup register split assumes the launch reserves exactly kLaunchRegs per
         // thread; refuse to launch (an error, not a hang) if the binary says otherwise
         cudaFuncAttributes fa{};
-        ok = cudaFuncGetAttributes(&fa, igemm_kernel<NB>) == cudaSuccess && fa.numRegs == Cfg<NB>::kLaunchRegs ? 1 : 0;
+        ok = cudaFuncGetAttributes(&fa, igemm_kernel<NB, EW>) == cudaSuccess &&
+                     fa.numRegs == Cfg<NB, EW>::kLaunchRegs
+                 ? 1
+                 : 0;
 #ifdef ADPB200_NO_REGSPLIT
         ok = 1;
 #endif
         if (!ok)
-            fprintf(stderr, "adpb200: igemm_kernel<%d> uses %d registers, expected %d\n", NB, fa.numRegs,
-                    Cfg<NB>::kLaunchRegs);
+            fprintf(stderr, "adpb200: igemm_kernel<%d, %d> uses %d registers, expected %d\n", NB, EW, fa.numRegs,
+                    Cfg<NB, EW>::kLaunchRegs);
     }
     return ok == 1;
 }
@@ -958,8 +964,13 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
             igemm_kernel<64><<<grid, Cfg<64>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
             break;
         case 48:
-            if (!set_attr_once<48>()) return -3;
-            igemm_kernel<48><<<grid, Cfg<48>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            if (nkb * kKB <= ADPB200_EPI12_MAXK) {
+                if (!set_attr_once<48, 12>()) return -3;
+                igemm_kernel<48, 12><<<grid, Cfg<48, 12>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            } else {
+                if (!set_attr_once<48>()) return -3;
+                igemm_kernel<48><<<grid, Cfg<48>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            }
             break;
         case 32:
             if (!set_attr_once<32>()) return -3;
