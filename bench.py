@@ -12,10 +12,15 @@ slice pairs below the target precision are skipped (d_a + d_b <= s). For
 N > 1 the rows of A/C are partitioned (weak scaling: 8192 rows per GPU,
 B replicated) and the ADP decision inputs are max-allreduced over NCCL.
 
-The JSON line also reports native FP64 (cuBLAS via torch.matmul) on the same
-GPU, the ADP overhead against fixed-slice emulation, the U[-1,1] (s = 8) and
-bitwise-reference (all s^2 pairs) variants, the per-stage times, the roofline
-of the dominant kernel and the reference CPU implementation timed on this
+The timed region follows a 2 s soak, so `value` is the power-capped steady
+state (`value_burst`: 5 steps right after the warm-up). The JSON line also
+reports native FP64 (cuBLAS via torch.matmul) on the same GPU, the ADP overhead
+against fixed-slice emulation, the U[-1,1] (s = 8) and bitwise-reference (all
+s^2 pairs) variants, BASELINE configs 2 (U[-1,1]) and 5, the native-fallback
+flavours on an input with a NaN (config 3), config 4 (32768^3) row-partitioned
+over the N ranks beside the same problem on one GPU (`strong_c4`), the
+per-stage times, the rooflines of the slice GEMM (INT8 tensor peak) and of the
+ESC (measured DPX peak), and the reference CPU implementation timed on this
 host's cores.
 """
 from __future__ import annotations
