@@ -19,7 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import json
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Optional, Tuple
 
 import numpy as np

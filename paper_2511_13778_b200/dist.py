@@ -23,7 +23,6 @@ from typing import Optional, Sequence, Tuple
 import torch
 import torch.distributed as dist
 
-from . import _lib
 from ._lib import check, lib
 from .adp import AdpConfig, Handle, _ptr, _stream
 
