@@ -6,7 +6,7 @@
 //   recompose       proj/src/igemm.cpp:99-127  (exact combine, one RNE, alpha/beta)
 //   WideInt / round_mag_to_double   proj/include/ozadp/exactsum.hpp:50-158
 //
-// Structure (one persistent CTA per SM, 12 warps):
+// Structure (one persistent CTA per SM, 12 warps — 16 for the short-k NB = 48 instance):
 //   warp 0      TMA producer: per 32-byte k-block, nsl A slice tiles
 //               (128 rows) + nsl B slice tiles (NB rows) into one stage —
 //               one linear box per operand (planes are pre-swizzled by K3).
@@ -17,7 +17,8 @@
 //               instruction of N = c*NB whose output columns land exactly on
 //               diagonals d_a+d_b..d_a+d_b+c-1.
 //   warp 2      TMEM allocator.
-//   warps 4-11  epilogue (2 per TMEM lane quadrant, one column half each):
+//   warps 4-11  epilogue (2 per TMEM lane quadrant, one column half each;
+//               igemm_kernel<48, 12> for short k: warps 4-15, 3 per quadrant):
 //               tcgen05.ld the L+1 diagonals of a column batch,
 //               fold them exactly (Horner in NL 64-bit limbs), round once to
 //               FP64 (RNE, gradual underflow, overflow -> Inf), apply the
