@@ -124,6 +124,25 @@ __device__ __forceinline__ void limbs_shl8_add(uint64_t (&S)[NL], int64_t x) {
         carry = c1 | c2;
     }
 }
+// S = S * 2^32 + x (x a signed 64-bit value), NL-limb two's complement
+template <int NL>
+__device__ __forceinline__ void limbs_shl32_add(uint64_t (&S)[NL], int64_t x) {
+#pragma unroll
+    for (int i = NL - 1; i >= 1; --i) S[i] = (S[i] << 32) | (S[i - 1] >> 32);
+    S[0] <<= 32;
+    const uint64_t ext = x < 0 ? ~0ull : 0ull;
+    const uint64_t prev = S[0];
+    S[0] += uint64_t(x);
+    uint64_t carry = S[0] < prev ? 1ull : 0ull;
+#pragma unroll
+    for (int i = 1; i < NL; ++i) {
+        const uint64_t t = S[i] + ext;
+        const uint64_t c1 = t < S[i] ? 1ull : 0ull;
+        S[i] = t + carry;
+        const uint64_t c2 = S[i] < t ? 1ull : 0ull;
+        carry = c1 | c2;
+    }
+}
 template <int NL>
 __device__ __forceinline__ void limbs_add(uint64_t (&S)[NL], const uint64_t (&P)[NL]) {
     uint64_t carry = 0;
@@ -743,6 +762,91 @@ __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
                             }
                             const double vv = round_i128(__int128((unsigned __int128)S[1] << 64 | S[0]),
                                                          ea + ebj - 14 - 8 * (C::kNDMax - 1));
+                            double r = __dmul_rn(g.alpha, vv);
+                            if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
+                            g.c_out[row + col * g.ldc] = r;
+                        }
+                        acc_phase ^= 1;
+                        continue;
+                    }
+                }
+#ifndef ADPB200_NL3_SPLIT
+#define ADPB200_NL3_SPLIT 1
+#endif
+                if constexpr (C::kNL == 3 && ADPB200_NL3_SPLIT) {
+                    if (!g.dump) {
+                        // NB = 32 (up to 16 diagonals, e.g. all s^2 pairs at s = 7 or 8): as for
+                        // NB >= 48, phase A folds every column while holding TMEM — int64 Horner
+                        // over groups of 4 diagonals (< 2^57 each), joined 32 bits at a time in
+                        // 192 bits, all kNDMax diagonals with the missing ones as zeros so the
+                        // shifts are static (|S'| < 2^155) — parks 160 bits and hands TMEM
+                        // back; phase B rounds and stores.
+                        constexpr int kB = 2;
+                        uint32_t w[kCols][5];  // |S'| < 2^155: five 32-bit words (sign in bit 159)
+#pragma unroll
+                        for (int b = 0; b < kCols / kB; ++b) {
+                            const int j0 = jh * kCols + b * kB;
+                            uint32_t v[C::kNDMax][kB];
+#pragma unroll
+                            for (int D = 0; D < C::kNDMax; ++D) {
+                                if (D < ndiag) {
+                                    tc::tmem_ld<kB>(trow + uint32_t(D * NB + j0), v[D]);
+                                } else {
+#pragma unroll
+                                    for (int cc = 0; cc < kB; ++cc) v[D][cc] = 0u;
+                                }
+                            }
+                            tc::tmem_wait_ld();
+#pragma unroll
+                            for (int cc = 0; cc < kB; ++cc) {
+                                uint64_t S3[3];
+#pragma unroll
+                                for (int g0 = 0; g0 < C::kNDMax; g0 += 4) {
+                                    int64_t h = 0;
+#pragma unroll
+                                    for (int D = g0; D < g0 + 4; ++D) h = h * 256 + int32_t(v[D][cc]);
+                                    if (g0 == 0) {
+                                        S3[0] = uint64_t(h);
+                                        S3[1] = S3[2] = h < 0 ? ~0ull : 0ull;
+                                    } else {
+                                        limbs_shl32_add<3>(S3, h);
+                                    }
+                                }
+                                w[b * kB + cc][0] = uint32_t(S3[0]);
+                                w[b * kB + cc][1] = uint32_t(S3[0] >> 32);
+                                w[b * kB + cc][2] = uint32_t(S3[1]);
+                                w[b * kB + cc][3] = uint32_t(S3[1] >> 32);
+                                w[b * kB + cc][4] = uint32_t(S3[2]);
+                            }
+                        }
+                        tc::fence_before();
+                        tc::mbar_arrive(&hdr->tmem_empty);
+                        if (timing) hold += clock64() - th;
+                        // phase B (TMEM already back with the MMA warp): round, scale, store
+#pragma unroll
+                        for (int jl = 0; jl < kCols; ++jl) {
+                            const int ebj = __shfl_sync(0xffffffffu, eb_lane, jl);
+                            const int64_t col = col_base + jh * kCols + jl;
+                            if (!row_ok || col >= col_end || (g.debug & 2)) continue;
+                            uint64_t S[3] = {uint64_t(w[jl][0]) | (uint64_t(w[jl][1]) << 32),
+                                             uint64_t(w[jl][2]) | (uint64_t(w[jl][3]) << 32),
+                                             uint64_t(int64_t(int32_t(w[jl][4])))};  // sign-extend bit 159
+                            if (lp.nchunks > 1) {
+                                uint64_t* P = g.partial + size_t(blockIdx.x) * (3 * NB * kBM) +
+                                              size_t(jh * kCols + jl) * kBM + (q * 32 + lane);
+                                const int64_t lstride = int64_t(NB) * kBM;
+                                if (c > 0) {
+                                    const uint64_t prev[3] = {P[0], P[lstride], P[2 * lstride]};
+                                    limbs_add<3>(S, prev);
+                                }
+                                if (!last) {
+                                    P[0] = S[0];
+                                    P[lstride] = S[1];
+                                    P[2 * lstride] = S[2];
+                                    continue;
+                                }
+                            }
+                            const double vv = round_limbs<3>(S, ea + ebj - 14 - 8 * (C::kNDMax - 1));
                             double r = __dmul_rn(g.alpha, vv);
                             if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
                             g.c_out[row + col * g.ldc] = r;

@@ -1,7 +1,7 @@
 """One warm-up and one profiled ADP DGEMM call for ncu captures (8192^3 U(1,2),
 target pairs by default; --u11 for U[-1,1] operands, --certified for the
 certified ESC option, --fast-fallback for the DMMA native fallback):
-    ncu --set full --launch-skip <per-call kernels> ... python tools/one_call.py [size | m n k] [--u11] [--certified]"""
+    ncu --set full --launch-skip <per-call kernels> ... python tools/one_call.py [size | m n k] [--u11] [--certified] [--full]"""
 import os
 import sys
 
@@ -19,6 +19,8 @@ A = grading.gen_uniform_rect(k, m, 1, lo, 2.0 if lo > 0 else 1.0)  # column-majo
 B = grading.gen_uniform_rect(n, k, 2, lo, 2.0 if lo > 0 else 1.0)  # column-major k x n
 C = torch.empty((n, m), dtype=torch.float64, device="cuda")
 cfg = adp.AdpConfig(pair_limit=adp.PAIRS_TARGET, esc_method="certified" if "--certified" in sys.argv else "coarsened")
+if "--full" in sys.argv:  # all s^2 slice pairs (the reference's adp_gemm policy)
+    cfg = adp.AdpConfig(esc_method=cfg.esc_method)
 if "--fast-fallback" in sys.argv:  # the native fallback's DMMA flavour (ForceNative)
     cfg = adp.AdpConfig(mode=adp.AdpMode.ForceNative, fallback="fast")
 h = adp.Handle.default(0)
