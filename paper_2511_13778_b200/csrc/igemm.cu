@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
 #ifndef ADPB200_NL3_SPLIT
 #define ADPB200_NL3_SPLIT 1
 #endif
-                if constexpr (C::kNL == 3 && ADPB200_NL3_SPLIT) {
+                if constexpr ((C::kNL == 3 || C::kNL == 5) && ADPB200_NL3_SPLIT) {
                     if (!g.dump) {
                         // NB = 32 (up to 16 diagonals, e.g. all s^2 pairs at s = 7 or 8): as for
                         // NB >= 48, phase A folds every column while holding TMEM — int64 Horner
@@ -781,8 +781,11 @@ __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
                         // 192 bits, all kNDMax diagonals with the missing ones as zeros so the
                         // shifts are static (|S'| < 2^155) — parks 160 bits and hands TMEM
                         // back; phase B rounds and stores.
-                        constexpr int kB = 2;
-                        uint32_t w[kCols][5];  // |S'| < 2^155: five 32-bit words (sign in bit 159)
+                        // NB = 16 (up to 32 diagonals) the same with 5 limbs: |S'| < 2^283, 9 words
+                        constexpr int kNL = C::kNL;
+                        constexpr int kPW = kNL == 3 ? 5 : 9;  // parked 32-bit words (sign in the top one)
+                        constexpr int kB = kNL == 3 ? 2 : 1;
+                        uint32_t w[kCols][kPW];
 #pragma unroll
                         for (int b = 0; b < kCols / kB; ++b) {
                             const int j0 = jh * kCols + b * kB;
@@ -799,24 +802,22 @@ __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
                             tc::tmem_wait_ld();
 #pragma unroll
                             for (int cc = 0; cc < kB; ++cc) {
-                                uint64_t S3[3];
+                                uint64_t SL[kNL];
 #pragma unroll
                                 for (int g0 = 0; g0 < C::kNDMax; g0 += 4) {
                                     int64_t h = 0;
 #pragma unroll
                                     for (int D = g0; D < g0 + 4; ++D) h = h * 256 + int32_t(v[D][cc]);
                                     if (g0 == 0) {
-                                        S3[0] = uint64_t(h);
-                                        S3[1] = S3[2] = h < 0 ? ~0ull : 0ull;
+                                        SL[0] = uint64_t(h);
+#pragma unroll
+                                        for (int i = 1; i < kNL; ++i) SL[i] = h < 0 ? ~0ull : 0ull;
                                     } else {
-                                        limbs_shl32_add<3>(S3, h);
+                                        limbs_shl32_add<kNL>(SL, h);
                                     }
                                 }
-                                w[b * kB + cc][0] = uint32_t(S3[0]);
-                                w[b * kB + cc][1] = uint32_t(S3[0] >> 32);
-                                w[b * kB + cc][2] = uint32_t(S3[1]);
-                                w[b * kB + cc][3] = uint32_t(S3[1] >> 32);
-                                w[b * kB + cc][4] = uint32_t(S3[2]);
+#pragma unroll
+                                for (int i = 0; i < kPW; ++i) w[b * kB + cc][i] = uint32_t(SL[i / 2] >> (32 * (i % 2)));
                             }
                         }
                         tc::fence_before();
@@ -828,25 +829,28 @@ __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
                             const int ebj = __shfl_sync(0xffffffffu, eb_lane, jl);
                             const int64_t col = col_base + jh * kCols + jl;
                             if (!row_ok || col >= col_end || (g.debug & 2)) continue;
-                            uint64_t S[3] = {uint64_t(w[jl][0]) | (uint64_t(w[jl][1]) << 32),
-                                             uint64_t(w[jl][2]) | (uint64_t(w[jl][3]) << 32),
-                                             uint64_t(int64_t(int32_t(w[jl][4])))};  // sign-extend bit 159
+                            uint64_t S[kNL];
+#pragma unroll
+                            for (int i = 0; i < kNL - 1; ++i)
+                                S[i] = uint64_t(w[jl][2 * i]) | (uint64_t(w[jl][2 * i + 1]) << 32);
+                            S[kNL - 1] = uint64_t(int64_t(int32_t(w[jl][kPW - 1])));  // sign-extend the top word
                             if (lp.nchunks > 1) {
-                                uint64_t* P = g.partial + size_t(blockIdx.x) * (3 * NB * kBM) +
+                                uint64_t* P = g.partial + size_t(blockIdx.x) * (kNL * NB * kBM) +
                                               size_t(jh * kCols + jl) * kBM + (q * 32 + lane);
                                 const int64_t lstride = int64_t(NB) * kBM;
                                 if (c > 0) {
-                                    const uint64_t prev[3] = {P[0], P[lstride], P[2 * lstride]};
-                                    limbs_add<3>(S, prev);
+                                    uint64_t prev[kNL];
+#pragma unroll
+                                    for (int i = 0; i < kNL; ++i) prev[i] = P[i * lstride];
+                                    limbs_add<kNL>(S, prev);
                                 }
                                 if (!last) {
-                                    P[0] = S[0];
-                                    P[lstride] = S[1];
-                                    P[2 * lstride] = S[2];
+#pragma unroll
+                                    for (int i = 0; i < kNL; ++i) P[i * lstride] = S[i];
                                     continue;
                                 }
                             }
-                            const double vv = round_limbs<3>(S, ea + ebj - 14 - 8 * (C::kNDMax - 1));
+                            const double vv = round_limbs<kNL>(S, ea + ebj - 14 - 8 * (C::kNDMax - 1));
                             double r = __dmul_rn(g.alpha, vv);
                             if (g.beta != 0.0) r = __dadd_rn(r, __dmul_rn(g.beta, g.c_in[row + col * g.ldc_in]));
                             g.c_out[row + col * g.ldc] = r;
