@@ -215,6 +215,14 @@ def test_emulated_gemm_multichunk(gpu, port):
     assert_bitwise(gpu.emulated_gemm(a, b, 7), port.emulated_gemm(a, b, 7))
 
 
+def test_emulated_gemm_multichunk_16_column_variant(gpu, port):
+    # s=9 Full: 17 diagonals -> the NB = 16 variant (5-limb fold parked in registers),
+    # 9 products per diagonal -> int32 chunk 14563; k=16000 runs 2 chunks
+    a = port.gen_uniform_rect(24, 16000, 7, -1.0, 1.0)
+    b = port.gen_uniform_rect(16000, 20, 8, -1.0, 1.0)
+    assert_bitwise(gpu.emulated_gemm(a, b, 9), port.emulated_gemm(a, b, 9))
+
+
 # ---- K6: native fallback ------------------------------------------------------------------------
 @pytest.mark.parametrize("m,n,k", [(1, 1, 0), (5, 7, 1), (65, 70, 131), (130, 64, 300)])
 def test_native_gemm_bitwise(gpu, port, m, n, k):
