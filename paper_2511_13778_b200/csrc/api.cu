@@ -332,6 +332,7 @@ bool certify_wanted(const Problem& P, const adpb200_options& o, bool esc_expecte
 int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace,
                  cudaStream_t st, int fixed_slices, int fixed_limit, int64_t* dump, int ndump, int phase = 0,
                  int32_t* xchg = nullptr, const HostOut* hout = nullptr) {
+    const PdlScope pdl(P.M, P.N, P.K);
     const int cap = plane_cap(o, fixed_slices, fixed_limit);
     // only this path rounds apart, and only the NB = 64 variant parks folded words: no
     // scratch unless the plan can actually reach that variant for these options and k
@@ -489,6 +490,7 @@ __global__ void copy_if_native_kernel(const Plan* plan, const double* __restrict
 
 int run_dist(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* trace, cudaStream_t st,
              int phase, const DistIO& io) {
+    const PdlScope pdl(P.M, P.N, P.K);
     const int cap = plane_cap(o, 0, 0);
     const Layout Lw = make_layout(P.M, P.N, P.K, o.esc_block_len, cap);
     int rc = ensure_ws(h, Lw.total, st);
@@ -710,6 +712,7 @@ __global__ void spec_fixup_kernel(Plan* plan, const Plan* spec) {
 template <class CopyA, class CopyB, class CopyC>
 int run_streamed(adpb200_context* h, const Problem& P, const adpb200_options& o, adpb200_trace* tdev, cudaStream_t st,
                  cudaEvent_t a_ready, CopyA copy_a, CopyB copy_b, CopyC copy_c, bool* streamed) {
+    const PdlScope pdl(P.M, P.N, P.K);
     *streamed = false;
     if (o.mode == ADPB200_MODE_NATIVE || P.M == 0 || P.K == 0) return ADPB200_OK;
     const int cap = plane_cap(o, 0, 0);

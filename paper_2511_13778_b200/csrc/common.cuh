@@ -51,6 +51,50 @@ struct Plan {
     int32_t esc_probe_fail;  // ESC tiles whose block-0 pruning probe failed against a published maximum
 };
 
+// ---- programmatic dependent launch (PDL) along the per-call kernel chain ----
+// Every chain kernel starts with pdl_enter(): griddepcontrol.wait blocks until
+// the previous kernel of the stream has completed and its writes are visible
+// (a no-op for a kernel launched without the attribute), then
+// launch_dependents lets the next kernel's CTAs be scheduled on the slots this
+// grid leaves free. Since each kernel waits before touching memory, the order
+// of effects is the plain stream order; what the overlap removes is the launch
+// gap between consecutive kernels (~13 per call), which dominates calls below
+// ~2048^3. The trigger only fires once every CTA of this grid has executed it,
+// so waiting dependents can never take the slots of CTAs not yet started.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+
+bool pdl_enabled();  // ADPB200_PDL (default 1) and the calling thread's per-call choice
+// Per-call choice (thread-local, default on): a pipeline call turns PDL off above
+// mnk = 2^35 (ADPB200_PDL_MAX_LOG2_MNK), where the launch gaps are hidden anyway and
+// the overlap measured 0.7 % slower at 8192^3 (lower clock at the same power cap).
+struct PdlScope {
+    bool prev;
+    PdlScope(int64_t m, int64_t n, int64_t k);
+    ~PdlScope();
+};
+
+// launch a chain kernel (one that begins with pdl_enter) with the PDL attribute
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_chain(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct DecideInput {
     int32_t exc_a, exc_b;
     int64_t m, n, k;

@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
                                                          int exc_bit, int transposed, int64_t tstride) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
                                                          int32_t* __restrict__ bmin_out,
                                                          unsigned long long* counts, int32_t* exc_flag,
                                                          int exc_bit, int transposed, int64_t tstride, int groups) {
+    pdl_enter();
     // 256 / groups adjacent lines x `groups` position groups per CTA: a warp loads a
     // 256-byte coalesced row across 32 lines, and a block's positions are split over
     // the groups (combined through shared memory) when the matrix is too small to
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
 // so all-zero blocks drop out and all-zero lines stay sentinel).
 __global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lines, int64_t blocks, int64_t stride,
                                   int32_t* __restrict__ line_max) {
+    pdl_enter();
     const int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (line >= lines) return;
     int mx = kNegSentinel;
@@ -227,6 +230,7 @@ __global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lin
 
 __global__ void line_max_kernel(const int32_t* __restrict__ bmax, int64_t lines, int64_t blocks,
                                 int32_t* __restrict__ line_max) {
+    pdl_enter();
     const int64_t line = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (line >= lines) return;
@@ -277,6 +281,7 @@ __global__ void __launch_bounds__(256, 4) esc_kernel(const int32_t* __restrict__
                                                   const int32_t* __restrict__ bline, int64_t m, int64_t n,
                                                   int64_t t, int64_t nr, int64_t rec, int64_t astride,
                                                   const Plan* plan, int32_t* esc_out, int32_t* ran_flag) {
+    pdl_enter();
     if (plan && plan->exc) return;  // exceptional inputs never reach the ESC (adp.cpp:58-62)
     // A words hold (a, a); B words hold (b_j, b_j+1) for the thread's j pairs
     __shared__ __align__(16) uint32_t sAmx[kEscTB][kEscBI];
@@ -476,6 +481,7 @@ __global__ void esc_finish_kernel(int32_t* out, int target_bits) {
 // ---- the decision kernel (one thread) ---------------------------------------------
 __global__ void decide_kernel(Plan* plan, adpb200_options opt, int64_t m, int64_t n, int64_t k,
                               int esc_expected, int swap_ab, adpb200_trace* trace, int defer) {
+    pdl_enter();
     Plan& p = *plan;
     DecideInput in;
     in.exc_a = p.exc & 1;
@@ -533,6 +539,26 @@ __global__ void decide_kernel(Plan* plan, adpb200_options opt, int64_t m, int64_
 }  // namespace
 
 // ---- launchers ------------------------------------------------------------------
+namespace {
+thread_local bool t_pdl_call = true;
+}
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("ADPB200_PDL");
+        return !e || atoi(e) != 0;
+    }();
+    return on && t_pdl_call;
+}
+PdlScope::PdlScope(int64_t m, int64_t n, int64_t k) : prev(t_pdl_call) {
+    static const double max_mnk = [] {
+        const char* e = getenv("ADPB200_PDL_MAX_LOG2_MNK");
+        const int lg = e ? atoi(e) : 35;
+        return lg >= 62 ? 1e300 : double(int64_t(1) << (lg < 0 ? 0 : lg));
+    }();
+    t_pdl_call = double(m) * double(n) * double(k) <= max_mnk;
+}
+PdlScope::~PdlScope() { t_pdl_call = prev; }
+
 int num_sms() {
     static int sms = 0;
     if (!sms) {
@@ -559,7 +585,7 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
             int grid = (int)(want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16);
             if (grid < 1) grid = 1;
             // lines of a single row-major line: ps may be anything when len == 1
-            stats_rows_kernel<<<grid, 256, 0, st>>>(w, block_len, blocks, bmax, bmin, counts, exc_flag,
+            launch_chain(stats_rows_kernel, dim3(grid), dim3(256), 0, st, w, block_len, blocks, bmax, bmin, counts, exc_flag,
                                                     exc_bit, transposed, tstride);
         } else {
             // position groups per (line, block): enough threads to fill the SMs (one group at 8192^2)
@@ -567,17 +593,17 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
             while (groups < 8 && v.lines * blocks * groups < int64_t(num_sms()) * 1024) groups *= 2;
             const int width = 256 / groups;
             dim3 grid((unsigned)((v.lines + width - 1) / width), (unsigned)(blocks < 65535 ? blocks : 65535));
-            stats_cols_kernel<<<grid, 256, 0, st>>>(v, block_len, blocks, bmax, bmin, counts, exc_flag,
+            launch_chain(stats_cols_kernel, grid, dim3(256), 0, st, v, block_len, blocks, bmax, bmin, counts, exc_flag,
                                                     exc_bit, transposed, tstride, groups);
         }
         ++*nlaunch;
     }
     if (transposed) {
-        line_max_t_kernel<<<(unsigned)((v.lines + 255) / 256), 256, 0, st>>>(bmax, v.lines, blocks, tstride,
+        launch_chain(line_max_t_kernel, dim3((unsigned)((v.lines + 255) / 256)), dim3(256), 0, st, bmax, v.lines, blocks, tstride,
                                                                                line_max);
     } else {
         int lgrid = (int)((v.lines * 32 + 255) / 256);
-        line_max_kernel<<<lgrid, 256, 0, st>>>(bmax, v.lines, blocks, line_max);
+        launch_chain(line_max_kernel, dim3(lgrid), dim3(256), 0, st, bmax, v.lines, blocks, line_max);
     }
     ++*nlaunch;
 }
@@ -605,7 +631,7 @@ void launch_esc(const int32_t* amax, const int32_t* amin, const int32_t* aline, 
     int64_t gy = t <= kEscTB ? int64_t(num_sms()) * 8 / gx : tiles_m;
     gy = gy < 1 ? 1 : (gy > tiles_m ? tiles_m : gy);
     dim3 grid((unsigned)gx, (unsigned)(gy < 65535 ? gy : 65535));
-    esc_kernel<<<grid, 256, 0, st>>>(amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, a_stride, plan,
+    launch_chain(esc_kernel, grid, dim3(256), 0, st, amax, amin, aline, bmax, bmin, bline, m, n, t, b_nr, b_rec, a_stride, plan,
                                      esc_out, ran_flag);
     ++*nlaunch;
 }
@@ -726,7 +752,7 @@ void launch_dist_import(Plan* plan, const int32_t* xchg, int target_bits, int ce
 
 void launch_decide(Plan* plan, const adpb200_options& opt, int64_t m, int64_t n, int64_t k, int esc_expected,
                    int swap_ab, adpb200_trace* trace, cudaStream_t st, uint64_t* nlaunch, int defer) {
-    decide_kernel<<<1, 1, 0, st>>>(plan, opt, m, n, k, esc_expected, swap_ab, trace, defer);
+    launch_chain(decide_kernel, dim3(1), dim3(1), 0, st, plan, opt, m, n, k, esc_expected, swap_ab, trace, defer);
     ++*nlaunch;
 }
 

@@ -474,6 +474,8 @@ __device__ __forceinline__ void mma_dispatch(int s, int L, const Loop& lp, SmemH
 template <int NB, int EW = 8>
 __global__ void __launch_bounds__(Cfg<NB, EW>::kThreads, 1)
     igemm_kernel(const __grid_constant__ PlaneMaps maps, GemmArgs g) {
+    pdl_wait();
+    if (g.pdl_early) pdl_trigger();
     using C = Cfg<NB, EW>;
     const Plan* plan = g.plan;
     if (plan->path != ADPB200_PATH_EMULATED || plan->variant != NB) return;
@@ -1067,31 +1069,36 @@ int launch_igemm(int nb, const int8_t* planes_a, const int8_t* planes_b, int64_t
     }();
     a.debug = debug;
     a.smem_bytes = kGemmSmemBytes;
+    static const int pdl_early = [] {
+        const char* e = getenv("ADPB200_PDL_GEMM_EARLY");
+        return e ? atoi(e) : 0;
+    }();
+    a.pdl_early = pdl_early;
     switch (nb) {
         case 64:
             if (!set_attr_once<64>()) return -3;
-            igemm_kernel<64><<<grid, Cfg<64>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            launch_chain(igemm_kernel<64>, dim3(grid), dim3(Cfg<64>::kThreads), kGemmSmemBytes, st, e.maps, a);
             break;
         case 48:
             if (nkb * kKB <= ADPB200_EPI12_MAXK) {
                 if (!set_attr_once<48, 12>()) return -3;
-                igemm_kernel<48, 12><<<grid, Cfg<48, 12>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+                launch_chain(igemm_kernel<48, 12>, dim3(grid), dim3(Cfg<48, 12>::kThreads), kGemmSmemBytes, st, e.maps, a);
             } else {
                 if (!set_attr_once<48>()) return -3;
-                igemm_kernel<48><<<grid, Cfg<48>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+                launch_chain(igemm_kernel<48>, dim3(grid), dim3(Cfg<48>::kThreads), kGemmSmemBytes, st, e.maps, a);
             }
             break;
         case 32:
             if (!set_attr_once<32>()) return -3;
-            igemm_kernel<32><<<grid, Cfg<32>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            launch_chain(igemm_kernel<32>, dim3(grid), dim3(Cfg<32>::kThreads), kGemmSmemBytes, st, e.maps, a);
             break;
         case 16:
             if (!set_attr_once<16>()) return -3;
-            igemm_kernel<16><<<grid, Cfg<16>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            launch_chain(igemm_kernel<16>, dim3(grid), dim3(Cfg<16>::kThreads), kGemmSmemBytes, st, e.maps, a);
             break;
         case 8:
             if (!set_attr_once<8>()) return -3;
-            igemm_kernel<8><<<grid, Cfg<8>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+            launch_chain(igemm_kernel<8>, dim3(grid), dim3(Cfg<8>::kThreads), kGemmSmemBytes, st, e.maps, a);
             break;
         default:
             return -2;
@@ -1169,7 +1176,7 @@ int launch_peer_nb(PeerCacheEntry& e, const int8_t* planes_a, int64_t slots_a, i
     const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) return 0;
     if (!set_attr_once<NB>()) return -3;
-    igemm_kernel<NB><<<grid, Cfg<NB>::kThreads, kGemmSmemBytes, st>>>(e.maps, a);
+    launch_chain(igemm_kernel<NB>, dim3(grid), dim3(Cfg<NB>::kThreads), kGemmSmemBytes, st, e.maps, a);
     return 0;
 }
 }  // namespace

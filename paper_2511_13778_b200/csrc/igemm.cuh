@@ -42,6 +42,7 @@ struct GemmArgs {
     int64_t peer_nr;
     const int32_t* peer_scale[kMaxPeers];
     int peer_rank[kMaxPeers];  // global rank of each of those entries (its column offset)
+    int pdl_early;             // trigger the dependent launch at kernel entry (else at exit)
 };
 
 // Fused peer variant of launch_igemm: B from world slab records ([scale int32 x nr |

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256, 1) native_kernel(LineView a, LineView b, 
                                                         const double* __restrict__ c_in, int64_t ldc_in,
                                                         double* __restrict__ c_out, int64_t ldc, const Plan* plan,
                                                         PeerB pb) {
+    pdl_enter();
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
     extern __shared__ __align__(16) double nsm[];
     // [buf][operand][k][line]
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) dmma_kernel(LineView a, LineVi
                                                               const double* __restrict__ c_in, int64_t ldc_in,
                                                               double* __restrict__ c_out, int64_t ldc,
                                                               const Plan* plan) {
+    pdl_enter();
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
     constexpr int kThreads = kWarps * 32;
     constexpr int kWarpsM = kWarps == 8 ? 2 : 4, kWarpsN = 4;
@@ -325,6 +327,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) dmma_ws_kernel(LineView a, Line
                                                                 const double* __restrict__ c_in, int64_t ldc_in,
                                                                 double* __restrict__ c_out, int64_t ldc,
                                                                 const Plan* plan, PeerB pb) {
+    pdl_enter();
     if (plan && plan->path != ADPB200_PATH_NATIVE) return;
     extern __shared__ __align__(128) unsigned char dws[];
     uint64_t* full = reinterpret_cast<uint64_t*>(dws);
@@ -489,7 +492,7 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         const Fn fn = fns[(use_peer ? 4 : 0) + (a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
         const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), kWsThreads, kDmmaWsSmem, tiles);
-        fn<<<grid, kWsThreads, kDmmaWsSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
+        launch_chain(fn, dim3(grid), dim3(kWsThreads), kDmmaWsSmem, st, a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
     } else if (flavour == ADPB200_FALLBACK_FAST) {
         // operand layouts in shared memory follow the contiguous direction in HBM
         using Fn0 = void (*)(LineView, LineView, double, double, const double*, int64_t, double*, int64_t,
@@ -506,7 +509,7 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         const Fn0 fn = fns[(a.ls == 1 ? 2 : 0) + (b.ls == 1 ? 1 : 0)];
         const int64_t tiles = ((a.lines + kDT - 1) / kDT) * ((b.lines + kDT - 1) / kDT);
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), kDmmaWarps * 32, kDmmaSmem, tiles);
-        fn<<<grid, kDmmaWarps * 32, kDmmaSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
+        launch_chain(fn, dim3(grid), dim3(kDmmaWarps * 32), kDmmaSmem, st, a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan);
     } else {
         static const Fn fns[2] = {native_kernel<false>, native_kernel<true>};
         static bool attr = false;
@@ -519,7 +522,7 @@ void launch_native(const LineView& a, const LineView& b, double alpha, double be
         const Fn fn = fns[use_peer ? 1 : 0];
         const int64_t tiles = ((a.lines + kT - 1) / kT) * ((b.lines + kT - 1) / kT);
         const int grid = resident_grid(reinterpret_cast<const void*>(fn), 256, kNativeSmem, tiles);
-        fn<<<grid, 256, kNativeSmem, st>>>(a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
+        launch_chain(fn, dim3(grid), dim3(256), kNativeSmem, st, a, b, alpha, beta, c_in, ldc_in, c_out, ldc, plan, pb);
     }
     ++*nlaunch;
 }

@@ -634,6 +634,7 @@ __device__ __forceinline__ void staged_body(const SliceArgs& a, int nsl, int64_t
 
 template <bool kRows, bool kVec>
 __global__ void __launch_bounds__(256, 3) slice_kernel(SliceArgs a) {
+    pdl_enter();
     int s, nsl;
     if (!resolve(a, s, nsl)) return;
     extern __shared__ __align__(16) char smem[];
@@ -695,7 +696,7 @@ void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, in
     }
     const int64_t cap = int64_t(num_sms()) * res[which];
     const int grid = int(tiles < cap ? tiles : cap);
-    fns[which]<<<grid, 256, kSliceSmem, st>>>(a);
+    launch_chain(fns[which], dim3(grid), dim3(256), kSliceSmem, st, a);
     ++*nlaunch;
 }
 

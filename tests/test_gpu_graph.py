@@ -53,3 +53,39 @@ def test_graphed_dgemm_helper(gpu):
         gpu.dgemm("N", "T", n, n, n, 0.5, A, n, B, n, 0.0, C, n, cfg)
         torch.cuda.synchronize()
         assert torch.equal(C.view(torch.int64), Cg.view(torch.int64))
+
+
+_PDL_SCRIPT = r"""
+import hashlib, sys, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2511_13778_b200 as adp
+from paper_2511_13778_b200 import grading
+out = []
+for (m, n, k, lo, ff) in ((384, 320, 1000, -1.0, None), (512, 512, 512, 1.0, None), (300, 200, 260, 1.0, "fast")):
+    A = grading.gen_uniform_rect(k, m, 3, lo, 2.0 if lo > 0 else 1.0)
+    B = grading.gen_uniform_rect(n, k, 4, lo, 2.0 if lo > 0 else 1.0)
+    C = torch.empty((n, m), dtype=torch.float64, device="cuda")
+    cfg = adp.AdpConfig(mode=adp.AdpMode.ForceNative, fallback=ff) if ff else adp.AdpConfig()
+    h = adp.Handle(0)
+    for _ in range(3):  # repeated calls: the chain of one call follows the previous call's kernels
+        adp.dgemm("N", "N", m, n, k, 1.0, A, m, B, k, 0.0, C, m, cfg, h)
+    torch.cuda.synchronize()
+    out.append(hashlib.sha256(C.cpu().numpy().tobytes()).hexdigest())
+print(" ".join(out))
+"""
+
+
+def test_programmatic_dependent_launch_bitwise():
+    """The chain kernels launched with programmatic dependent launch (default for small
+    calls) give the same bits as plain stream serialisation (ADPB200_PDL=0)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for pdl in ("1", "0"):
+        env = dict(os.environ, ADPB200_PDL=pdl)
+        res[pdl] = subprocess.run([sys.executable, "-c", _PDL_SCRIPT, root], env=env, capture_output=True,
+                                  text=True, check=True, timeout=600).stdout.strip()
+    assert res["1"] and res["1"] == res["0"]
