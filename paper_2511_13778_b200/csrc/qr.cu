@@ -76,6 +76,7 @@ __device__ __forceinline__ double seq_dot(double init, const double* __restrict_
 
 __global__ void panel_load_kernel(const double* __restrict__ f, int64_t ld, int64_t p0, int64_t rows, int pw,
                                   double* __restrict__ P) {
+    pdl_enter();
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pw; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / pw, j = e - r * pw;
         P[j * rows + r] = f[(p0 + r) * ld + p0 + j];
@@ -169,6 +170,7 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __restrict__ P, int64_t rows, int j,
                                                                   double* __restrict__ tau,
                                                                   double* __restrict__ vglob) {
+    pdl_enter();
     extern __shared__ double vsh[];
     double* v = kSmem ? vsh : vglob;
     double* col = P + int64_t(j) * rows;
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(kPanelThreads) reflector_kernel(double* __rest
 template <bool kStaged>
 __global__ void __launch_bounds__(kPanelThreads) apply_kernel(double* __restrict__ P, int64_t rows, int j,
                                                               const double* __restrict__ tau) {
+    pdl_enter();
     const double tj = tau[j];
     if (tj == 0.0) return;
     extern __shared__ double sh[];
@@ -215,6 +218,7 @@ __global__ void __launch_bounds__(kPanelThreads) apply_kernel(double* __restrict
 // column; the other CTAs' updates run meanwhile. Shared-memory (staged) path only.
 __global__ void __launch_bounds__(kPanelThreads) apply_reflect_kernel(double* __restrict__ P, int64_t rows, int j,
                                                                       double* __restrict__ tau) {
+    pdl_enter();
     const double tj = tau[j];
     const bool next = blockIdx.x == 0;  // this CTA owns column j + 1
     if (tj == 0.0 && !next) return;
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(kPanelThreads) apply_reflect_kernel(double* __
 // write the panel back to f; build_y (qr.cpp:64-71)
 __global__ void panel_store_kernel(const double* __restrict__ P, double* __restrict__ f, int64_t ld, int64_t p0,
                                    int64_t rows, int pw, double* __restrict__ y, double* __restrict__ yT) {
+    pdl_enter();
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pw; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / pw, j = e - r * pw;
         const double val = P[j * rows + r];
@@ -270,6 +275,7 @@ __global__ void panel_store_kernel(const double* __restrict__ P, double* __restr
 template <bool kStaged>
 __global__ void __launch_bounds__(kPanelThreads) build_z_kernel(const double* __restrict__ P, int64_t rows, int pw,
                                                                 double* __restrict__ z) {
+    pdl_enter();
     extern __shared__ double sh[];
     const int j = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
     if (j == 0) return;
@@ -290,6 +296,7 @@ template <bool kSmem>
 __global__ void __launch_bounds__(kPanelThreads) build_t_kernel(const double* __restrict__ tau,
                                                                 const double* __restrict__ z, int pw,
                                                                 double* __restrict__ t, double* __restrict__ tT) {
+    pdl_enter();
     // T (pw x pw) in shared memory when it fits, and z's column j staged per step: the
     // short sequential dots of the recursion then read LDS instead of global memory
     extern __shared__ double tsh[];
@@ -322,6 +329,7 @@ __global__ void __launch_bounds__(kPanelThreads) build_t_kernel(const double* __
 // dst (rows x cols, leading dimension ldd) = src (leading dimension lds)
 __global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst, int64_t ldd,
                                   int64_t rows, int64_t cols) {
+    pdl_enter();
     const int64_t total = rows * cols;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / cols, c = e - r * cols;
@@ -454,37 +462,37 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         // memory when it fits: sequential sums at shared-memory latency
         const size_t vbytes = 2 * size_t(rows) * sizeof(double);
         const bool vsmem = vbytes <= kPanelSmemMax;
-        panel_load_kernel<<<grid_for(rows * pw), 256, 0, st>>>(f, n, p0, rows, pw, P);
+        launch_chain(panel_load_kernel, dim3(grid_for(rows * pw)), dim3(256), 0, st, f, n, p0, rows, pw, P);
         ++*nl;
         if (vsmem) {
             // one launch per column: update the later columns, make the next reflector
-            reflector_kernel<true><<<1, threads, vbytes, st>>>(P, rows, 0, tau, nullptr);
+            launch_chain(reflector_kernel<true>, dim3(1), dim3(threads), vbytes, st, P, rows, 0, tau, nullptr);
             ++*nl;
             for (int j = 0; j + 1 < pw; ++j) {
-                apply_reflect_kernel<<<unsigned(pw - j - 1), threads, vbytes, st>>>(P, rows, j, tau);
+                launch_chain(apply_reflect_kernel, dim3(unsigned(pw - j - 1)), dim3(threads), vbytes, st, P, rows, j, tau);
                 ++*nl;
             }
         } else {
             for (int j = 0; j < pw; ++j) {
-                reflector_kernel<false><<<1, threads, 0, st>>>(P, rows, j, tau, vg);
+                launch_chain(reflector_kernel<false>, dim3(1), dim3(threads), 0, st, P, rows, j, tau, vg);
                 ++*nl;
                 if (j + 1 < pw) {
-                    apply_kernel<false><<<unsigned(pw - j - 1), threads, 0, st>>>(P, rows, j, tau);
+                    launch_chain(apply_kernel<false>, dim3(unsigned(pw - j - 1)), dim3(threads), 0, st, P, rows, j, tau);
                     ++*nl;
                 }
             }
         }
-        panel_store_kernel<<<grid_for(rows * pw), 256, 0, st>>>(P, f, n, p0, rows, pw, y, yT);
-        if (vsmem) build_z_kernel<true><<<unsigned(pw), threads, vbytes / 2, st>>>(P, rows, pw, z);
-        else build_z_kernel<false><<<unsigned(pw), threads, 0, st>>>(P, rows, pw, z);
+        launch_chain(panel_store_kernel, dim3(grid_for(rows * pw)), dim3(256), 0, st, P, f, n, p0, rows, pw, y, yT);
+        if (vsmem) launch_chain(build_z_kernel<true>, dim3(unsigned(pw)), dim3(threads), vbytes / 2, st, P, rows, pw, z);
+        else launch_chain(build_z_kernel<false>, dim3(unsigned(pw)), dim3(threads), 0, st, P, rows, pw, z);
         const size_t tbytes = (size_t(pw) * pw + pw) * sizeof(double);
-        if (tbytes <= kPanelSmemMax) build_t_kernel<true><<<1, threads, tbytes, st>>>(tau, z, pw, t, tT);
-        else build_t_kernel<false><<<1, threads, 0, st>>>(tau, z, pw, t, tT);
+        if (tbytes <= kPanelSmemMax) launch_chain(build_t_kernel<true>, dim3(1), dim3(threads), tbytes, st, tau, z, pw, t, tT);
+        else launch_chain(build_t_kernel<false>, dim3(1), dim3(threads), 0, st, tau, z, pw, t, tT);
         *nl += 3;
-        copy_block_kernel<<<grid_for(int64_t(pw) * pw), 256, 0, st>>>(t, pw, t_blocks + p * panel * panel, pw, pw, pw);
+        launch_chain(copy_block_kernel, dim3(grid_for(int64_t(pw) * pw)), dim3(256), 0, st, t, pw, t_blocks + p * panel * panel, pw, pw, pw);
         ++*nl;
         if (nt > 0) {
-            copy_block_kernel<<<grid_for(rows * nt), 256, 0, st>>>(f + p0 * n + p0 + pw, n, as, nt, rows, nt);
+            launch_chain(copy_block_kernel, dim3(grid_for(rows * nt)), dim3(256), 0, st, f + p0 * n + p0 + pw, n, as, nt, rows, nt);
             ++*nl;
         }
         // A_s -= Y T^T Y^T A_s, all three products dispatched (qr.cpp:127-132)
@@ -493,7 +501,7 @@ int qr_geqrf(adpb200_handle h, int64_t m, int64_t n, int64_t panel, double* f, d
         if (!rc) rc = adpb200_adp_gemm(h, rows, nt, pw, -1.0, y, w2, 1.0, as, up, opt, traces + 3 * p + 2, st);
         if (rc) return rc;
         if (nt > 0) {
-            copy_block_kernel<<<grid_for(rows * nt), 256, 0, st>>>(up, nt, f + p0 * n + p0 + pw, n, rows, nt);
+            launch_chain(copy_block_kernel, dim3(grid_for(rows * nt)), dim3(256), 0, st, up, nt, f + p0 * n + p0 + pw, n, rows, nt);
             ++*nl;
         }
     }
