@@ -407,8 +407,9 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
         int32_t* sa = at<int32_t>(h, Lw.scale_a);
         int32_t* sb = at<int32_t>(h, Lw.scale_b);
         tm.begin(3);
-        launch_slice(P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, 1, sa, plan, fixed_slices, cap, st, nl);
-        launch_slice(P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, 1, sb, plan, fixed_slices, cap, st, nl);
+        launch_slice_pair(SliceOperand{P.a, aline, pa, Lw.slots_a, Lw.pitch * Lw.slots_a, sa},
+                          SliceOperand{P.b, bline, pb, Lw.slots_b, Lw.pitch * Lw.slots_b, sb}, 1, plan, fixed_slices,
+                          cap, st, nl);
         tm.end(3);
         // K4/K5: one launch per GEMM variant; exactly one does work
         GemmArgs g = product_args(h, Lw, P, plan, sb);

@@ -56,6 +56,17 @@ void launch_set_plan(Plan* plan, int s, int pair_limit, int64_t k, cudaStream_t 
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
                   int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
                   uint64_t* nlaunch, int indicator = 0);
+// Slicing of both operands (same plan and blocking): one launch when the layouts
+// allow it (ADPB200_SLICE_PAIR, default 1), else two launch_slice calls.
+struct SliceOperand {
+    LineView v;
+    const int32_t* line_max;
+    int8_t* planes;
+    int64_t pitch, plane_stride;
+    int32_t* scale;
+};
+void launch_slice_pair(const SliceOperand& A, const SliceOperand& B, int blocked, const Plan* plan, int slices_fixed,
+                       int plane_cap, cudaStream_t st, uint64_t* nlaunch);
 
 // Certified ESC (adpb200_options.esc_method): prep turns the coarsened result in
 // `plan` into the indicator-GEMM plan `rplan` (path kPathDone when there is

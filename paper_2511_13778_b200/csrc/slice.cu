@@ -258,6 +258,7 @@ struct SliceArgs {
     int slices_fixed;
     int indicator;         // certified ESC: plan->nsl planes of (e >= line_max - delta) bytes,
                            // delta = plan->aux (plane 0) / plan->aux2 (plane 1)
+    int plane_cap;         // planes the buffer holds (> 0): digit planes past it are not stored
 };
 
 // Certified-ESC indicator bytes of 8 elements: 1 where the element is finite,
@@ -284,11 +285,13 @@ __device__ __forceinline__ bool resolve(const SliceArgs& a, int& s, int& nsl) {
     if (a.slices_fixed > 0) {
         s = a.slices_fixed;
         nsl = s;
-        return true;
+    } else {
+        if (a.plan->path != ADPB200_PATH_EMULATED) return false;
+        s = a.plan->slices;
+        nsl = a.plan->nsl;
     }
-    if (a.plan->path != ADPB200_PATH_EMULATED) return false;
-    s = a.plan->slices;
-    nsl = a.plan->nsl;
+    // a fixed s with a pair limit L only uses planes 0..L (the buffer holds L + 1)
+    if (!a.indicator && a.plane_cap > 0 && nsl > a.plane_cap) nsl = a.plane_cap;
     return true;
 }
 
@@ -487,16 +490,17 @@ struct Tiler {
     static constexpr int kL = kRows ? kRowsLines : kColsLines;
     static constexpr int kP = kRows ? kRowsPos : kColsPos;
     const SliceArgs& a;
-    int64_t nlt, npt, glt, gpt;  // tiles along lines / positions; gridDim.x as (lines, positions) step
-    __device__ __forceinline__ Tiler(const SliceArgs& a_, int64_t span) : a(a_) {
+    int64_t nlt, npt, glt, gpt;  // tiles along lines / positions; the CTA count as (lines, positions) step
+    int64_t cta;
+    __device__ __forceinline__ Tiler(const SliceArgs& a_, int64_t span, int cta_, int nctas) : a(a_), cta(cta_) {
         nlt = (a.v.lines + kL - 1) / kL;
         npt = (span + kP - 1) / kP;
-        gpt = int64_t(gridDim.x) / nlt;
-        glt = int64_t(gridDim.x) - gpt * nlt;
+        gpt = int64_t(nctas) / nlt;
+        glt = int64_t(nctas) - gpt * nlt;
     }
     __device__ __forceinline__ TileIdx first() const {
-        const int64_t pt = int64_t(blockIdx.x) / nlt;
-        return TileIdx{int64_t(blockIdx.x) - pt * nlt, pt};
+        const int64_t pt = cta / nlt;
+        return TileIdx{cta - pt * nlt, pt};
     }
     __device__ __forceinline__ void step(TileIdx& t) const {
         t.lt += glt;
@@ -598,8 +602,9 @@ struct Tiler {
 };
 
 template <int S, bool kRows, bool kVec>
-__device__ __forceinline__ void staged_body(const SliceArgs& a, int nsl, int64_t span, char* smem) {
-    const Tiler<kRows, kVec> T(a, span);
+__device__ __forceinline__ void staged_body(const SliceArgs& a, int nsl, int64_t span, char* smem, int cta,
+                                            int nctas) {
+    const Tiler<kRows, kVec> T(a, span, cta, nctas);
     const uint32_t s0 = uint32_t(__cvta_generic_to_shared(smem));
     int lsub, psub;
     T.mine(lsub, psub);
@@ -632,28 +637,45 @@ __device__ __forceinline__ void staged_body(const SliceArgs& a, int nsl, int64_t
     cp_wait<0>();
 }
 
+// one operand's slicing by CTAs cta = 0..nctas-1 of the grid
 template <bool kRows, bool kVec>
-__global__ void __launch_bounds__(256, 3) slice_kernel(SliceArgs a) {
-    pdl_enter();
+__device__ __forceinline__ void slice_operand(const SliceArgs& a, char* smem, int cta, int nctas) {
     int s, nsl;
     if (!resolve(a, s, nsl)) return;
-    extern __shared__ __align__(16) char smem[];
     // blocked planes are zero-filled up to the 32-byte k-block
     const int64_t span = a.blocked ? (a.v.len + 31) / 32 * 32 : a.v.len;
     if (a.indicator) {
-        staged_body<0, kRows, kVec>(a, nsl, span, smem);
+        staged_body<0, kRows, kVec>(a, nsl, span, smem, cta, nctas);
         return;
     }
     switch (s) {
 #define ADPB200_SLICE_CASE(S) \
-    case S: staged_body<S, kRows, kVec>(a, nsl, span, smem); break;
+    case S: staged_body<S, kRows, kVec>(a, nsl, span, smem, cta, nctas); break;
         ADPB200_SLICE_CASE(1) ADPB200_SLICE_CASE(2) ADPB200_SLICE_CASE(3) ADPB200_SLICE_CASE(4)
         ADPB200_SLICE_CASE(5) ADPB200_SLICE_CASE(6) ADPB200_SLICE_CASE(7) ADPB200_SLICE_CASE(8)
         ADPB200_SLICE_CASE(9) ADPB200_SLICE_CASE(10) ADPB200_SLICE_CASE(11) ADPB200_SLICE_CASE(12)
         ADPB200_SLICE_CASE(13) ADPB200_SLICE_CASE(14) ADPB200_SLICE_CASE(15) ADPB200_SLICE_CASE(16)
 #undef ADPB200_SLICE_CASE
-        default: staged_body<32, kRows, kVec>(a, nsl, span, smem); break;
+        default: staged_body<32, kRows, kVec>(a, nsl, span, smem, cta, nctas); break;
     }
+}
+
+template <bool kRows, bool kVec>
+__global__ void __launch_bounds__(256, 3) slice_kernel(SliceArgs a) {
+    pdl_enter();
+    extern __shared__ __align__(16) char smem[];
+    slice_operand<kRows, kVec>(a, smem, blockIdx.x, gridDim.x);
+}
+
+// Both operands in one launch (the common layout: A-lines with adjacent lines,
+// B-lines contiguous): CTAs [0, grid_a) slice A, the rest B. At small sizes one
+// operand alone does not fill the SMs' slots and the second launch is one more
+// kernel boundary on the call's critical path.
+__global__ void __launch_bounds__(256, 3) slice_pair_kernel(SliceArgs a, SliceArgs b, int grid_a) {
+    pdl_enter();
+    extern __shared__ __align__(16) char smem[];
+    if (int(blockIdx.x) < grid_a) slice_operand<false, true>(a, smem, blockIdx.x, grid_a);
+    else slice_operand<true, true>(b, smem, int(blockIdx.x) - grid_a, int(gridDim.x) - grid_a);
 }
 
 using SliceFn = void (*)(SliceArgs);
@@ -670,33 +692,94 @@ int resident(SliceFn fn) {
 
 }  // namespace
 
+namespace {
+struct SlicePrep {
+    SliceArgs a;
+    int which;      // 0 cols, 1 cols 16-byte, 2 rows, 3 rows 16-byte
+    int64_t tiles;  // 0: nothing to do
+};
+
+const SliceFn kSliceFns[4] = {slice_kernel<false, false>, slice_kernel<false, true>, slice_kernel<true, false>,
+                              slice_kernel<true, true>};
+
+int slice_resident(int which) {  // which 4 = the paired kernel
+    static int res[5] = {0, 0, 0, 0, 0};
+    if (!res[0]) {
+        for (int i = 0; i < 4; ++i) res[i] = resident(kSliceFns[i]);
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(slice_pair_kernel),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSliceSmem));
+        int per_sm = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, slice_pair_kernel, 256, kSliceSmem) !=
+                cudaSuccess ||
+            per_sm < 1)
+            per_sm = 1;
+        res[4] = per_sm;
+    }
+    return res[which];
+}
+
+SlicePrep prep_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
+                     int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int indicator, int plane_cap) {
+    SlicePrep p{
+        SliceArgs{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed, indicator, plane_cap},
+        0, 0};
+    const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
+    if (v.lines == 0 || span == 0) return p;
+    const bool aligned = (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
+    if (v.ps == 1 || v.len == 1) {
+        if (v.lines == 1) p.a.v.ls = 0;
+        p.which = 2 + ((aligned && (p.a.v.ls & 1) == 0) ? 1 : 0);  // 16-byte chunks need even line starts
+        p.tiles = (v.lines + kRowsLines - 1) / kRowsLines * ((span + kRowsPos - 1) / kRowsPos);
+    } else {
+        p.which = (aligned && v.ls == 1 && (v.ps & 1) == 0) ? 1 : 0;  // two adjacent lines per 16-byte chunk
+        p.tiles = (v.lines + kColsLines - 1) / kColsLines * ((span + kColsPos - 1) / kColsPos);
+    }
+    return p;
+}
+
+void launch_prepped(const SlicePrep& p, cudaStream_t st, uint64_t* nlaunch) {
+    if (!p.tiles) return;
+    const int64_t cap = int64_t(num_sms()) * slice_resident(p.which);
+    const int grid = int(p.tiles < cap ? p.tiles : cap);
+    launch_chain(kSliceFns[p.which], dim3(grid), dim3(256), kSliceSmem, st, p.a);
+    ++*nlaunch;
+}
+}  // namespace
+
 void launch_slice(const LineView& v, const int32_t* line_max, int8_t* planes, int64_t pitch, int64_t plane_stride,
                   int blocked, int32_t* scale, const Plan* plan, int slices_fixed, int plane_cap, cudaStream_t st,
                   uint64_t* nlaunch, int indicator) {
-    (void)plane_cap;
-    if (v.lines == 0) return;
-    SliceArgs a{v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed, indicator};
-    const int64_t span = blocked ? (v.len + 31) / 32 * 32 : v.len;
-    if (span == 0) return;
-    static const SliceFn fns[4] = {slice_kernel<false, false>, slice_kernel<false, true>, slice_kernel<true, false>,
-                                   slice_kernel<true, true>};
-    static int res[4] = {0, 0, 0, 0};
-    if (!res[0])
-        for (int i = 0; i < 4; ++i) res[i] = resident(fns[i]);
-    const bool aligned = (reinterpret_cast<uintptr_t>(v.ptr) & 15) == 0;
-    int which;
-    int64_t tiles;
-    if (v.ps == 1 || v.len == 1) {
-        if (v.lines == 1) a.v.ls = 0;
-        which = 2 + ((aligned && (a.v.ls & 1) == 0) ? 1 : 0);  // 16-byte chunks need even line starts
-        tiles = (v.lines + kRowsLines - 1) / kRowsLines * ((span + kRowsPos - 1) / kRowsPos);
-    } else {
-        which = (aligned && v.ls == 1 && (v.ps & 1) == 0) ? 1 : 0;  // two adjacent lines per 16-byte chunk
-        tiles = (v.lines + kColsLines - 1) / kColsLines * ((span + kColsPos - 1) / kColsPos);
+    launch_prepped(
+        prep_slice(v, line_max, planes, pitch, plane_stride, blocked, scale, plan, slices_fixed, indicator, plane_cap),
+        st, nlaunch);
+}
+
+void launch_slice_pair(const SliceOperand& A, const SliceOperand& B, int blocked, const Plan* plan, int slices_fixed,
+                       int plane_cap, cudaStream_t st, uint64_t* nlaunch) {
+    const SlicePrep pa = prep_slice(A.v, A.line_max, A.planes, A.pitch, A.plane_stride, blocked, A.scale, plan,
+                                    slices_fixed, 0, plane_cap);
+    const SlicePrep pb = prep_slice(B.v, B.line_max, B.planes, B.pitch, B.plane_stride, blocked, B.scale, plan,
+                                    slices_fixed, 0, plane_cap);
+    static const bool paired = [] {
+        const char* e = getenv("ADPB200_SLICE_PAIR");
+        return !e || atoi(e) != 0;
+    }();
+    if (!paired || !pa.tiles || !pb.tiles || pa.which != 1 || pb.which != 3) {
+        launch_prepped(pa, st, nlaunch);
+        launch_prepped(pb, st, nlaunch);
+        return;
     }
-    const int64_t cap = int64_t(num_sms()) * res[which];
-    const int grid = int(tiles < cap ? tiles : cap);
-    launch_chain(fns[which], dim3(grid), dim3(256), kSliceSmem, st, a);
+    // split the persistent grid in proportion to the tiles (each part at least one CTA)
+    const int64_t cap = int64_t(num_sms()) * slice_resident(4);
+    int64_t ga = pa.tiles, gb = pb.tiles;
+    if (ga + gb > cap) {
+        ga = (cap * pa.tiles + (pa.tiles + pb.tiles) / 2) / (pa.tiles + pb.tiles);
+        ga = ga < 1 ? 1 : (ga > cap - 1 ? cap - 1 : ga);
+        gb = cap - ga;
+        if (ga > pa.tiles) ga = pa.tiles;
+        if (gb > pb.tiles) gb = pb.tiles;
+    }
+    launch_chain(slice_pair_kernel, dim3(unsigned(ga + gb)), dim3(256), kSliceSmem, st, pa.a, pb.a, int(ga));
     ++*nlaunch;
 }
 
