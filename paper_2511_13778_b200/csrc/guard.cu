@@ -228,6 +228,27 @@ __global__ void line_max_t_kernel(const int32_t* __restrict__ bmaxT, int64_t lin
     line_max[line] = mx;
 }
 
+// line_max_t_kernel over A's lines then B's (threads [0, alines) then [alines, alines + blines))
+__global__ void line_max_t_pair_kernel(const int32_t* __restrict__ amaxT, int64_t alines, int32_t* __restrict__ aline,
+                                       const int32_t* __restrict__ bmaxT, int64_t blines, int32_t* __restrict__ bline,
+                                       int64_t blocks) {
+    pdl_enter();
+    int64_t line = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int32_t* src = amaxT;
+    int32_t* out = aline;
+    int64_t stride = alines;
+    if (line >= alines) {
+        line -= alines;
+        if (line >= blines) return;
+        src = bmaxT;
+        out = bline;
+        stride = blines;
+    }
+    int mx = kNegSentinel;
+    for (int64_t b = 0; b < blocks; ++b) mx = max(mx, src[b * stride + line]);
+    out[line] = mx;
+}
+
 __global__ void line_max_kernel(const int32_t* __restrict__ bmax, int64_t lines, int64_t blocks,
                                 int32_t* __restrict__ line_max) {
     pdl_enter();
@@ -572,7 +593,7 @@ int num_sms() {
 
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
-                  uint64_t* nlaunch, int64_t tstride) {
+                  uint64_t* nlaunch, int64_t tstride, int skip_line_max) {
     const int64_t blocks = v.len == 0 ? 0 : (v.len + block_len - 1) / block_len;
     if (tstride <= 0) tstride = v.lines;
     if (v.lines == 0) return;
@@ -598,6 +619,7 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
         }
         ++*nlaunch;
     }
+    if (skip_line_max) return;
     if (transposed) {
         launch_chain(line_max_t_kernel, dim3((unsigned)((v.lines + 255) / 256)), dim3(256), 0, st, bmax, v.lines, blocks, tstride,
                                                                                line_max);
@@ -605,6 +627,15 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
         int lgrid = (int)((v.lines * 32 + 255) / 256);
         launch_chain(line_max_kernel, dim3(lgrid), dim3(256), 0, st, bmax, v.lines, blocks, line_max);
     }
+    ++*nlaunch;
+}
+
+void launch_line_max_t_pair(const int32_t* amaxT, int64_t alines, int32_t* aline, const int32_t* bmaxT,
+                            int64_t blines, int32_t* bline, int64_t blocks, cudaStream_t st, uint64_t* nlaunch) {
+    const int64_t lines = alines + blines;
+    if (lines == 0) return;
+    launch_chain(line_max_t_pair_kernel, dim3((unsigned)((lines + 255) / 256)), dim3(256), 0, st, amaxT, alines, aline,
+                 bmaxT, blines, bline, blocks);
     ++*nlaunch;
 }
 

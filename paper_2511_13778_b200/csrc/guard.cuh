@@ -12,7 +12,11 @@ int num_sms();
 // can write into a larger block-major array.
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
-                  uint64_t* nlaunch, int64_t tstride = 0);
+                  uint64_t* nlaunch, int64_t tstride = 0, int skip_line_max = 0);
+// The line maxima of two transposed statistics arrays (A's and B's, lines x blocks
+// each, line stride = lines) in one launch, for launch_stats(..., skip_line_max = 1).
+void launch_line_max_t_pair(const int32_t* amaxT, int64_t alines, int32_t* aline, const int32_t* bmaxT,
+                            int64_t blines, int32_t* bline, int64_t blocks, cudaStream_t st, uint64_t* nlaunch);
 void launch_scan(const double* a, int64_t count, unsigned long long* counts, int32_t* exc, cudaStream_t st,
                  uint64_t* nlaunch);
 // K2: coarsened ESC over block-major stats (atomicMax into esc_out, which must start at 0).
