@@ -362,10 +362,14 @@ int run_pipeline(adpb200_context* h, const Problem& P, const adpb200_options& o,
     if (!native_only && phase != 2) {
         // both operands' line maxima in one launch after both statistics kernels
         const int pair = P.M > 0 && P.N > 0;
-        if (P.M > 0)
-            launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl, 0, pair);
-        if (P.N > 0)
-            launch_stats(P.b, o.esc_block_len, bmax, bmin, bline, plan->counts + 3, &plan->exc, 2, 1, st, nl, 0, pair);
+        if (pair) {
+            launch_stats_pair(P.a, amax, amin, plan->counts, P.b, bmax, bmin, plan->counts + 3, o.esc_block_len,
+                              &plan->exc, st, nl);
+        } else if (P.M > 0) {
+            launch_stats(P.a, o.esc_block_len, amax, amin, aline, plan->counts, &plan->exc, 1, 1, st, nl);
+        } else if (P.N > 0) {
+            launch_stats(P.b, o.esc_block_len, bmax, bmin, bline, plan->counts + 3, &plan->exc, 2, 1, st, nl);
+        }
         if (pair)
             launch_line_max_t_pair(amax, P.M, aline, bmax, P.N, bline,
                                    P.K == 0 ? 0 : (P.K + o.esc_block_len - 1) / o.esc_block_len, st, nl);

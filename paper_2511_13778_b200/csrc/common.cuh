@@ -58,7 +58,7 @@ struct Plan {
 // launch_dependents lets the next kernel's CTAs be scheduled on the slots this
 // grid leaves free. Since each kernel waits before touching memory, the order
 // of effects is the plain stream order; what the overlap removes is the launch
-// gap between consecutive kernels (11 per call), which dominates calls below
+// gap between consecutive kernels (10 per call), which dominates calls below
 // ~2048^3. The trigger only fires once every CTA of this grid has executed it,
 // so waiting dependents can never take the slots of CTAs not yet started.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }

@@ -96,15 +96,28 @@ __device__ __forceinline__ void flush_counts(int nan, int inf, int negz, unsigne
 
 // Lines contiguous (ps == 1): one warp per (line, block); lanes stride the
 // block so every load instruction is a coalesced 256 B request.
-__global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t block_len, int64_t blocks,
-                                                         int32_t* __restrict__ bmax_out,
-                                                         int32_t* __restrict__ bmin_out,
-                                                         unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit, int transposed, int64_t tstride) {
-    pdl_enter();
+struct StatsArgs {
+    LineView v;
+    int64_t block_len, blocks;
+    int32_t* bmax_out;
+    int32_t* bmin_out;
+    unsigned long long* counts;
+    int32_t* exc_flag;
+    int exc_bit, transposed;
+    int64_t tstride;
+    int groups;  // cols variant only
+};
+
+// rows variant run by CTAs cta = 0..nctas-1
+__device__ __forceinline__ void stats_rows_body(const StatsArgs& A, int64_t cta, int64_t nctas) {
+    const LineView& v = A.v;
+    const int64_t block_len = A.block_len, blocks = A.blocks, tstride = A.tstride;
+    int32_t* __restrict__ bmax_out = A.bmax_out;
+    int32_t* __restrict__ bmin_out = A.bmin_out;
+    const int transposed = A.transposed;
     const int lane = threadIdx.x & 31;
-    const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int64_t warp = (cta * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (nctas * blockDim.x) >> 5;
     int nan = 0, inf = 0, negz = 0;
     const int64_t tasks = v.lines * blocks;
     for (int64_t task = warp; task < tasks; task += nwarps) {
@@ -145,17 +158,23 @@ __global__ void __launch_bounds__(256) stats_rows_kernel(LineView v, int64_t blo
             bmin_out[o] = any ? bmin : kNegSentinel;
         }
     }
-    flush_counts(nan, inf, negz, counts, exc_flag, exc_bit);
+    flush_counts(nan, inf, negz, A.counts, A.exc_flag, A.exc_bit);
+}
+
+__global__ void __launch_bounds__(256) stats_rows_kernel(StatsArgs A) {
+    pdl_enter();
+    stats_rows_body(A, blockIdx.x, gridDim.x);
 }
 
 // Lines adjacent (ls == 1): one thread per (line, block); a warp covers 32
 // consecutive lines so each load is a coalesced 256 B request.
-__global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t block_len, int64_t blocks,
-                                                         int32_t* __restrict__ bmax_out,
-                                                         int32_t* __restrict__ bmin_out,
-                                                         unsigned long long* counts, int32_t* exc_flag,
-                                                         int exc_bit, int transposed, int64_t tstride, int groups) {
-    pdl_enter();
+// cols variant as CTA (bx, by) of a gx x gy grid
+__device__ __forceinline__ void stats_cols_body(const StatsArgs& A, int64_t bx, int64_t by, int64_t gy) {
+    const LineView& v = A.v;
+    const int64_t block_len = A.block_len, blocks = A.blocks, tstride = A.tstride;
+    int32_t* __restrict__ bmax_out = A.bmax_out;
+    int32_t* __restrict__ bmin_out = A.bmin_out;
+    const int transposed = A.transposed, groups = A.groups;
     // 256 / groups adjacent lines x `groups` position groups per CTA: a warp loads a
     // 256-byte coalesced row across 32 lines, and a block's positions are split over
     // the groups (combined through shared memory) when the matrix is too small to
@@ -164,9 +183,9 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
     int nan = 0, inf = 0, negz = 0;
     const int width = 256 / groups;
     const int li = threadIdx.x % width, grp = threadIdx.x / width;
-    const int64_t line = int64_t(blockIdx.x) * width + li;
+    const int64_t line = bx * width + li;
     const int64_t per = (block_len + groups - 1) / groups;
-    for (int64_t blk = blockIdx.y; blk < blocks; blk += gridDim.y) {
+    for (int64_t blk = by; blk < blocks; blk += gy) {
         int bmax = kNegSentinel, bmin = -kNegSentinel;
         if (line < v.lines) {
             const int64_t b0 = blk * block_len, b1 = b0 + block_len < v.len ? b0 + block_len : v.len;
@@ -213,7 +232,21 @@ __global__ void __launch_bounds__(256) stats_cols_kernel(LineView v, int64_t blo
         }
         if (groups > 1) __syncthreads();
     }
-    flush_counts(nan, inf, negz, counts, exc_flag, exc_bit);
+    flush_counts(nan, inf, negz, A.counts, A.exc_flag, A.exc_bit);
+}
+
+__global__ void __launch_bounds__(256) stats_cols_kernel(StatsArgs A) {
+    pdl_enter();
+    stats_cols_body(A, blockIdx.x, blockIdx.y, gridDim.y);
+}
+
+// Both operands' statistics in one launch (A-lines adjacent, B-lines contiguous: the
+// column-major N,N case): CTAs [0, gx*gy) run A's cols grid, the rest B's rows grid.
+__global__ void __launch_bounds__(256) stats_pair_kernel(StatsArgs A, int gx, int gy, StatsArgs B) {
+    pdl_enter();
+    const int64_t ncols = int64_t(gx) * gy, id = blockIdx.x;
+    if (id < ncols) stats_cols_body(A, id % gx, id / gx, gy);
+    else stats_rows_body(B, id - ncols, int64_t(gridDim.x) - ncols);
 }
 
 // line_max[line] = max over the line's block maxima (sentinel is the minimum,
@@ -591,6 +624,43 @@ int num_sms() {
     return sms;
 }
 
+namespace {
+// grid of one operand's statistics kernel: rows (1-D, gx CTAs) or cols (gx x gy)
+struct StatsPlan {
+    StatsArgs args;
+    bool rows;
+    int gx, gy;
+};
+
+StatsPlan plan_stats(const LineView& v, int64_t block_len, int64_t blocks, int32_t* bmax, int32_t* bmin,
+                     unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, int64_t tstride) {
+    StatsPlan p{StatsArgs{v, block_len, blocks, bmax, bmin, counts, exc_flag, exc_bit, transposed, tstride, 1}, false,
+                1, 1};
+    if (v.ps == 1 || v.lines == 1) {
+        // lines of a single row-major line: ps may be anything when len == 1
+        if (v.lines == 1) p.args.v.ls = 0;
+        p.rows = true;
+        const int64_t want = (v.lines * blocks + 7) / 8;
+        const int64_t grid = want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16;
+        p.gx = int(grid < 1 ? 1 : grid);
+    } else {
+        // position groups per (line, block): enough threads to fill the SMs (one group at 8192^2)
+        int groups = 1;
+        while (groups < 8 && v.lines * blocks * groups < int64_t(num_sms()) * 1024) groups *= 2;
+        const int width = 256 / groups;
+        p.args.groups = groups;
+        p.gx = int((v.lines + width - 1) / width);
+        p.gy = int(blocks < 65535 ? blocks : 65535);
+    }
+    return p;
+}
+
+void launch_planned(const StatsPlan& p, cudaStream_t st) {
+    if (p.rows) launch_chain(stats_rows_kernel, dim3(p.gx), dim3(256), 0, st, p.args);
+    else launch_chain(stats_cols_kernel, dim3(p.gx, p.gy), dim3(256), 0, st, p.args);
+}
+}  // namespace
+
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
                   uint64_t* nlaunch, int64_t tstride, int skip_line_max) {
@@ -598,25 +668,8 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
     if (tstride <= 0) tstride = v.lines;
     if (v.lines == 0) return;
     if (blocks > 0) {
-        if (v.ps == 1 || v.lines == 1) {
-            LineView w = v;
-            if (w.lines == 1) w.ls = 0;
-            int64_t tasks = v.lines * blocks;
-            int64_t want = (tasks + 7) / 8;
-            int grid = (int)(want < int64_t(num_sms()) * 16 ? want : int64_t(num_sms()) * 16);
-            if (grid < 1) grid = 1;
-            // lines of a single row-major line: ps may be anything when len == 1
-            launch_chain(stats_rows_kernel, dim3(grid), dim3(256), 0, st, w, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit, transposed, tstride);
-        } else {
-            // position groups per (line, block): enough threads to fill the SMs (one group at 8192^2)
-            int groups = 1;
-            while (groups < 8 && v.lines * blocks * groups < int64_t(num_sms()) * 1024) groups *= 2;
-            const int width = 256 / groups;
-            dim3 grid((unsigned)((v.lines + width - 1) / width), (unsigned)(blocks < 65535 ? blocks : 65535));
-            launch_chain(stats_cols_kernel, grid, dim3(256), 0, st, v, block_len, blocks, bmax, bmin, counts, exc_flag,
-                                                    exc_bit, transposed, tstride, groups);
-        }
+        launch_planned(plan_stats(v, block_len, blocks, bmax, bmin, counts, exc_flag, exc_bit, transposed, tstride),
+                       st);
         ++*nlaunch;
     }
     if (skip_line_max) return;
@@ -628,6 +681,28 @@ void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* 
         launch_chain(line_max_kernel, dim3(lgrid), dim3(256), 0, st, bmax, v.lines, blocks, line_max);
     }
     ++*nlaunch;
+}
+
+void launch_stats_pair(const LineView& va, int32_t* amax, int32_t* amin, unsigned long long* acounts,
+                       const LineView& vb, int32_t* bmax, int32_t* bmin, unsigned long long* bcounts,
+                       int64_t block_len, int32_t* exc_flag, cudaStream_t st, uint64_t* nlaunch) {
+    const int64_t blocks = va.len == 0 ? 0 : (va.len + block_len - 1) / block_len;
+    if (va.lines == 0 || vb.lines == 0 || blocks == 0) return;
+    const StatsPlan pa = plan_stats(va, block_len, blocks, amax, amin, acounts, exc_flag, 1, 1, va.lines);
+    const StatsPlan pb = plan_stats(vb, block_len, blocks, bmax, bmin, bcounts, exc_flag, 2, 1, vb.lines);
+    static const bool paired = [] {
+        const char* e = getenv("ADPB200_STATS_PAIR");
+        return !e || atoi(e) != 0;
+    }();
+    if (paired && !pa.rows && pb.rows) {
+        launch_chain(stats_pair_kernel, dim3(unsigned(int64_t(pa.gx) * pa.gy + pb.gx)), dim3(256), 0, st, pa.args,
+                     pa.gx, pa.gy, pb.args);
+        ++*nlaunch;
+    } else {
+        launch_planned(pa, st);
+        launch_planned(pb, st);
+        *nlaunch += 2;
+    }
 }
 
 void launch_line_max_t_pair(const int32_t* amaxT, int64_t alines, int32_t* aline, const int32_t* bmaxT,

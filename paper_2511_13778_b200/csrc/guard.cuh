@@ -13,6 +13,13 @@ int num_sms();
 void launch_stats(const LineView& v, int64_t block_len, int32_t* bmax, int32_t* bmin, int32_t* line_max,
                   unsigned long long* counts, int32_t* exc_flag, int exc_bit, int transposed, cudaStream_t st,
                   uint64_t* nlaunch, int64_t tstride = 0, int skip_line_max = 0);
+// Statistics of A (exc bit 1) and B (exc bit 2), same K and block length, transposed
+// layout (line stride = lines): one launch in the column-major N,N case
+// (ADPB200_STATS_PAIR, default 1), else two; the line maxima are left to
+// launch_line_max_t_pair.
+void launch_stats_pair(const LineView& va, int32_t* amax, int32_t* amin, unsigned long long* acounts,
+                       const LineView& vb, int32_t* bmax, int32_t* bmin, unsigned long long* bcounts,
+                       int64_t block_len, int32_t* exc_flag, cudaStream_t st, uint64_t* nlaunch);
 // The line maxima of two transposed statistics arrays (A's and B's, lines x blocks
 // each, line stride = lines) in one launch, for launch_stats(..., skip_line_max = 1).
 void launch_line_max_t_pair(const int32_t* amaxT, int64_t alines, int32_t* aline, const int32_t* bmaxT,
